@@ -1,0 +1,353 @@
+"""Benchmark: RRS query-depths/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload config4]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1)
+    python bench.py --impl reference ...                       (CPU reference arm)
+
+Workload (default, BASELINE.json configs[3] / north_star target): halfspace
+depth RRS, n=100k Toeplitz-Gaussian points (reference generator bytes), d=50,
+k=NRandom=20,000 = 1000 directions x 20 refinements, alpha=0.9, RRS seed 1,
+queries = the data points themselves (query index = row index).  One step =
+one batch of B queries per GPU through all 20 refinements; scaling is weak
+(B per GPU fixed).  value = queries of all ranks / max-over-ranks device time.
+
+The FP32 roofline (north_star): FLOPs = 2 n d m per (query, refinement); the
+dominant kernel is contract_kernel<count> (K2), measured with CUDA events on
+the engine stream.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (notion, n, d, k, r, alpha, distribution, batch per GPU)
+    "config1": ("halfspace", 1_000, 5, 1_000, 10, 0.9, "gaussian", 1000),
+    "config2": ("projection", 10_000, 20, 20_000, 20, 0.9, "gaussian", 512),
+    "config3": ("asym_projection", 50_000, 50, 20_000, 20, 0.9, "cauchy", 32),
+    "config4": ("halfspace", 100_000, 50, 20_000, 20, 0.9, "gaussian", 1024),
+}
+WORKLOAD_TEXT = {
+    "config1": "halfspace depth RRS, n=1000 Gaussian, d=5, NRandom=1000, n_refinements=10, all points as queries",
+    "config2": "projection depth RRS (median/MAD), n=10k, d=20, Gaussian, k=20000 x r=20",
+    "config3": "asymmetric projection depth RRS, n=50k, d=50, Cauchy (t, nu=1), k=20000 x r=20",
+    "config4": "halfspace depth RRS, n=100k, d=50, K=1000x20 refinements (k=20000), all n points as queries",
+}
+FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: 148 SMs x 128 FP32 lanes x FMA x 1965 MHz
+
+
+def make_data(dist: str, n: int, d: int) -> np.ndarray:
+    from paper_2506_08262_b200.synthetic import student_t, toeplitz_gaussian
+
+    return toeplitz_gaussian(d, n, seed=0) if dist == "gaussian" else student_t(d, n, 1.0, seed=0)
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+def profile_traffic(workload: str):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        return json.load(open(p)).get(workload, {}).get("contract_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+def cpu_baseline(X, notion, k, r, alpha, budget_queries=None):
+    """The CPU port of the reference (oracle/, kind "port") on this host's
+    cores: a bounded sample of the same workload (one query per thread)."""
+    from oracle import oracle
+
+    oracle.build()
+    cores = os.cpu_count() or 1
+    q = budget_queries or max(cores, 1)
+    Z = X[:q]
+    t0 = time.perf_counter()
+    oracle.depth_batch(Z, X, total_directions=k, refinements=r, shrink=alpha, notion=notion, seed=1,
+                       threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": q / dt, "unit": "query-depths/s", "cores": cores, "kind": "port",
+            "sample": f"{q} in-sample queries (rows 0..{q - 1}) of the same workload, full RRS, "
+                      f"{cores} threads, {dt:.1f} s wall"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, wl):
+    """--impl reference: the reference's CPU algorithm (oracle port) on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    notion, n, d, k, r, alpha, dist, _ = WORKLOADS[wl]
+    X = make_data(dist, n, d)
+    cores = os.cpu_count() or 1
+    from oracle import oracle
+
+    oracle.build()
+    q = cores
+    for _ in range(args.warmup):
+        oracle.depth_batch(X[:1], X, total_directions=k, refinements=r, shrink=alpha, notion=notion, seed=1,
+                           threads=1)
+    times = []
+    for s in range(args.steps):
+        Z = X[(s * q) % n:(s * q) % n + q]
+        t0 = time.perf_counter()
+        oracle.depth_batch(Z, X, total_directions=k, refinements=r, shrink=alpha, notion=notion, seed=1,
+                           threads=cores, q0=(s * q) % n)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = q * args.steps / total
+    line = {
+        "impl": "reference", "metric": "query-depths/s (RRS, all n points)", "value": value,
+        "unit": "query-depths/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generators)",
+        "config": {"workload": WORKLOAD_TEXT[wl], "notion": notion, "n": n, "d": d, "NRandom": k,
+                   "n_refinements": r, "sphcap_shrink": alpha, "queries_per_step": q},
+        "cpu_baseline": {"value": value, "unit": "query-depths/s", "cores": cores, "kind": "port",
+                         "sample": f"{q} queries per step ({cores} threads, {cpu_model()}); warm-up steps "
+                                   "run one query"},
+        "e2e": {"value": value, "unit": "query-depths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="config4", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=0, help="queries per GPU per step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = args.workload
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_08262_b200 as rrs
+    from paper_2506_08262_b200.distributed import depth_sharded_device
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    notion, n, d, k, r, alpha, distn, B = WORKLOADS[wl]
+    if args.batch:
+        B = args.batch
+    m = -(-k // r)
+    cfg = rrs.RrsConfig(total_directions=k, refinements=r, shrink=alpha, notion=notion, seed=1)
+    X = make_data(distn, n, d)
+    eng = rrs.engine(local)
+    stream = torch.cuda.current_stream()
+    eng.set_stream(stream.cuda_stream)
+    eng.set_dataset(X, key="bench")
+    Xd = torch.from_numpy(X).cuda()
+
+    def step_rows(s):
+        start = ((s * world + rank) * B) % n
+        return start, Xd[start:start + B] if start + B <= n else torch.cat([Xd[start:], Xd[: B - (n - start)]])
+
+    total_steps = args.warmup + args.steps
+    inputs = [step_rows(s) for s in range(total_steps)]  # resident in HBM before timing
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def run_step(s):
+        q0, Z = inputs[s]
+        return depth_sharded_device(Z.contiguous(), cfg, q_offset=q0, eng=eng)
+
+    for s in range(args.warmup):
+        run_step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    eng.enable_timing(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches = 0
+    contract_ms = 0.0
+    contract_launches = 0
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush between timed iterations (outside the events)
+        ev[i][0].record(stream)
+        run_step(args.warmup + i)
+        ev[i][1].record(stream)
+        st = eng.stats()  # syncs; per-kernel event times of this step
+        launches += st["kernel_launches"]
+        contract_ms += st["ms_contract_total"]
+        contract_launches += st["contract_launches"]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    eng.enable_timing(False)
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * B * args.steps / (ms_max / 1e3)
+
+    # roofline of the dominant kernel (K2 contraction): algorithmic FLOPs per launch
+    flops_total = 2.0 * n * d * m * r * B * args.steps
+    avg_launch_ms = contract_ms / max(contract_launches, 1)
+    flops_per_launch = flops_total / max(contract_launches, 1)
+    achieved = flops_per_launch / (avg_launch_ms / 1e3) / 1e12
+    traffic = profile_traffic(wl)
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": FP32_NOMINAL_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP32_NOMINAL_TFLOPS, "traffic": traffic,
+                "kernel": "contract_kernel<count>" if notion == "halfspace" else "contract_kernel<store>",
+                "peak_source": "nominal FP32 FFMA (148 SMs x 128 lanes x 2 x 1.965 GHz); MEASURED_PEAKS.json "
+                               "has no FP32 entry",
+                "flops_per_launch": flops_per_launch, "avg_launch_ms": avg_launch_ms,
+                "kernel_share_of_step": contract_ms / ms if ms else None,
+                "hbm_peak_measured_gbs": measured_peaks().get("hbm_gbs")}
+
+    # e2e through the public API with host buffers (H2D of data + queries, D2H of results)
+    e2e = None
+    if not args.no_e2e:
+        from paper_2506_08262_b200.distributed import depth_sharded
+        from paper_2506_08262_b200.solver import depth_batch_arrays
+
+        Zh = [inputs[args.warmup + i][1].cpu().numpy() for i in range(args.steps)]
+        q0s = [inputs[args.warmup + i][0] for i in range(args.steps)]
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            data = rrs.Dataset(X)  # a fresh Dataset: validated and uploaded every call
+            if world > 1:
+                Zall = np.concatenate([Zh[i]] * world)  # every rank passes the full list; shards by rank
+                depth_sharded(Zall, data, cfg)
+            else:
+                depth_batch_arrays(Zh[i], data, cfg, q0=q0s[i])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e2e_s = time.perf_counter() - t0
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * B * args.steps / float(tt.item()), "unit": "query-depths/s",
+               "h2d_bytes_per_step": int(n * d * 8 + B * d * 8),
+               "d2h_bytes_per_step": int(B * (8 + 8 * d + 8)),
+               "api": "paper_2506_08262_b200.depth_batch_arrays -> rrs_depth_batch_host (C ABI)"}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(X, notion, k, r, alpha)
+            cpu["cpu_model"] = cpu_model()
+        line = {
+            "metric": "query-depths/s (RRS, all n points)", "value": value, "unit": "query-depths/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference generators: Toeplitz Gaussian / Student-t seed 0)",
+            "config": {"workload": WORKLOAD_TEXT[wl], "notion": notion, "n": n, "d": d, "NRandom": k,
+                       "n_refinements": r, "directions_per_refinement": m, "sphcap_shrink": alpha,
+                       "queries_per_gpu_per_step": B, "global_batch": B * world, "parallelism": f"query-shard x{world}",
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

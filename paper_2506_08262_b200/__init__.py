@@ -1,0 +1,38 @@
+"""B200-native Refined Random Search (RRS) for projection-based depths
+(arXiv 2506.08262), a drop-in for depthforge's RRS hot path.
+
+depthforge-compatible names (optimizer.py / projection.py / directions.py):
+    RrsConfig, ParallelConfig, Dataset, DimensionMismatch, DepthResult,
+    RefinementRecord, PhaseTimer, depth_batch, refined_random_search,
+    evaluate_directions, simple_random_search, pole_update_rule,
+    generate_batch, Pole, CapSpec, DirectionBatch
+data-depth-style wrappers:
+    halfspace, projection, aprojection (NRandom, n_refinements, sphcap_shrink,
+    solver="refinedrandom")
+
+All compute runs in the sm_100a C-ABI library librrs_b200.so (built in-tree,
+see build.py); there is no CPU fallback.
+"""
+
+from ._lib import Engine, LibraryNotBuilt, device_count, engine, load_library
+from .config import (CapSpec, Dataset, DepthResult, DimensionMismatch, DirectionBatch, NOTIONS,
+                     ParallelConfig, PhaseTimer, Pole, RefinementRecord, RrsConfig)
+from .datadepth import aprojection, halfspace, projection
+from .solver import (depth_batch, depth_batch_arrays, evaluate_directions, evaluate_directions_counts,
+                     generate_batch, pole_update_rule, refined_random_search, simple_random_search)
+
+
+def backend_name() -> str:
+    """_core/__init__.py:25 analogue: the only backend is the B200 library."""
+    return "b200"
+
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CapSpec", "Dataset", "DepthResult", "DimensionMismatch", "DirectionBatch", "Engine",
+    "LibraryNotBuilt", "NOTIONS", "ParallelConfig", "PhaseTimer", "Pole", "RefinementRecord",
+    "RrsConfig", "aprojection", "backend_name", "depth_batch", "depth_batch_arrays", "device_count",
+    "engine", "evaluate_directions", "evaluate_directions_counts", "generate_batch", "halfspace",
+    "load_library", "pole_update_rule", "projection", "refined_random_search", "simple_random_search",
+]

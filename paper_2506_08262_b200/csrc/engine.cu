@@ -1,0 +1,679 @@
+// engine.cu -- the C-ABI (include/rrs_b200.h) and the per-device RRS engine.
+//
+// The engine owns the device-resident dataset (FP32, tile-blocked), a grow-only
+// workspace sized for a batch of queries, and one CUDA stream.  depth_batch
+// runs, per query batch, r refinements of
+//     K1 cap_generate  ->  K2 contract (count | store)  [-> K3 select]  ->  K4 update
+// entirely on device (no host round-trips between refinements), then writes
+// DepthResult fields.  Reference: optimizer.py:145-279.
+#include "common.cuh"
+#include "kernels.h"
+#include "../../include/rrs_b200.h"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace rrs;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(expr)                                                                                \
+    do {                                                                                        \
+        cudaError_t _e = (expr);                                                                \
+        if (_e != cudaSuccess)                                                                  \
+            return fail(RRS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));      \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t need) {
+        if (need <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t want = need + need / 8;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            e = cudaMalloc(&p, need);
+            if (e != cudaSuccess) {
+                p = nullptr;
+                return e;
+            }
+            want = need;
+        }
+        bytes = want;
+        return cudaSuccess;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+int sm_count_of(int device) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    return v;
+}
+
+}  // namespace
+
+struct rrs_engine {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    int64_t ws_limit = 8ll << 30;
+    // dataset
+    DevBuf xb;
+    int64_t n = 0;
+    int d = 0;
+    int64_t tiles = 0;
+    // workspace
+    DevBuf zq, u64, u32, counts, depths, y, pole, reflv, reflmode, dmin, bestcnt;
+    DevBuf tmp_in, tmp_out0, tmp_out1, tmp_out2, tmp_out3;
+    // timing
+    bool timing = false;
+    rrs_stats stats{};
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct Mark {
+        int stage;  // 0 gen, 1 contract, 2 univariate, 3 update
+        size_t a, b;
+    };
+    std::vector<Mark> marks;
+
+    cudaEvent_t next_event() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
+};
+
+namespace {
+
+struct Timer {
+    rrs_engine* e;
+    int stage;
+    size_t a = 0;
+    Timer(rrs_engine* e_, int stage_) : e(e_), stage(stage_) {
+        if (e->timing) {
+            a = e->ev_used;
+            cudaEventRecord(e->next_event(), e->stream);
+        }
+    }
+    ~Timer() {
+        if (e->timing) {
+            size_t b = e->ev_used;
+            cudaEventRecord(e->next_event(), e->stream);
+            e->marks.push_back({stage, a, b});
+        }
+    }
+};
+
+int set_device(rrs_engine* e) {
+    CK(cudaSetDevice(e->device));
+    return RRS_OK;
+}
+
+int validate_cfg(const rrs_config* c) {
+    if (!c) return fail(RRS_ERR_INVALID, "config is null");
+    if (c->refinements < 1 || c->total_directions < c->refinements)
+        return fail(RRS_ERR_INVALID, "need total_directions >= refinements >= 1");
+    if (!(c->shrink > 0.0 && c->shrink < 1.0))
+        return fail(RRS_ERR_INVALID, "shrink factor must lie in (0, 1)");
+    if (c->notion < 0 || c->notion > 2) return fail(RRS_ERR_INVALID, "unknown depth notion");
+    if (c->pole_update < 0 || c->pole_update > 1)
+        return fail(RRS_ERR_INVALID, "unknown pole update mode");
+    if ((c->total_directions + c->refinements - 1) / c->refinements > (int64_t)1 << 24)
+        return fail(RRS_ERR_INVALID, "directions per refinement exceed 2^24");
+    return RRS_OK;
+}
+
+struct Plan {
+    int m, mpad, MB, Qb;
+    int jchunk;  // direction blocks per store launch (projection notions)
+    int tpu, chunks;
+};
+
+Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
+    Plan p{};
+    p.m = m;
+    p.MB = (m + BN - 1) / BN;
+    p.mpad = p.MB * BN;
+    const int64_t d = e->d, n = e->n;
+    int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * d * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 8 +
+                    d * 40 + 64;
+    int64_t budget = e->ws_limit;
+    int64_t qb = 4096;
+    if (notion != RRS_HALFSPACE) {
+        const int64_t ybudget = budget / 2;
+        const int64_t yq = (int64_t)p.mpad * n * 4;
+        if (yq <= ybudget) {
+            p.jchunk = p.MB;
+            int64_t lim = ybudget / yq;
+            if (lim < qb) qb = lim;
+        } else {
+            qb = 1;
+            int64_t jc = ybudget / ((int64_t)BN * n * 4);
+            p.jchunk = (int)(jc < 1 ? 1 : (jc > p.MB ? p.MB : jc));
+        }
+        budget -= (int64_t)qb * p.jchunk * BN * n * 4;
+    } else {
+        p.jchunk = p.MB;
+    }
+    int64_t lim = budget / per_q;
+    if (lim < qb) qb = lim;
+    if (qb > Q) qb = Q;
+    if (qb < 1) qb = 1;
+    p.Qb = (int)qb;
+    // point-tile chunking for load balance: aim for >= 16 units per CTA slot
+    const int64_t target = (int64_t)16 * 2 * e->sms;
+    const int64_t base_units = (int64_t)p.Qb * p.jchunk;
+    int64_t chunks = (target + base_units - 1) / base_units;
+    if (chunks < 1) chunks = 1;
+    if (chunks > e->tiles) chunks = e->tiles;
+    int64_t tpu = (e->tiles + chunks - 1) / chunks;
+    if (tpu < 4 && e->tiles >= 4) tpu = 4;  // amortise the direction-block load
+    p.tpu = (int)tpu;
+    p.chunks = (int)((e->tiles + tpu - 1) / tpu);
+    return p;
+}
+
+int ensure_ws(rrs_engine* e, const Plan& p, int notion) {
+    const size_t Qb = p.Qb, d = e->d;
+    CK(e->zq.ensure(Qb * d * 4));
+    CK(e->u64.ensure(Qb * p.m * d * 8));
+    CK(e->u32.ensure(Qb * p.mpad * d * 4));
+    CK(e->pole.ensure(Qb * d * 8));
+    CK(e->reflv.ensure(Qb * d * 8));
+    CK(e->reflmode.ensure(Qb * 4));
+    CK(e->dmin.ensure(Qb * 8));
+    CK(e->bestcnt.ensure(Qb * 8));
+    if (notion == RRS_HALFSPACE) {
+        CK(e->counts.ensure(Qb * p.mpad * 2 * 4));
+        CK(e->depths.ensure(8));
+    } else {
+        CK(e->counts.ensure(8));
+        CK(e->depths.ensure(Qb * p.m * 8));
+        CK(e->y.ensure(Qb * (size_t)p.jchunk * BN * e->n * 4));
+    }
+    return RRS_OK;
+}
+
+ContractArgs contract_args(rrs_engine* e, const Plan& p, int Qb, int jb0, int jbn) {
+    ContractArgs c{};
+    c.xb = e->xb.as<float>();
+    c.u32 = e->u32.as<float>();
+    c.zq = e->zq.as<float>();
+    c.counts = e->counts.as<int>();
+    c.y = e->y.as<float>();
+    c.n = e->n;
+    c.tiles = e->tiles;
+    c.d = e->d;
+    c.Qb = Qb;
+    c.MB = p.MB;
+    c.jb0 = jb0;
+    c.jbn = jbn;
+    c.m = p.m;
+    c.tiles_per_unit = p.tpu;
+    c.chunks = p.chunks;
+    return c;
+}
+
+// y -> per-direction depths for the projection notions, chunked over direction blocks
+int univariate_from_store(rrs_engine* e, const Plan& p, int Qb, int notion) {
+    for (int jb0 = 0; jb0 < p.MB; jb0 += p.jchunk) {
+        const int jbn = (p.MB - jb0) < p.jchunk ? (p.MB - jb0) : p.jchunk;
+        {
+            Timer t(e, 1);
+            ContractArgs c = contract_args(e, p, Qb, jb0, jbn);
+            CK(launch_contract_store(c, e->stream));
+            e->stats.kernel_launches++;
+            e->stats.contract_launches++;
+        }
+        {
+            Timer t(e, 2);
+            SelectArgs s{};
+            s.y = e->y.as<float>();
+            s.depths = e->depths.as<double>();
+            s.n = e->n;
+            s.Qb = Qb;
+            s.jcount = jbn * BN;
+            s.j0 = jb0 * BN;
+            s.m = p.m;
+            s.notion = notion;
+            CK(launch_select(s, e->stream));
+            e->stats.kernel_launches++;
+        }
+    }
+    return RRS_OK;
+}
+
+void reset_stats(rrs_engine* e) {
+    e->stats = rrs_stats{};
+    e->ev_used = 0;
+    e->marks.clear();
+}
+
+int collect_stats(rrs_engine* e) {
+    if (!e->timing) return RRS_OK;
+    CK(cudaStreamSynchronize(e->stream));
+    for (const auto& mk : e->marks) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e->ev_pool[mk.a], e->ev_pool[mk.b]));
+        switch (mk.stage) {
+            case 0: e->stats.ms_generate += ms; break;
+            case 1:
+                e->stats.ms_contract += ms;
+                e->stats.ms_contract_total += ms;
+                break;
+            case 2: e->stats.ms_univariate += ms; break;
+            default: e->stats.ms_update += ms; break;
+        }
+    }
+    e->marks.clear();
+    e->ev_used = 0;
+    return RRS_OK;
+}
+
+// Core device path: queries_dev (Q x d FP64) -> device outputs.
+int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const rrs_config* cfg,
+                const double* eps_host, double* depth, double* argmin, double* trace,
+                int64_t* mincount) {
+    const int r = cfg->refinements;
+    const int m = (int)((cfg->total_directions + r - 1) / r);  // optimizer.py:64-66
+    std::vector<double> eps(r);
+    for (int l = 0; l < r; ++l)  // optimizer.py:175, HALF_PI = math.pi / 2.0
+        eps[l] = eps_host ? eps_host[l] : (3.141592653589793 / 2.0) * std::pow(cfg->shrink, (double)l);
+    const Plan p = make_plan(e, Q, m, cfg->notion);
+    if (int rc = ensure_ws(e, p, cfg->notion)) return rc;
+    if (cfg->notion == RRS_HALFSPACE)
+        CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.Qb * p.mpad * 2 * 4, e->stream));
+    const int d = e->d;
+    for (int64_t b0 = 0; b0 < Q; b0 += p.Qb) {
+        const int Qb = (int)((Q - b0) < p.Qb ? (Q - b0) : p.Qb);
+        CK(launch_queries_to_f32(zdev + b0 * d, e->zq.as<float>(), (int64_t)Qb * d, e->stream));
+        StateArgs s{e->pole.as<double>(), e->reflv.as<double>(), e->reflmode.as<int>(),
+                    e->dmin.as<double>(), e->bestcnt.as<long long>(), (long long)e->n, Qb, d};
+        CK(launch_state_init(s, e->stream));
+        e->stats.kernel_launches += 2;
+        for (int l = 0; l < r; ++l) {
+            {
+                Timer t(e, 0);
+                GenArgs g{};
+                g.pole = e->pole.as<double>();
+                g.refl_mode = e->reflmode.as<int>();
+                g.refl_v = e->reflv.as<double>();
+                g.u64 = e->u64.as<double>();
+                g.u32 = e->u32.as<float>();
+                g.seed = cfg->seed;
+                g.q0 = q0 + b0;
+                g.refinement = (uint32_t)l;
+                g.eps = eps[l];
+                g.Qb = Qb;
+                g.m = m;
+                g.mpad = p.mpad;
+                g.d = d;
+                CK(launch_cap_generate(g, e->stream));
+                e->stats.kernel_launches++;
+            }
+            if (cfg->notion == RRS_HALFSPACE) {
+                Timer t(e, 1);
+                ContractArgs c = contract_args(e, p, Qb, 0, p.MB);
+                CK(launch_contract_count(c, e->stream));
+                e->stats.kernel_launches++;
+                e->stats.contract_launches++;
+            } else {
+                if (int rc = univariate_from_store(e, p, Qb, cfg->notion)) return rc;
+            }
+            {
+                Timer t(e, 3);
+                UpdateArgs u{};
+                u.counts = e->counts.as<int>();
+                u.depths = e->depths.as<double>();
+                u.u64 = e->u64.as<double>();
+                u.pole = e->pole.as<double>();
+                u.refl_v = e->reflv.as<double>();
+                u.refl_mode = e->reflmode.as<int>();
+                u.dmin = e->dmin.as<double>();
+                u.best_count = e->bestcnt.as<long long>();
+                u.trace = trace ? trace + (size_t)b0 * r * (2 + d) : nullptr;
+                u.n = e->n;
+                u.eps = eps[l];
+                u.Qb = Qb;
+                u.m = m;
+                u.mpad = p.mpad;
+                u.d = d;
+                u.r = r;
+                u.refinement = l;
+                u.notion = cfg->notion;
+                CK(launch_update(u, e->stream));
+                e->stats.kernel_launches++;
+            }
+        }
+        FinalArgs f{e->pole.as<double>(), e->dmin.as<double>(), e->bestcnt.as<long long>(),
+                    depth + b0, argmin ? argmin + (size_t)b0 * d : nullptr,
+                    mincount ? (long long*)mincount + b0 : nullptr, Qb, d};
+        CK(launch_finalize(f, e->stream));
+        e->stats.kernel_launches++;
+    }
+    return RRS_OK;
+}
+
+int check_dataset(const rrs_engine* e) {
+    if (!e) return fail(RRS_ERR_INVALID, "engine is null");
+    if (e->n < 1 || e->d < 1) return fail(RRS_ERR_STATE, "no dataset set");
+    return RRS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rrs_abi_version(void) { return RRS_ABI_VERSION; }
+
+const char* rrs_last_error(void) { return g_err.c_str(); }
+
+int rrs_device_count(int32_t* count) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    if (count) *count = c;
+    return RRS_OK;
+}
+
+int rrs_engine_create(int32_t device, rrs_engine** out) {
+    if (!out) return fail(RRS_ERR_INVALID, "out is null");
+    *out = nullptr;
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess || c == 0) {
+        cudaGetLastError();
+        return fail(RRS_ERR_CUDA, "no CUDA device visible (the B200 path has no CPU fallback)");
+    }
+    if (device < 0 || device >= c) return fail(RRS_ERR_INVALID, "device index out of range");
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(RRS_ERR_CUDA, std::string("device is not sm_100 (found ") + prop.name + ")");
+    rrs_engine* e = new rrs_engine();
+    e->device = device;
+    e->sms = sm_count_of(device);
+    cudaError_t ce = cudaSetDevice(device);
+    if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking);
+    if (ce != cudaSuccess) {
+        delete e;
+        return fail(RRS_ERR_CUDA, std::string("stream create: ") + cudaGetErrorString(ce));
+    }
+    e->stream = e->own;
+    *out = e;
+    return RRS_OK;
+}
+
+int rrs_engine_destroy(rrs_engine* e) {
+    if (!e) return RRS_OK;
+    cudaSetDevice(e->device);
+    cudaStreamSynchronize(e->stream);
+    for (DevBuf* b : {&e->xb, &e->zq, &e->u64, &e->u32, &e->counts, &e->depths, &e->y, &e->pole,
+                      &e->reflv, &e->reflmode, &e->dmin, &e->bestcnt, &e->tmp_in, &e->tmp_out0,
+                      &e->tmp_out1, &e->tmp_out2, &e->tmp_out3})
+        b->release();
+    for (auto ev : e->ev_pool) cudaEventDestroy(ev);
+    if (e->own) cudaStreamDestroy(e->own);
+    delete e;
+    return RRS_OK;
+}
+
+int rrs_engine_set_stream(rrs_engine* e, void* stream) {
+    if (!e) return fail(RRS_ERR_INVALID, "engine is null");
+    e->stream = stream ? static_cast<cudaStream_t>(stream) : e->own;
+    return RRS_OK;
+}
+
+int rrs_engine_synchronize(rrs_engine* e) {
+    if (!e) return fail(RRS_ERR_INVALID, "engine is null");
+    if (int rc = set_device(e)) return rc;
+    CK(cudaStreamSynchronize(e->stream));
+    return RRS_OK;
+}
+
+int rrs_engine_set_workspace_limit(rrs_engine* e, int64_t bytes) {
+    if (!e) return fail(RRS_ERR_INVALID, "engine is null");
+    if (bytes < (1 << 20)) return fail(RRS_ERR_INVALID, "workspace limit below 1 MiB");
+    e->ws_limit = bytes;
+    return RRS_OK;
+}
+
+int rrs_engine_enable_timing(rrs_engine* e, int32_t on) {
+    if (!e) return fail(RRS_ERR_INVALID, "engine is null");
+    e->timing = on != 0;
+    return RRS_OK;
+}
+
+int rrs_engine_stats(rrs_engine* e, rrs_stats* out) {
+    if (!e || !out) return fail(RRS_ERR_INVALID, "null argument");
+    if (int rc = set_device(e)) return rc;
+    if (int rc = collect_stats(e)) return rc;
+    *out = e->stats;
+    return RRS_OK;
+}
+
+static int set_dataset_common(rrs_engine* e, const double* xdev, int64_t n, int32_t d) {
+    if (d > MAX_D)
+        return fail(RRS_ERR_INVALID, "dimension " + std::to_string(d) + " exceeds the supported maximum " +
+                                         std::to_string(MAX_D));
+    const int64_t tiles = (n + BM - 1) / BM;
+    CK(e->xb.ensure((size_t)tiles * d * BM * 4));
+    CK(launch_block_dataset(xdev, e->xb.as<float>(), n, d, tiles, e->stream));
+    e->n = n;
+    e->d = d;
+    e->tiles = tiles;
+    return RRS_OK;
+}
+
+int rrs_set_dataset_host(rrs_engine* e, const double* x, int64_t n, int32_t d) {
+    if (!e || !x) return fail(RRS_ERR_INVALID, "null argument");
+    if (n < 1 || d < 1) return fail(RRS_ERR_INVALID, "dataset must be a non-empty 2-D matrix");
+    for (int64_t i = 0; i < n * (int64_t)d; ++i) {
+        if (!std::isfinite(x[i])) return fail(RRS_ERR_INVALID, "dataset contains non-finite entries");
+        if (std::fabs(x[i]) > 1.0e38)
+            return fail(RRS_ERR_INVALID, "dataset entries exceed the FP32 contraction range (|x| > 1e38)");
+    }
+    if (int rc = set_device(e)) return rc;
+    CK(e->tmp_in.ensure((size_t)n * d * 8));
+    CK(cudaMemcpyAsync(e->tmp_in.p, x, (size_t)n * d * 8, cudaMemcpyHostToDevice, e->stream));
+    int rc = set_dataset_common(e, e->tmp_in.as<double>(), n, d);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(e->stream));
+    return RRS_OK;
+}
+
+int rrs_set_dataset_device(rrs_engine* e, const double* x_dev, int64_t n, int32_t d) {
+    if (!e || !x_dev) return fail(RRS_ERR_INVALID, "null argument");
+    if (n < 1 || d < 1) return fail(RRS_ERR_INVALID, "dataset must be a non-empty 2-D matrix");
+    if (int rc = set_device(e)) return rc;
+    return set_dataset_common(e, x_dev, n, d);
+}
+
+int rrs_depth_batch_device(rrs_engine* e, const double* queries_dev, int64_t Q, int64_t q0,
+                           const rrs_config* cfg, const double* eps, double* depth_dev,
+                           double* argmin_dev, double* trace_dev, int64_t* min_count_dev) {
+    if (int rc = check_dataset(e)) return rc;
+    if (int rc = validate_cfg(cfg)) return rc;
+    if (Q < 0) return fail(RRS_ERR_INVALID, "negative query count");
+    if (Q == 0) return RRS_OK;
+    if (!queries_dev || !depth_dev) return fail(RRS_ERR_INVALID, "null argument");
+    if (int rc = set_device(e)) return rc;
+    reset_stats(e);
+    return run_batches(e, queries_dev, Q, q0, cfg, eps, depth_dev, argmin_dev, trace_dev, min_count_dev);
+}
+
+int rrs_depth_batch_host(rrs_engine* e, const double* queries, int64_t Q, int64_t q0,
+                         const rrs_config* cfg, const double* eps, double* depth, double* argmin,
+                         double* trace, int64_t* min_count) {
+    if (int rc = check_dataset(e)) return rc;
+    if (int rc = validate_cfg(cfg)) return rc;
+    if (Q < 0) return fail(RRS_ERR_INVALID, "negative query count");
+    if (Q == 0) return RRS_OK;
+    if (!queries || !depth) return fail(RRS_ERR_INVALID, "null argument");
+    if (int rc = set_device(e)) return rc;
+    reset_stats(e);
+    const int d = e->d, r = cfg->refinements;
+    const size_t zb = (size_t)Q * d * 8;
+    CK(e->tmp_in.ensure(zb));
+    CK(e->tmp_out0.ensure((size_t)Q * 8));
+    CK(e->tmp_out1.ensure((size_t)Q * d * 8));
+    if (trace) CK(e->tmp_out2.ensure((size_t)Q * r * (2 + d) * 8));
+    CK(e->tmp_out3.ensure((size_t)Q * 8));
+    CK(cudaMemcpyAsync(e->tmp_in.p, queries, zb, cudaMemcpyHostToDevice, e->stream));
+    int rc = run_batches(e, e->tmp_in.as<double>(), Q, q0, cfg, eps, e->tmp_out0.as<double>(),
+                         e->tmp_out1.as<double>(), trace ? e->tmp_out2.as<double>() : nullptr,
+                         e->tmp_out3.as<int64_t>());
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(depth, e->tmp_out0.p, (size_t)Q * 8, cudaMemcpyDeviceToHost, e->stream));
+    if (argmin)
+        CK(cudaMemcpyAsync(argmin, e->tmp_out1.p, (size_t)Q * d * 8, cudaMemcpyDeviceToHost, e->stream));
+    if (trace)
+        CK(cudaMemcpyAsync(trace, e->tmp_out2.p, (size_t)Q * r * (2 + d) * 8, cudaMemcpyDeviceToHost,
+                           e->stream));
+    if (min_count)
+        CK(cudaMemcpyAsync(min_count, e->tmp_out3.p, (size_t)Q * 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    return RRS_OK;
+}
+
+int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U, int32_t m,
+                                 int32_t notion, double* out, int64_t* cle, int64_t* cge) {
+    if (int rc = check_dataset(e)) return rc;
+    if (!z || !U || !out) return fail(RRS_ERR_INVALID, "null argument");
+    if (m < 1) return fail(RRS_ERR_INVALID, "batch size must be >= 1");
+    if (notion < 0 || notion > 2) return fail(RRS_ERR_INVALID, "unknown depth notion");
+    if (int rc = set_device(e)) return rc;
+    reset_stats(e);
+    const int d = e->d;
+    Plan p = make_plan(e, 1, m, notion);
+    if (int rc = ensure_ws(e, p, notion)) return rc;
+    CK(e->tmp_in.ensure((size_t)d * 8));
+    CK(cudaMemcpyAsync(e->u64.p, U, (size_t)m * d * 8, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(e->tmp_in.p, z, (size_t)d * 8, cudaMemcpyHostToDevice, e->stream));
+    CK(launch_queries_to_f32(e->tmp_in.as<double>(), e->zq.as<float>(), d, e->stream));
+    CK(launch_pack_directions(e->u64.as<double>(), e->u32.as<float>(), 1, m, p.mpad, d, e->stream));
+    if (notion == RRS_HALFSPACE) {
+        CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.mpad * 2 * 4, e->stream));
+        ContractArgs c = contract_args(e, p, 1, 0, p.MB);
+        CK(launch_contract_count(c, e->stream));
+        std::vector<int> cnt((size_t)p.mpad * 2);
+        CK(cudaMemcpyAsync(cnt.data(), e->counts.p, cnt.size() * 4, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        const int64_t n = e->n;
+        for (int j = 0; j < m; ++j) {
+            const int64_t lt = cnt[2 * j], gt = cnt[2 * j + 1];
+            const int64_t le = n - gt, ge = n - lt;  // ties (y == 0) on both sides
+            if (cle) cle[j] = le;
+            if (cge) cge[j] = ge;
+            out[j] = (double)(le < ge ? le : ge) / (double)n;  // _kernels.pyx:288-289
+        }
+        return RRS_OK;
+    }
+    if (int rc = univariate_from_store(e, p, 1, notion)) return rc;
+    CK(cudaMemcpyAsync(out, e->depths.p, (size_t)m * 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    return RRS_OK;
+}
+
+int rrs_cap_directions_host(rrs_engine* e, const double* pole, int32_t d, double eps, int32_t m,
+                            uint64_t seed, uint32_t refinement, uint32_t query, double* U) {
+    if (!e || !pole || !U) return fail(RRS_ERR_INVALID, "null argument");
+    if (m < 1) return fail(RRS_ERR_INVALID, "batch size must be >= 1");
+    if (d < 1 || d > GEN_MAX_D) return fail(RRS_ERR_INVALID, "dimension out of range");
+    if (!(eps > 0.0 && eps <= 3.141592653589793 / 2 + 1e-15))
+        return fail(RRS_ERR_INVALID, "cap half-angle must lie in (0, pi/2]");
+    if (int rc = set_device(e)) return rc;
+    // reflect_to_pole vector, directions.py:150-164 (same arithmetic as update_kernel)
+    std::vector<double> v(d, 0.0);
+    int mode = 0;
+    const double p1 = pole[0];
+    if (1.0 - p1 < 1e-12) mode = 0;
+    else if (1.0 + p1 < 1e-12) mode = 1;
+    else {
+        mode = 2;
+        for (int c = 0; c < d; ++c) v[c] = -pole[c];
+        v[0] += 1.0;
+        double ss = 0.0;
+        for (int c = 0; c < d; ++c) ss += v[c] * v[c];
+        const double vn = std::sqrt(ss);
+        for (int c = 0; c < d; ++c) v[c] /= vn;
+    }
+    const int mpad = ((m + BN - 1) / BN) * BN;
+    DevBuf pb, vb, mb, ub, u32b;
+    CK(pb.ensure((size_t)d * 8));
+    CK(vb.ensure((size_t)d * 8));
+    CK(mb.ensure(4));
+    CK(ub.ensure((size_t)m * d * 8));
+    CK(u32b.ensure((size_t)mpad * d * 4));
+    CK(cudaMemcpyAsync(pb.p, pole, (size_t)d * 8, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(vb.p, v.data(), (size_t)d * 8, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(mb.p, &mode, 4, cudaMemcpyHostToDevice, e->stream));
+    GenArgs g{};
+    g.pole = pb.as<double>();
+    g.refl_mode = mb.as<int>();
+    g.refl_v = vb.as<double>();
+    g.u64 = ub.as<double>();
+    g.u32 = u32b.as<float>();
+    g.seed = seed;
+    g.q0 = query;
+    g.refinement = refinement;
+    g.eps = eps;
+    g.Qb = 1;
+    g.m = m;
+    g.mpad = mpad;
+    g.d = d;
+    CK(launch_cap_generate(g, e->stream));
+    CK(cudaMemcpyAsync(U, ub.p, (size_t)m * d * 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    for (DevBuf* b : {&pb, &vb, &mb, &ub, &u32b}) b->release();
+    return RRS_OK;
+}
+
+int rrs_philox4x32_host(rrs_engine* e, const uint32_t* ctr, int64_t N, uint32_t key0, uint32_t key1,
+                        uint32_t* out) {
+    if (!e || !ctr || !out) return fail(RRS_ERR_INVALID, "null argument");
+    if (N < 0) return fail(RRS_ERR_INVALID, "negative count");
+    if (N == 0) return RRS_OK;
+    if (int rc = set_device(e)) return rc;
+    DevBuf a, b;
+    CK(a.ensure((size_t)N * 16));
+    CK(b.ensure((size_t)N * 16));
+    CK(cudaMemcpyAsync(a.p, ctr, (size_t)N * 16, cudaMemcpyHostToDevice, e->stream));
+    CK(launch_philox_words(a.as<uint32_t>(), b.as<uint32_t>(), N, key0, key1, e->stream));
+    CK(cudaMemcpyAsync(out, b.p, (size_t)N * 16, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    a.release();
+    b.release();
+    return RRS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,469 @@
+// gen.cu -- FP64 kernels: Philox spherical-cap direction generation, RRS state
+// (init / argmin + pole update / reflection vector / trace), layout conversion.
+//
+// Compiled with -fmad=false: the FP64 arithmetic here restates the reference's
+// numpy/C operation sequence (no contraction), so device directions track the
+// reference rows to a few ulp (CUDA vs glibc cos/log are the only differences).
+#include "common.cuh"
+#include "kernels.h"
+
+#include <math.h>
+
+namespace rrs {
+
+// ------------------------------------------------------------------ Philox --
+// Philox-4x32-10: philox.py:27-65 / _kernels.pyx:24-61.
+__device__ __forceinline__ void philox10(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
+                                         uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint32_t hi0 = __umulhi(c0, 0xD2511F53u), lo0 = c0 * 0xD2511F53u;
+        uint32_t hi1 = __umulhi(c2, 0xCD9E8D57u), lo1 = c2 * 0xCD9E8D57u;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+// philox.py:88-114: counter (v, j, l, q), key = seed lo/hi words, 53-bit mantissa.
+__device__ __forceinline__ double uniform1(uint64_t seed, uint32_t v, uint32_t j, uint32_t l,
+                                           uint32_t q) {
+    uint32_t c0 = v, c1 = j, c2 = l, c3 = q;
+    philox10(c0, c1, c2, c3, (uint32_t)seed, (uint32_t)(seed >> 32));
+    uint64_t bits = (uint64_t)c0 | ((uint64_t)c1 << 32);
+    return ((double)(bits >> 11) + 0.5) * 0x1.0p-53;
+}
+
+// ------------------------------------------------------------------- ndtri --
+// Inverse normal CDF, Cephes algorithm (scipy.special.ndtri, scipy 1.18.1);
+// Q* tables evaluated with an implicit leading 1 (p1evl).
+__constant__ double c_P0[5] = {-5.99633501014107895267E1, 9.80010754185999661536E1,
+                               -5.66762857469070293439E1, 1.39312609387279679503E1,
+                               -1.23916583867381258016E0};
+__constant__ double c_Q0[8] = {1.95448858338141759834E0,  4.67627912898881538453E0,
+                               8.63602421390890590575E1,  -2.25462687854119370527E2,
+                               2.00260212380060660359E2,  -8.20372256168333339912E1,
+                               1.59056225126211695515E1,  -1.18331621121330003142E0};
+__constant__ double c_P1[9] = {4.05544892305962419923E0,   3.15251094599893866154E1,
+                               5.71628192246421288162E1,   4.40805073893200834700E1,
+                               1.46849561928858024014E1,   2.18663306850790267539E0,
+                               -1.40256079171354495875E-1, -3.50424626827848203418E-2,
+                               -8.57456785154685413611E-4};
+__constant__ double c_Q1[8] = {1.57799883256466749731E1,   4.53907635128879210584E1,
+                               4.13172038254672030440E1,   1.50425385692907503408E1,
+                               2.50464946208309415979E0,   -1.42182922854787788574E-1,
+                               -3.80806407691578277194E-2, -9.33259480895457427372E-4};
+__constant__ double c_P2[9] = {3.23774891776946035970E0,  6.91522889068984211695E0,
+                               3.93881025292474443415E0,  1.33303460815807542389E0,
+                               2.01485389549179081538E-1, 1.23716634817820021358E-2,
+                               3.01581553508235416007E-4, 2.65806974686737550832E-6,
+                               6.23974539184983293730E-9};
+__constant__ double c_Q2[8] = {6.02427039364742014255E0,  3.67983563856160859403E0,
+                               1.37702099489081330271E0,  2.16236993594496635890E-1,
+                               1.34204006088543189037E-2, 3.28014464682127739104E-4,
+                               2.89247864745380683936E-6, 6.79019408009981274425E-9};
+
+__device__ __forceinline__ double polevl(double x, const double* c, int deg) {
+    double a = c[0];
+    for (int i = 1; i <= deg; ++i) a = a * x + c[i];
+    return a;
+}
+__device__ __forceinline__ double p1evl(double x, const double* c, int deg) {
+    double a = x + c[0];
+    for (int i = 1; i < deg; ++i) a = a * x + c[i];
+    return a;
+}
+
+__device__ double ndtri(double y0) {
+    const double s2pi = 2.50662827463100050242E0;
+    const double e2 = 0.13533528323661269189;  // exp(-2)
+    bool negate = true;
+    double y = y0;
+    if (y > 1.0 - e2) {
+        y = 1.0 - y;
+        negate = false;
+    }
+    if (y > e2) {
+        y = y - 0.5;
+        double y2 = y * y;
+        double x = y + y * (y2 * polevl(y2, c_P0, 4) / p1evl(y2, c_Q0, 8));
+        return x * s2pi;
+    }
+    double x = sqrt(-2.0 * log(y));
+    double x0 = x - log(x) / x;
+    double z = 1.0 / x;
+    double x1 = (x < 8.0) ? z * polevl(z, c_P1, 8) / p1evl(z, c_Q1, 8)
+                          : z * polevl(z, c_P2, 8) / p1evl(z, c_Q2, 8);
+    x = x0 - x1;
+    return negate ? -x : x;
+}
+
+// numpy float64 add.reduce over a contiguous row = 0.0 + pairwise sum
+// (8 running partials up to 128 elements, halving at multiples of 8 beyond).
+__device__ double pw_rec(const double* a, int n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int i = 0; i < n; ++i) r += a[i];
+        return r;
+    }
+    if (n <= 128) {
+        double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6],
+               r7 = a[7];
+        int i = 8;
+        for (; i < n - (n % 8); i += 8) {
+            r0 += a[i];
+            r1 += a[i + 1];
+            r2 += a[i + 2];
+            r3 += a[i + 3];
+            r4 += a[i + 4];
+            r5 += a[i + 5];
+            r6 += a[i + 6];
+            r7 += a[i + 7];
+        }
+        double res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return pw_rec(a, n2) + pw_rec(a + n2, n - n2);
+}
+
+__device__ __forceinline__ double pw_sum(const double* a, int n) { return 0.0 + pw_rec(a, n); }
+
+// ------------------------------------------------------- cap generation K1 --
+// directions.py:167-182 (_cap_rows) for every (query, direction): one warp per
+// direction.  theta = U(v=0,j)*eps; d-1 normals from v = 1..d-1 (zero-norm
+// rows redrawn from the next d-1 addresses, directions.py:113-135); row =
+// [cos theta, sqrt(1-cos^2)*g/|g|]; Householder e1 -> pole with the per-query
+// reflection vector prepared by the update kernel (directions.py:150-164).
+// Writes U64[q][j][d] (pole candidates) and U32[q][jb][d][BN] (contraction
+// operand, FP32, K-major per direction block); padded directions j >= m get 0.
+__global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
+    extern __shared__ double gsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int d = a.d;
+    double* g = gsm + (size_t)warp * 2 * d;  // d values + d scratch
+    double* sc = g + d;
+    const int64_t gdir = (int64_t)blockIdx.x * 8 + warp;  // over Qb * mpad
+    const int64_t total = (int64_t)a.Qb * a.mpad;
+    if (gdir >= total) return;
+    const int q = (int)(gdir / a.mpad);
+    const int j = (int)(gdir % a.mpad);
+    float* u32 = a.u32 + (size_t)q * a.mpad * d + (size_t)(j / BN) * d * BN + (j % BN);
+    if (j >= a.m) {
+        for (int c = lane; c < d; c += 32) u32[(size_t)c * BN] = 0.0f;
+        return;
+    }
+    const uint32_t qg = (uint32_t)((uint64_t)(a.q0 + q) & 0xFFFFFFFFu);
+    const uint32_t l = a.refinement;
+    const double* pole = a.pole + (size_t)q * d;
+    double* u64 = a.u64 + ((size_t)q * a.m + j) * d;
+    if (d == 1) {  // directions.py:172-173
+        if (lane == 0) {
+            u64[0] = pole[0];
+            u32[0] = (float)pole[0];
+        }
+        return;
+    }
+    const int dm = d - 1;
+    double u1 = 0.0;
+    if (lane == 0) u1 = cos(uniform1(a.seed, 0u, (uint32_t)j, l, qg) * a.eps);
+    uint32_t vbase = 1;
+    double nrm;
+    for (;;) {
+        for (int c = lane; c < dm; c += 32) {
+            double gv = ndtri(uniform1(a.seed, vbase + (uint32_t)c, (uint32_t)j, l, qg));
+            g[c] = gv;
+            sc[c] = gv * gv;
+        }
+        __syncwarp();
+        if (lane == 0) nrm = sqrt(pw_sum(sc, dm));
+        nrm = __shfl_sync(0xffffffffu, nrm, 0);
+        __syncwarp();
+        if (nrm != 0.0) break;
+        vbase += (uint32_t)dm;
+    }
+    u1 = __shfl_sync(0xffffffffu, u1, 0);
+    const double s = sqrt(1.0 - u1 * u1);
+    // row stored in sc[0..d): sc[0] = u1, sc[1+c] = s * (g[c]/nrm)
+    __syncwarp();
+    for (int c = lane; c < dm; c += 32) g[c] = s * (g[c] / nrm);
+    __syncwarp();
+    for (int c = lane; c < dm; c += 32) sc[1 + c] = g[c];
+    if (lane == 0) sc[0] = u1;
+    __syncwarp();
+    const int mode = a.refl_mode[q];
+    if (mode == 1) {
+        if (lane == 0) sc[0] = -sc[0];
+        __syncwarp();
+    } else if (mode == 2) {
+        const double* v = a.refl_v + (size_t)q * d;
+        for (int c = lane; c < d; c += 32) g[c] = sc[c] * v[c];
+        __syncwarp();
+        double f = 0.0;
+        if (lane == 0) f = 2.0 * pw_sum(g, d);
+        f = __shfl_sync(0xffffffffu, f, 0);
+        for (int c = lane; c < d; c += 32) sc[c] = sc[c] - f * v[c];
+        __syncwarp();
+    }
+    for (int c = lane; c < d; c += 32) {
+        double val = sc[c];
+        u64[c] = val;
+        u32[(size_t)c * BN] = (float)val;
+    }
+}
+
+// Explicit-direction mode: U64 given; build the FP32 contraction operand.
+__global__ void pack_directions_kernel(const double* __restrict__ u64, float* __restrict__ u32, int Qb,
+                                       int m, int mpad, int d) {
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = (int64_t)Qb * mpad * d;
+    if (idx >= total) return;
+    int c = (int)(idx % d);
+    int64_t r = idx / d;
+    int j = (int)(r % mpad);
+    int q = (int)(r / mpad);
+    float v = (j < m) ? (float)u64[((size_t)q * m + j) * d + c] : 0.0f;
+    u32[(size_t)q * mpad * d + (size_t)(j / BN) * d * BN + (size_t)c * BN + (j % BN)] = v;
+}
+
+// ------------------------------------------------------------- RRS state --
+// optimizer.py:164-167: pole = e1, d_min = 1.0, argmin = e1.
+__global__ void state_init_kernel(StateArgs s) {
+    int q = blockIdx.x;
+    if (q >= s.Qb) return;
+    for (int c = threadIdx.x; c < s.d; c += blockDim.x) {
+        s.pole[(size_t)q * s.d + c] = (c == 0) ? 1.0 : 0.0;
+        s.refl_v[(size_t)q * s.d + c] = 0.0;
+    }
+    if (threadIdx.x == 0) {
+        s.dmin[q] = 1.0;
+        s.best_count[q] = s.n;
+        s.refl_mode[q] = 0;  // pole == e1: 1 - p1 < 1e-12, no reflection
+    }
+}
+
+// Per-query argmin over the refinement's m directions (np.argmin: first index
+// of the minimum), strict-< pole update against d_min (optimizer.py:200-205;
+// the per_direction branch :206-218 ends on the same direction), trace record
+// (optimizer.py:219) and the Householder vector of the new pole for the next
+// refinement (directions.py:150-164).  Halfspace reads integer (#<, #>) counts,
+// min count = n - max(lt, gt); the projection notions read FP64 depths.
+// Also clears the halfspace counters for the next refinement.
+__global__ void __launch_bounds__(256) update_kernel(UpdateArgs a) {
+    const int q = blockIdx.x;
+    if (q >= a.Qb) return;
+    __shared__ double s_val[8];
+    __shared__ long long s_cnt[8];
+    __shared__ int s_idx[8];
+    __shared__ int s_best;
+    __shared__ int s_improved;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int d = a.d;
+    double bval = INFINITY;
+    long long bcnt = 0;
+    int bidx = 0x7fffffff;
+    if (a.notion == 0) {
+        const int* cnt = a.counts + (size_t)q * a.mpad * 2;
+        for (int j = tid; j < a.m; j += blockDim.x) {
+            long long lt = cnt[2 * j], gt = cnt[2 * j + 1];
+            long long c = a.n - (lt > gt ? lt : gt);
+            double v = (double)c / (double)a.n;
+            if (v < bval) {
+                bval = v;
+                bcnt = c;
+                bidx = j;
+            }
+        }
+    } else {
+        const double* dep = a.depths + (size_t)q * a.m;
+        for (int j = tid; j < a.m; j += blockDim.x) {
+            double v = dep[j];
+            if (v < bval) {
+                bval = v;
+                bidx = j;
+            }
+        }
+    }
+    // lexicographic (value, index) min
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, bval, off);
+        long long oc = __shfl_xor_sync(0xffffffffu, bcnt, off);
+        int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+        if (ov < bval || (ov == bval && oi < bidx)) {
+            bval = ov;
+            bcnt = oc;
+            bidx = oi;
+        }
+    }
+    if (lane == 0) {
+        s_val[warp] = bval;
+        s_cnt[warp] = bcnt;
+        s_idx[warp] = bidx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+            if (s_val[w] < bval || (s_val[w] == bval && s_idx[w] < bidx)) {
+                bval = s_val[w];
+                bcnt = s_cnt[w];
+                bidx = s_idx[w];
+            }
+        int improved = 0;
+        if (bval < a.dmin[q]) {
+            a.dmin[q] = bval;
+            a.best_count[q] = bcnt;
+            improved = 1;
+        }
+        s_best = bidx;
+        s_improved = improved;
+    }
+    __syncthreads();
+    double* pole = a.pole + (size_t)q * d;
+    if (s_improved) {
+        const double* src = a.u64 + ((size_t)q * a.m + s_best) * d;
+        for (int c = tid; c < d; c += blockDim.x) pole[c] = src[c];
+    }
+    __syncthreads();
+    if (a.trace) {
+        double* rec = a.trace + ((size_t)q * a.r + a.refinement) * (2 + d);
+        for (int c = tid; c < d; c += blockDim.x) rec[2 + c] = pole[c];
+        if (tid == 0) {
+            rec[0] = a.dmin[q];
+            rec[1] = a.eps;
+        }
+    }
+    // reflection vector for the next refinement's cap (reflect_to_pole)
+    if (s_improved && tid == 0) {
+        const double p1 = pole[0];
+        double* v = a.refl_v + (size_t)q * d;
+        int mode;
+        if (1.0 - p1 < 1e-12) mode = 0;
+        else if (1.0 + p1 < 1e-12) mode = 1;
+        else {
+            mode = 2;
+            for (int c = 0; c < d; ++c) v[c] = -pole[c];
+            v[0] += 1.0;
+            double ss = 0.0;
+            for (int c = 0; c < d; ++c) ss += v[c] * v[c];
+            double vn = sqrt(ss);
+            for (int c = 0; c < d; ++c) v[c] /= vn;
+        }
+        a.refl_mode[q] = mode;
+    }
+    if (a.notion == 0) {
+        int* cnt = a.counts + (size_t)q * a.mpad * 2;
+        for (int j = tid; j < a.mpad * 2; j += blockDim.x) cnt[j] = 0;
+    }
+}
+
+// DepthResult outputs for queries [0, Qb) of the batch.
+__global__ void finalize_kernel(FinalArgs f) {
+    int q = blockIdx.x;
+    if (q >= f.Qb) return;
+    for (int c = threadIdx.x; c < f.d; c += blockDim.x)
+        if (f.argmin_out) f.argmin_out[(size_t)q * f.d + c] = f.pole[(size_t)q * f.d + c];
+    if (threadIdx.x == 0) {
+        f.depth_out[q] = f.dmin[q];
+        if (f.count_out) f.count_out[q] = f.best_count[q];
+    }
+}
+
+// ---------------------------------------------------------- data layouts --
+// Dataset n x d FP64 row-major -> FP32 tile-blocked [T][d][BM]; pad rows 0.
+__global__ void block_dataset_kernel(const double* __restrict__ x, float* __restrict__ xb, int64_t n,
+                                     int d, int64_t tiles) {
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = tiles * d * BM;
+    if (idx >= total) return;
+    int i = (int)(idx % BM);
+    int64_t r = idx / BM;
+    int c = (int)(r % d);
+    int64_t t = r / d;
+    int64_t row = t * BM + i;
+    xb[idx] = (row < n) ? (float)x[row * d + c] : 0.0f;
+}
+
+__global__ void queries_to_f32_kernel(const double* __restrict__ z, float* __restrict__ zq,
+                                      int64_t count) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) zq[i] = (float)z[i];
+}
+
+// Known-answer entry: Philox words on device for a (4, N) counter array.
+__global__ void philox_words_kernel(const uint32_t* __restrict__ ctr, uint32_t* __restrict__ out,
+                                    int64_t N, uint32_t k0, uint32_t k1) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    uint32_t c0 = ctr[i], c1 = ctr[N + i], c2 = ctr[2 * N + i], c3 = ctr[3 * N + i];
+    philox10(c0, c1, c2, c3, k0, k1);
+    out[i] = c0;
+    out[N + i] = c1;
+    out[2 * N + i] = c2;
+    out[3 * N + i] = c3;
+}
+
+// ----------------------------------------------------------------- launch --
+cudaError_t launch_cap_generate(const GenArgs& a, cudaStream_t st) {
+    int64_t total = (int64_t)a.Qb * a.mpad;
+    int blocks = (int)((total + 7) / 8);
+    size_t smem = (size_t)8 * 2 * a.d * sizeof(double);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(cap_generate_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    cap_generate_kernel<<<blocks, 256, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_directions(const double* u64, float* u32, int Qb, int m, int mpad, int d,
+                                   cudaStream_t st) {
+    int64_t total = (int64_t)Qb * mpad * d;
+    pack_directions_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(u64, u32, Qb, m, mpad, d);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_state_init(const StateArgs& s, cudaStream_t st) {
+    state_init_kernel<<<s.Qb, 64, 0, st>>>(s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update(const UpdateArgs& a, cudaStream_t st) {
+    update_kernel<<<a.Qb, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const FinalArgs& f, cudaStream_t st) {
+    finalize_kernel<<<f.Qb, 64, 0, st>>>(f);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_block_dataset(const double* x, float* xb, int64_t n, int d, int64_t tiles,
+                                 cudaStream_t st) {
+    int64_t total = tiles * d * BM;
+    block_dataset_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(x, xb, n, d, tiles);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_queries_to_f32(const double* z, float* zq, int64_t count, cudaStream_t st) {
+    if (count == 0) return cudaSuccess;
+    queries_to_f32_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(z, zq, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_philox_words(const uint32_t* ctr, uint32_t* out, int64_t N, uint32_t k0,
+                                uint32_t k1, cudaStream_t st) {
+    if (N == 0) return cudaSuccess;
+    philox_words_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(ctr, out, N, k0, k1);
+    return cudaGetLastError();
+}
+
+}  // namespace rrs

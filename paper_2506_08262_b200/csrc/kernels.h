@@ -1,0 +1,103 @@
+// kernels.h -- argument blocks and launchers shared by the engine and kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rrs {
+
+struct GenArgs {
+    const double* pole;      // [Qb][d]
+    const int* refl_mode;    // [Qb] 0 none, 1 negate e1 coordinate, 2 Householder
+    const double* refl_v;    // [Qb][d]
+    double* u64;             // [Qb][m][d]
+    float* u32;              // [Qb][mpad/BN][d][BN]
+    uint64_t seed;
+    int64_t q0;              // global query index of batch row 0
+    uint32_t refinement;
+    double eps;
+    int Qb, m, mpad, d;
+};
+
+struct StateArgs {
+    double* pole;
+    double* refl_v;
+    int* refl_mode;
+    double* dmin;
+    long long* best_count;
+    long long n;
+    int Qb, d;
+};
+
+struct UpdateArgs {
+    int* counts;             // [Qb][mpad][2] (lt, gt), halfspace; cleared after use
+    const double* depths;    // [Qb][m], projection notions
+    const double* u64;       // [Qb][m][d]
+    double* pole;
+    double* refl_v;
+    int* refl_mode;
+    double* dmin;
+    long long* best_count;
+    double* trace;           // [Qb][r][2+d] or null
+    long long n;
+    double eps;
+    int Qb, m, mpad, d, r, refinement, notion;
+};
+
+struct FinalArgs {
+    const double* pole;
+    const double* dmin;
+    const long long* best_count;
+    double* depth_out;
+    double* argmin_out;
+    long long* count_out;
+    int Qb, d;
+};
+
+// Contraction of the blocked data against one direction block per work unit.
+struct ContractArgs {
+    const float* xb;         // [T][d][BM]
+    const float* u32;        // [Qb][MB][d][BN]
+    const float* zq;         // [Qb][d]
+    int* counts;             // [Qb][MB*BN][2]       (count mode)
+    float* y;                // [Qb][jcount*BN][n]   (store mode), direction j - jb0*BN
+    int64_t n;
+    int64_t tiles;           // T
+    int d;
+    int Qb;
+    int MB;                  // direction blocks per query (mpad / BN)
+    int jb0, jbn;            // direction-block range handled by this launch
+    int m;                   // real directions per query
+    int tiles_per_unit;
+    int chunks;              // ceil(T / tiles_per_unit)
+};
+
+// Univariate projection depths from stored projections y (difference form).
+struct SelectArgs {
+    const float* y;          // [Qb][jcount][n] (row stride n)
+    double* depths;          // [Qb][m]
+    int64_t n;
+    int Qb;
+    int jcount;              // directions per query in this chunk (rows of y)
+    int j0;                  // first direction of the chunk
+    int m;
+    int notion;              // 1 projection, 2 asym projection
+};
+
+cudaError_t launch_cap_generate(const GenArgs& a, cudaStream_t st);
+cudaError_t launch_pack_directions(const double* u64, float* u32, int Qb, int m, int mpad, int d,
+                                   cudaStream_t st);
+cudaError_t launch_state_init(const StateArgs& s, cudaStream_t st);
+cudaError_t launch_update(const UpdateArgs& a, cudaStream_t st);
+cudaError_t launch_finalize(const FinalArgs& f, cudaStream_t st);
+cudaError_t launch_block_dataset(const double* x, float* xb, int64_t n, int d, int64_t tiles,
+                                 cudaStream_t st);
+cudaError_t launch_queries_to_f32(const double* z, float* zq, int64_t count, cudaStream_t st);
+cudaError_t launch_philox_words(const uint32_t* ctr, uint32_t* out, int64_t N, uint32_t k0,
+                                uint32_t k1, cudaStream_t st);
+cudaError_t launch_contract_count(const ContractArgs& a, cudaStream_t st);
+cudaError_t launch_contract_store(const ContractArgs& a, cudaStream_t st);
+cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
+size_t contract_smem_bytes(int d);
+
+}  // namespace rrs

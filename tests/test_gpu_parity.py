@@ -1,0 +1,221 @@
+"""Parity of the CUDA path (through the C ABI) against the reference fixtures
+and the CPU oracle.  Three tiers (BASELINE.json north_star):
+
+  1. halfspace counts bit-exact except inside the tie zone
+     |<u,x_i> - <u,z>| < 1e-6 * max(|x_i|, |z|), whose size is logged;
+  2. per-direction projection / asymmetric-projection depths within 1e-5 rel;
+  3. end-to-end RRS depths: Kendall tau >= 0.99 at equal hyperparameters
+     (plus exact count equality on the config-4 shape).
+"""
+
+import numpy as np
+import pytest
+from scipy.stats import kendalltau
+
+pytestmark = pytest.mark.gpu
+
+TIE_REL = 1e-6
+DEPTH_RTOL = 1e-5
+
+
+def tie_zone(X, z, U):
+    px = X @ U.T  # (n, m) FP64
+    pz = U @ z
+    scale = np.maximum(np.linalg.norm(X, axis=1)[:, None], np.linalg.norm(z))
+    return (np.abs(px - pz[None, :]) < TIE_REL * scale).sum(axis=0)
+
+
+def test_philox_kats_on_device(b200):
+    eng = b200.engine()
+    z = eng.philox4x32(np.zeros((4, 1), dtype=np.uint32), 0, 0)[:, 0]
+    assert [int(w) for w in z] == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    ones = eng.philox4x32(np.full((4, 1), 0xFFFFFFFF, dtype=np.uint32), 0xFFFFFFFF, 0xFFFFFFFF)[:, 0]
+    assert [int(w) for w in ones] == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    ctr = np.array([[0x243F6A88], [0x85A308D3], [0x13198A2E], [0x03707344]], dtype=np.uint32)
+    pi = eng.philox4x32(ctr, 0xA4093822, 0x299F31D0)[:, 0]
+    assert [int(w) for w in pi] == [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
+
+
+def test_philox_words_bitexact(b200, golden):
+    k0, k1 = (int(k) for k in golden["philox_key"])
+    got = b200.engine().philox4x32(golden["philox_ctr"], k0, k1)
+    assert np.array_equal(got, golden["philox_out"])
+
+
+def test_cap_directions_match_reference(b200, golden):
+    """Device generate_batch rows vs the reference rows (FP64; CUDA cos/log
+    may differ from glibc by an ulp)."""
+    eng = b200.engine()
+    worst = 0.0
+    for i in range(int(golden["cap_count"])):
+        p = golden[f"cap{i}_pole"]
+        eps, m, seed, l, q = golden[f"cap{i}_args"]
+        U = eng.cap_directions(p, eps, int(m), int(seed), int(l), int(q))
+        ref = golden[f"cap{i}_U"]
+        worst = max(worst, float(np.max(np.abs(U - ref))))
+        assert np.all(np.abs(np.linalg.norm(U, axis=1) - 1.0) <= 1e-12)
+        assert np.all(U @ p >= np.cos(eps) - 1e-10)  # cap membership
+    print(f"max |U_gpu - U_ref| = {worst:.3e}")
+    assert worst <= 1e-13
+
+
+@pytest.mark.parametrize("tag", ["ed_small", "ed_cauchy"])
+def test_tier1_halfspace_counts(b200, golden, tag):
+    X, U, Z = golden[f"{tag}_x"], golden[f"{tag}_U"], golden[f"{tag}_Z"]
+    data = b200.Dataset(X)
+    total_zone = used = 0
+    for qi, z in enumerate(Z):
+        out, cle, cge = b200.evaluate_directions_counts(z, data, U)
+        rcle, rcge = golden[f"{tag}_cle"][qi], golden[f"{tag}_cge"][qi]
+        T = tie_zone(X, z, U)
+        total_zone += int(T.sum())
+        dle, dge = np.abs(cle - rcle), np.abs(cge - rcge)
+        assert np.all(dle <= T) and np.all(dge <= T), (qi, np.flatnonzero((dle > T) | (dge > T)))
+        used += int(np.count_nonzero((dle > 0) | (dge > 0)))
+        ref_depth = golden[f"{tag}_halfspace"][qi]
+        exact = (dle == 0) & (dge == 0)
+        assert np.array_equal(out[exact], ref_depth[exact])
+    print(f"{tag}: tie-zone elements {total_zone}, directions using slack {used}")
+
+
+def test_self_tie_in_sample(b200, golden):
+    """z = x_i: the query's own row projects to exactly 0 (difference form), so
+    it is counted on both sides of every direction."""
+    X, U = golden["ed_small_x"], golden["ed_small_U"]
+    data = b200.Dataset(X)
+    for i in (0, 7, 123):
+        _, cle, cge = b200.evaluate_directions_counts(X[i], data, U)
+        assert np.all(cle >= 1) and np.all(cge >= 1)
+        assert np.all(cle + cge >= X.shape[0] + 1)
+
+
+@pytest.mark.parametrize("tag", ["ed_small", "ed_cauchy"])
+@pytest.mark.parametrize("notion", ["projection", "asym_projection"])
+def test_tier2_projection_depths(b200, golden, tag, notion):
+    X, U, Z = golden[f"{tag}_x"], golden[f"{tag}_U"], golden[f"{tag}_Z"]
+    data = b200.Dataset(X)
+    cfg = b200.ParallelConfig(workers=1)
+    for qi, z in enumerate(Z):
+        got = b200.evaluate_directions(z, data, U, notion, cfg)
+        np.testing.assert_allclose(got, golden[f"{tag}_{notion}"][qi], rtol=DEPTH_RTOL, atol=0)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 18, 101, 1024])
+def test_univariate_spans_tie_heavy(b200, golden, n):
+    """The reference's tie-heavy span cases (test_backends.py:59-73) through the
+    fused device path: d = 1, u = 1, so y = x - z."""
+    px, pz = golden[f"span_n{n}_px"], golden[f"span_n{n}_pz"]
+    U = np.ones((1, 1))
+    cfg = b200.ParallelConfig(workers=1)
+    for name in ("halfspace", "projection", "asym_projection"):
+        ref = golden[f"span_n{n}_{name}"]
+        got = np.array([b200.evaluate_directions(pz[j:j + 1], b200.Dataset(px[j][:, None]), U, name, cfg)[0]
+                        for j in range(px.shape[0])])
+        if name == "halfspace":
+            assert np.array_equal(got, ref)
+        else:
+            np.testing.assert_allclose(got, ref, rtol=DEPTH_RTOL, atol=0)
+
+
+def test_degenerate_rows(b200, golden):
+    px, pz = golden["degen_px"], golden["degen_pz"]
+    cfg = b200.ParallelConfig(workers=1)
+    for name in ("halfspace", "projection", "asym_projection"):
+        got = [b200.evaluate_directions(pz[j:j + 1], b200.Dataset(px[j][:, None]), np.ones((1, 1)), name,
+                                        cfg)[0] for j in range(3)]
+        assert np.array_equal(np.array(got), golden[f"degen_{name}"]), name
+
+
+def test_tier3_config1_all_points(b200, golden):
+    """BASELINE config 1: halfspace, n=1000, d=5, k=1000, r=10, alpha=0.9, seed 1."""
+    X = golden["c1_x"]
+    data = b200.Dataset(X)
+    cfg = b200.RrsConfig(total_directions=1000, refinements=10, shrink=0.9, notion="halfspace", seed=1)
+    depth, argmin, tr, cnt = b200.depth_batch_arrays(X, data, cfg, trace=True)
+    ref = golden["c1_depth"]
+    same = np.mean(depth == ref)
+    tau = kendalltau(depth, ref).statistic
+    print(f"config 1: {same:.4f} of depths identical, tau = {tau:.5f}")
+    assert tau >= 0.99
+    assert same >= 0.98
+    assert np.array_equal(np.rint(depth * X.shape[0]).astype(np.int64), cnt)
+    assert np.all(np.abs(np.linalg.norm(argmin, axis=1) - 1.0) <= 1e-12)
+    eps = np.array(cfg.epsilons())
+    assert np.array_equal(tr[:, :, 1], np.broadcast_to(eps, tr[:, :, 1].shape))  # exact schedule
+    assert np.all(np.diff(tr[:, :, 0], axis=1) <= 0)  # monotone trace
+
+
+@pytest.mark.parametrize("notion", ["halfspace", "projection", "asym_projection"])
+def test_tier3_small_rrs(b200, golden, notion):
+    X, Z = golden[f"rrs_{notion}_x"], golden[f"rrs_{notion}_z"]
+    cfg = b200.RrsConfig(total_directions=400, refinements=8, shrink=0.8, notion=notion, seed=77)
+    res = b200.depth_batch(list(Z), b200.Dataset(X), cfg)
+    depth = np.array([r.depth for r in res])
+    ref = golden[f"rrs_{notion}_depth"]
+    if notion == "halfspace":
+        assert np.mean(depth == ref) >= 0.9
+    else:
+        close = np.isclose(depth, ref, rtol=DEPTH_RTOL, atol=0)
+        assert np.mean(close) >= 0.9
+    assert kendalltau(depth, ref).statistic >= 0.99
+    for r in res:
+        assert len(r.trace) == 8 and r.directions_used == 400
+        assert all(t.epsilon == (np.pi / 2) * 0.8**l for l, t in enumerate(r.trace))
+
+
+def test_config4_miniature_exact_counts(b200, golden):
+    X, Z = golden["c4mini_x"], golden["c4mini_z"]
+    cfg = b200.RrsConfig(total_directions=2000, refinements=20, shrink=0.9, notion="halfspace", seed=1)
+    depth, _, _, cnt = b200.depth_batch_arrays(Z, b200.Dataset(X), cfg)
+    ref = golden["c4mini_depth"]
+    n = X.shape[0]
+    assert np.array_equal(cnt[:6], np.ones(6, dtype=np.int64))  # in-sample: self-tie only
+    assert np.array_equal(depth[:6], ref[:6])
+    rc = np.rint(ref * n).astype(np.int64)
+    assert np.all(np.abs(cnt - rc) <= np.maximum(1, rc // 50)), (cnt, rc)
+
+
+def test_shard_offsets_bitwise(b200, golden):
+    """Global query indices make results independent of how queries are split."""
+    X = golden["c1_x"]
+    data = b200.Dataset(X)
+    cfg = b200.RrsConfig(total_directions=1000, refinements=10, shrink=0.9, notion="halfspace", seed=1)
+    full = b200.depth_batch_arrays(X[:96], data, cfg)
+    parts = [b200.depth_batch_arrays(X[a:a + 24], data, cfg, q0=a) for a in range(0, 96, 24)]
+    assert np.array_equal(full[0], np.concatenate([p[0] for p in parts]))
+    assert np.array_equal(full[1], np.concatenate([p[1] for p in parts]))
+
+
+def test_structure_cases(b200):
+    data = b200.Dataset([[0.3, -0.7]])
+    assert b200.simple_random_search(data.x[0], data, 50, "halfspace", 0).depth == 1.0
+    rng = np.random.default_rng(1)
+    data = b200.Dataset(rng.standard_normal((100, 3)))
+    assert b200.simple_random_search(np.full(3, 1e6), data, 32, "halfspace", 1).depth == 0.0
+
+
+def test_datadepth_wrappers(b200, golden):
+    X = golden["rrs_halfspace_x"]
+    Z = golden["rrs_halfspace_z"]
+    for fn, notion in ((b200.halfspace, "halfspace"), (b200.projection, "projection"),
+                       (b200.aprojection, "asym_projection")):
+        got = fn(Z, X, NRandom=400, n_refinements=8, sphcap_shrink=0.8, solver="refinedrandom", seed=77)
+        cfg = b200.RrsConfig(total_directions=400, refinements=8, shrink=0.8, notion=notion, seed=77)
+        ref = b200.depth_batch_arrays(Z, b200.Dataset(X), cfg)[0]
+        assert np.array_equal(got, ref)
+    with pytest.raises(ValueError):
+        b200.halfspace(Z, X, solver="neldermead")
+
+
+@pytest.mark.slow
+def test_config4_scale_in_sample_counts(b200):
+    """Config 4 at full size (n=100k, d=50, k=20000, r=20) on a few in-sample
+    queries: every depth is exactly 1/n (self-tie only)."""
+    from paper_2506_08262_b200.synthetic import toeplitz_gaussian
+
+    X = toeplitz_gaussian(50, 100_000, seed=0)
+    cfg = b200.RrsConfig(total_directions=20_000, refinements=20, shrink=0.9, notion="halfspace", seed=1)
+    idx = np.array([0, 12345, 99_999])
+    depth, _, _, cnt = b200.depth_batch_arrays(X[idx], b200.Dataset(X), cfg, q0=0)
+    assert np.array_equal(cnt, np.ones(3, dtype=np.int64))
+    assert np.all(depth == 1.0 / 100_000)
