@@ -228,7 +228,8 @@ def main():
     cfg = rrs.RrsConfig(total_directions=k, refinements=r, shrink=alpha, notion=notion, seed=1)
     X = make_data(distn, n, d)
     eng = rrs.engine(local)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # one non-default stream shared by torch and the engine
+    torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
     eng.set_dataset(X, key="bench")
     Xd = torch.from_numpy(X).cuda()

@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
         if (S > 1) issue(1);
     }
     for (int k = tid; k < d; k += CT_THREADS) zs[k] = a.zq[(size_t)q * d + k];
+    __syncthreads();  // zs is read by every thread in the subtract pass
     mbar_wait(&bars[0], 0);
 
     float acc[8][8];
