@@ -90,11 +90,11 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
     mbar_wait(&bars[0], 0);
 
     float acc[8][8];
-    unsigned lt[8], gt[8];
+    unsigned lt[8], le[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         lt[j] = 0u;
-        gt[j] = 0u;
+        le[j] = 0u;
     }
 
     for (int s = 0; s < S; ++s) {
@@ -112,17 +112,28 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
             const int64_t vrows = a.n - row0;
             const int valid = vrows < BM ? (int)vrows : BM;
             float4* A4 = reinterpret_cast<float4*>(Ab);
-            const int total4 = kcnt * (BM / 4);
-            for (int idx = tid; idx < total4; idx += CT_THREADS) {
-                const int k = idx / (BM / 4);
-                const int i4 = (idx - k * (BM / 4)) * 4;
-                const float zk = zs[k0 + k];
-                float4 v = A4[idx];
-                v.x = (i4 + 0 < valid) ? v.x - zk : 0.0f;
-                v.y = (i4 + 1 < valid) ? v.y - zk : 0.0f;
-                v.z = (i4 + 2 < valid) ? v.z - zk : 0.0f;
-                v.w = (i4 + 3 < valid) ? v.w - zk : 0.0f;
-                A4[idx] = v;
+            // thread owns column group i4 = (tid % 32) * 4 of rows k = tid / 32 + 8 * step
+            const int i4 = (tid & 31) * 4;
+            if (valid == BM) {
+                for (int k = tid >> 5; k < kcnt; k += CT_THREADS / 32) {
+                    const float zk = zs[k0 + k];
+                    float4 v = A4[k * (BM / 4) + (tid & 31)];
+                    v.x -= zk;
+                    v.y -= zk;
+                    v.z -= zk;
+                    v.w -= zk;
+                    A4[k * (BM / 4) + (tid & 31)] = v;
+                }
+            } else {
+                for (int k = tid >> 5; k < kcnt; k += CT_THREADS / 32) {
+                    const float zk = zs[k0 + k];
+                    float4 v = A4[k * (BM / 4) + (tid & 31)];
+                    v.x = (i4 + 0 < valid) ? v.x - zk : 0.0f;
+                    v.y = (i4 + 1 < valid) ? v.y - zk : 0.0f;
+                    v.z = (i4 + 2 < valid) ? v.z - zk : 0.0f;
+                    v.w = (i4 + 3 < valid) ? v.w - zk : 0.0f;
+                    A4[k * (BM / 4) + (tid & 31)] = v;
+                }
             }
         }
         __syncthreads();
@@ -152,15 +163,16 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
 
         if (kc == nkc - 1) {
             if constexpr (!STORE) {
-                // exact zeros are +0 (accumulators start at +0, RN), so the sign
-                // bit is #(y<0) and the sign bit of the integer negation is #(y>0)
+                // exact zeros are +0 (accumulators start at +0, RN): the sign bit
+                // of y is [y < 0] and the sign bit of bits(y) - 1 is [y <= 0]
+                // (padding rows are +0 and are removed from le at the end)
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const int b = __float_as_int(acc[i][j]);
-                        lt[j] += (unsigned)b >> 31;
-                        gt[j] += (unsigned)(-b) >> 31;
+                        const unsigned b = __float_as_uint(acc[i][j]);
+                        lt[j] += b >> 31;
+                        le[j] += (b - 1u) >> 31;
                     }
             } else {
                 const int64_t row0 = t * BM;
@@ -199,7 +211,7 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             lt[j] += __shfl_xor_sync(0xffffffffu, lt[j], 16);
-            gt[j] += __shfl_xor_sync(0xffffffffu, gt[j], 16);
+            le[j] += __shfl_xor_sync(0xffffffffu, le[j], 16);
         }
         int* red = reinterpret_cast<int*>(As);  // [8 warps][BN][2]
         const int warp = tid >> 5;
@@ -208,17 +220,22 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
             for (int j = 0; j < 8; ++j) {
                 const int col = (j < 4) ? tx * 4 + j : 64 + tx * 4 + (j - 4);
                 red[(warp * BN + col) * 2 + 0] = (int)lt[j];
-                red[(warp * BN + col) * 2 + 1] = (int)gt[j];
+                red[(warp * BN + col) * 2 + 1] = (int)le[j];
             }
         }
         __syncthreads();
         if (tid < BN) {
-            int slt = 0, sgt = 0;
+            int slt = 0, sle = 0;
 #pragma unroll
             for (int w = 0; w < CT_THREADS / 32; ++w) {
                 slt += red[(w * BN + tid) * 2 + 0];
-                sgt += red[(w * BN + tid) * 2 + 1];
+                sle += red[(w * BN + tid) * 2 + 1];
             }
+            // rows of this unit: real ones plus zero padding (counted in le only)
+            const int64_t rows_all = (t_end - t_begin) * BM;
+            int64_t rows_real = a.n - t_begin * BM;
+            if (rows_real > rows_all) rows_real = rows_all;
+            const int sgt = (int)(rows_real - (sle - (rows_all - rows_real)));
             int* dst = a.counts + ((size_t)q * a.MB * BN + (size_t)jb * BN + tid) * 2;
             if (slt) atomicAdd(dst + 0, slt);
             if (sgt) atomicAdd(dst + 1, sgt);
