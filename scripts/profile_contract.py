@@ -14,7 +14,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--notion", default="halfspace")
 ap.add_argument("--n", type=int, default=100_000)
 ap.add_argument("--d", type=int, default=50)
-ap.add_argument("--q", type=int, default=64)
+ap.add_argument("--q", type=int, default=1024)
 ap.add_argument("--m", type=int, default=1000)
 ap.add_argument("--r", type=int, default=2)
 a = ap.parse_args()
