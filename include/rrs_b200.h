@@ -106,6 +106,11 @@ int rrs_cap_directions_host(rrs_engine* e, const double* pole, int32_t d, double
 int rrs_philox4x32_host(rrs_engine* e, const uint32_t* ctr, int64_t N, uint32_t key0,
                         uint32_t key1, uint32_t* out);
 
+/* Halfspace contraction kernel: 0 = auto (tensor cores when d <= 64 and
+ * n >= 4096), 1 = FP32 FFMA (contract.cu), 2 = tcgen05 int8-limb exact
+ * integer (contract_tc.cu; halfspace, d <= 64, m <= 4096). */
+int rrs_engine_set_contract_path(rrs_engine* e, int32_t path);
+
 /* Diagnostics for the last batch: device time (ms) of each stage summed over
  * the batch (generation, contraction, univariate, update) and launch count. */
 typedef struct {

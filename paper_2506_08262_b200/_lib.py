@@ -74,6 +74,7 @@ SIGNATURES = [
      [_vp, _u32p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint32, _u32p]),
     ("rrs_engine_stats", ctypes.c_int, [_vp, ctypes.POINTER(RrsStatsC)]),
     ("rrs_engine_enable_timing", ctypes.c_int, [_vp, ctypes.c_int32]),
+    ("rrs_engine_set_contract_path", ctypes.c_int, [_vp, ctypes.c_int32]),
 ]
 
 _lib = None
@@ -168,6 +169,11 @@ class Engine:
 
     def set_workspace_limit(self, nbytes: int):
         _raise(load_library().rrs_engine_set_workspace_limit(self._h, int(nbytes)))
+
+    def set_contract_path(self, path: str):
+        """'auto' | 'ffma' | 'tensor' (halfspace contraction kernel)."""
+        code = {"auto": 0, "ffma": 1, "tensor": 2}[path]
+        _raise(load_library().rrs_engine_set_contract_path(self._h, code))
 
     def enable_timing(self, on: bool = True):
         _raise(load_library().rrs_engine_enable_timing(self._h, 1 if on else 0))

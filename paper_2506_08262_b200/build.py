@@ -23,6 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = {  # file -> extra flags
     "gen.cu": ["-fmad=false"],
     "contract.cu": [],
+    "contract_tc.cu": [],
     "select.cu": [],
     "engine.cu": [],
 }

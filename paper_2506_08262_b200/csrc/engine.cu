@@ -87,7 +87,8 @@ struct rrs_engine {
     int d = 0;
     int64_t tiles = 0;
     // workspace
-    DevBuf zq, u64, u32, counts, depths, y, pole, reflv, reflmode, dmin, bestcnt;
+    DevBuf zq, u64, u32, u8, counts, depths, y, pole, reflv, reflmode, dmin, bestcnt;
+    int contract_path = 0;  // 0 auto, 1 FFMA (contract.cu), 2 tensor cores (contract_tc.cu)
     DevBuf tmp_in, tmp_out0, tmp_out1, tmp_out2, tmp_out3;
     // timing
     bool timing = false;
@@ -152,6 +153,8 @@ int validate_cfg(const rrs_config* c) {
 
 struct Plan {
     int m, mpad, MB, Qb;
+    bool tc;     // tensor-core int8-limb contraction (halfspace, d <= 64)
+    int nb8;     // 64-direction blocks per query (tensor path)
     int jchunk;  // direction blocks per store launch (projection notions)
     int tpu, chunks;
 };
@@ -161,9 +164,12 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     p.m = m;
     p.MB = (m + BN - 1) / BN;
     p.mpad = p.MB * BN;
+    p.nb8 = (m + 63) / 64;
+    const bool tc_ok = notion == RRS_HALFSPACE && e->d <= 64 && p.nb8 * 64 <= 4096;
+    p.tc = tc_ok && (e->contract_path == 2 || (e->contract_path == 0 && e->n >= 4096));
     const int64_t d = e->d, n = e->n;
     int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * d * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 8 +
-                    d * 40 + 64;
+                    d * 40 + 64 + (int64_t)p.nb8 * 12288;
     int64_t budget = e->ws_limit;
     int64_t qb = 4096;
     if (notion != RRS_HALFSPACE) {
@@ -210,6 +216,7 @@ int ensure_ws(rrs_engine* e, const Plan& p, int notion) {
     CK(e->reflmode.ensure(Qb * 4));
     CK(e->dmin.ensure(Qb * 8));
     CK(e->bestcnt.ensure(Qb * 8));
+    CK(e->u8.ensure(p.tc ? Qb * (size_t)p.nb8 * 12288 : 16));
     if (notion == RRS_HALFSPACE) {
         CK(e->counts.ensure(Qb * p.mpad * 2 * 4));
         CK(e->depths.ensure(8));
@@ -239,6 +246,28 @@ ContractArgs contract_args(rrs_engine* e, const Plan& p, int Qb, int jb0, int jb
     c.tiles_per_unit = p.tpu;
     c.chunks = p.chunks;
     return c;
+}
+
+int contract_halfspace(rrs_engine* e, const Plan& p, int Qb) {
+    if (p.tc) {
+        TcArgs t{};
+        t.xb = e->xb.as<float>();
+        t.zq = e->zq.as<float>();
+        t.u8 = e->u8.as<unsigned char>();
+        t.counts = e->counts.as<int>();
+        t.n = e->n;
+        t.tiles = e->tiles;
+        t.d = e->d;
+        t.Qb = Qb;
+        t.NB = p.nb8;
+        t.m = p.m;
+        t.mpad = p.mpad;
+        CK(launch_contract_tc(t, e->sms, e->stream));
+    } else {
+        ContractArgs c = contract_args(e, p, Qb, 0, p.MB);
+        CK(launch_contract_count(c, e->stream));
+    }
+    return RRS_OK;
 }
 
 // y -> per-direction depths for the projection notions, chunked over direction blocks
@@ -335,13 +364,14 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 g.m = m;
                 g.mpad = p.mpad;
                 g.d = d;
+                g.u8 = p.tc ? e->u8.as<unsigned char>() : nullptr;
+                g.nb8 = p.nb8;
                 CK(launch_cap_generate(g, e->stream));
                 e->stats.kernel_launches++;
             }
             if (cfg->notion == RRS_HALFSPACE) {
                 Timer t(e, 1);
-                ContractArgs c = contract_args(e, p, Qb, 0, p.MB);
-                CK(launch_contract_count(c, e->stream));
+                if (int rc = contract_halfspace(e, p, Qb)) return rc;
                 e->stats.kernel_launches++;
                 e->stats.contract_launches++;
             } else {
@@ -437,7 +467,7 @@ int rrs_engine_destroy(rrs_engine* e) {
     if (!e) return RRS_OK;
     cudaSetDevice(e->device);
     cudaStreamSynchronize(e->stream);
-    for (DevBuf* b : {&e->xb, &e->zq, &e->u64, &e->u32, &e->counts, &e->depths, &e->y, &e->pole,
+    for (DevBuf* b : {&e->xb, &e->zq, &e->u64, &e->u32, &e->u8, &e->counts, &e->depths, &e->y, &e->pole,
                       &e->reflv, &e->reflmode, &e->dmin, &e->bestcnt, &e->tmp_in, &e->tmp_out0,
                       &e->tmp_out1, &e->tmp_out2, &e->tmp_out3})
         b->release();
@@ -464,6 +494,13 @@ int rrs_engine_set_workspace_limit(rrs_engine* e, int64_t bytes) {
     if (!e) return fail(RRS_ERR_INVALID, "engine is null");
     if (bytes < (1 << 20)) return fail(RRS_ERR_INVALID, "workspace limit below 1 MiB");
     e->ws_limit = bytes;
+    return RRS_OK;
+}
+
+int rrs_engine_set_contract_path(rrs_engine* e, int32_t path) {
+    if (!e) return fail(RRS_ERR_INVALID, "engine is null");
+    if (path < 0 || path > 2) return fail(RRS_ERR_INVALID, "contract path must be 0 (auto), 1 (FFMA) or 2 (tensor)");
+    e->contract_path = path;
     return RRS_OK;
 }
 
@@ -581,10 +618,10 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
     CK(cudaMemcpyAsync(e->tmp_in.p, z, (size_t)d * 8, cudaMemcpyHostToDevice, e->stream));
     CK(launch_queries_to_f32(e->tmp_in.as<double>(), e->zq.as<float>(), d, e->stream));
     CK(launch_pack_directions(e->u64.as<double>(), e->u32.as<float>(), 1, m, p.mpad, d, e->stream));
+    if (p.tc) CK(launch_pack_limbs(e->u64.as<double>(), e->u8.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (notion == RRS_HALFSPACE) {
         CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.mpad * 2 * 4, e->stream));
-        ContractArgs c = contract_args(e, p, 1, 0, p.MB);
-        CK(launch_contract_count(c, e->stream));
+        if (int rc = contract_halfspace(e, p, 1)) return rc;
         std::vector<int> cnt((size_t)p.mpad * 2);
         CK(cudaMemcpyAsync(cnt.data(), e->counts.p, cnt.size() * 4, cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));

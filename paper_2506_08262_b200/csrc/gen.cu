@@ -136,6 +136,21 @@ __device__ double pw_rec(const double* a, int n) {
 
 __device__ __forceinline__ double pw_sum(const double* a, int n) { return 0.0 + pw_rec(a, n); }
 
+// Tensor-path direction operand: U = rint(u * 2^22) (|u| <= 1) split into three
+// signed int8 limbs U = b2*2^16 + b1*2^8 + b0, stored in the canonical K-major
+// no-swizzle UMMA layout of a 64-direction block:
+//   [limb 3][k-chunk 4][direction 64][16 bytes]   (12 KB per block)
+// u8row points at (block, direction) = base + (j & 63) * 16.
+__device__ __forceinline__ int quantize22(double u) { return __double2int_rn(u * 4194304.0); }
+__device__ __forceinline__ void put_limbs(unsigned char* u8row, int c, int U) {
+    const int U1 = (U + 128) >> 8;
+    const int U2 = (U1 + 128) >> 8;
+    unsigned char* p = u8row + (c >> 4) * 1024 + (c & 15);
+    p[0] = (unsigned char)(U & 0xFF);
+    p[4096] = (unsigned char)(U1 & 0xFF);
+    p[8192] = (unsigned char)(U2 & 0xFF);
+}
+
 // ------------------------------------------------------- cap generation K1 --
 // directions.py:167-182 (_cap_rows) for every (query, direction): one warp per
 // direction.  theta = U(v=0,j)*eps; d-1 normals from v = 1..d-1 (zero-norm
@@ -156,8 +171,13 @@ __global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
     const int q = (int)(gdir / a.mpad);
     const int j = (int)(gdir % a.mpad);
     float* u32 = a.u32 + (size_t)q * a.mpad * d + (size_t)(j / BN) * d * BN + (j % BN);
+    unsigned char* u8 = nullptr;
+    if (a.u8 && j < a.nb8 * 64)
+        u8 = a.u8 + ((size_t)q * a.nb8 + (j >> 6)) * 12288 + (size_t)(j & 63) * 16;
     if (j >= a.m) {
         for (int c = lane; c < d; c += 32) u32[(size_t)c * BN] = 0.0f;
+        if (u8)
+            for (int c = lane; c < 64; c += 32) put_limbs(u8, c, 0);
         return;
     }
     const uint32_t qg = (uint32_t)((uint64_t)(a.q0 + q) & 0xFFFFFFFFu);
@@ -169,6 +189,8 @@ __global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
             u64[0] = pole[0];
             u32[0] = (float)pole[0];
         }
+        if (u8)
+            for (int c = lane; c < 64; c += 32) put_limbs(u8, c, c == 0 ? quantize22(pole[0]) : 0);
         return;
     }
     const int dm = d - 1;
@@ -217,6 +239,8 @@ __global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
         u64[c] = val;
         u32[(size_t)c * BN] = (float)val;
     }
+    if (u8)
+        for (int c = lane; c < 64; c += 32) put_limbs(u8, c, c < d ? quantize22(sc[c]) : 0);
 }
 
 // Explicit-direction mode: U64 given; build the FP32 contraction operand.
@@ -231,6 +255,26 @@ __global__ void pack_directions_kernel(const double* __restrict__ u64, float* __
     int q = (int)(r / mpad);
     float v = (j < m) ? (float)u64[((size_t)q * m + j) * d + c] : 0.0f;
     u32[(size_t)q * mpad * d + (size_t)(j / BN) * d * BN + (size_t)c * BN + (j % BN)] = v;
+}
+
+__global__ void pack_limbs_kernel(const double* __restrict__ u64, unsigned char* __restrict__ u8, int Qb,
+                                  int m, int nb8, int d) {
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = (int64_t)Qb * nb8 * 64 * 64;
+    if (idx >= total) return;
+    int c = (int)(idx & 63);
+    int64_t r = idx >> 6;
+    int j = (int)(r % (nb8 * 64));
+    int q = (int)(r / (nb8 * 64));
+    int U = (j < m && c < d) ? quantize22(u64[((size_t)q * m + j) * d + c]) : 0;
+    put_limbs(u8 + ((size_t)q * nb8 + (j >> 6)) * 12288 + (size_t)(j & 63) * 16, c, U);
+}
+
+cudaError_t launch_pack_limbs(const double* u64, unsigned char* u8, int Qb, int m, int nb8, int d,
+                              cudaStream_t st) {
+    int64_t total = (int64_t)Qb * nb8 * 64 * 64;
+    pack_limbs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(u64, u8, Qb, m, nb8, d);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------- RRS state --

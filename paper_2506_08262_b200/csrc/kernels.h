@@ -12,6 +12,8 @@ struct GenArgs {
     const double* refl_v;    // [Qb][d]
     double* u64;             // [Qb][m][d]
     float* u32;              // [Qb][mpad/BN][d][BN]
+    unsigned char* u8;       // nullable: [Qb][NB8][3 limbs][4][64][16] int8 limbs (tensor path)
+    int nb8;                 // 64-direction blocks per query in u8
     uint64_t seed;
     int64_t q0;              // global query index of batch row 0
     uint32_t refinement;
@@ -72,6 +74,17 @@ struct ContractArgs {
     int chunks;              // ceil(T / tiles_per_unit)
 };
 
+// Tensor-core (int8 limb) halfspace contraction, contract_tc.cu.
+struct TcArgs {
+    const float* xb;            // [T][d][128]
+    const float* zq;            // [Qb][d]
+    const unsigned char* u8;    // [Qb][NB][3][4][64][16]
+    int* counts;                // [Qb][mpad][2]
+    int64_t n;
+    int64_t tiles;
+    int d, Qb, NB, m, mpad;
+};
+
 // Univariate projection depths from stored projections y (difference form).
 struct SelectArgs {
     const float* y;          // [Qb][jcount][n] (row stride n)
@@ -98,6 +111,10 @@ cudaError_t launch_philox_words(const uint32_t* ctr, uint32_t* out, int64_t N, u
 cudaError_t launch_contract_count(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_contract_store(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
+cudaError_t launch_contract_tc(const TcArgs& a, int sms, cudaStream_t st);
+cudaError_t launch_pack_limbs(const double* u64, unsigned char* u8, int Qb, int m, int nb8, int d,
+                              cudaStream_t st);
+size_t contract_tc_smem_bytes();
 size_t contract_smem_bytes(int d);
 
 }  // namespace rrs

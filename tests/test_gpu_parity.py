@@ -18,6 +18,22 @@ TIE_REL = 1e-6
 DEPTH_RTOL = 1e-5
 
 
+PATHS = ["ffma", "tensor"]
+
+
+class contract_path:
+    """Force the halfspace contraction kernel (FFMA or tcgen05) for a block."""
+
+    def __init__(self, pkg, path):
+        self.eng, self.path = pkg.engine(), path
+
+    def __enter__(self):
+        self.eng.set_contract_path(self.path)
+
+    def __exit__(self, *exc):
+        self.eng.set_contract_path("auto")
+
+
 def tie_zone(X, z, U):
     px = X @ U.T  # (n, m) FP64
     pz = U @ z
@@ -59,13 +75,15 @@ def test_cap_directions_match_reference(b200, golden):
     assert worst <= 1e-13
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("tag", ["ed_small", "ed_cauchy"])
-def test_tier1_halfspace_counts(b200, golden, tag):
+def test_tier1_halfspace_counts(b200, golden, tag, path):
     X, U, Z = golden[f"{tag}_x"], golden[f"{tag}_U"], golden[f"{tag}_Z"]
     data = b200.Dataset(X)
     total_zone = used = 0
     for qi, z in enumerate(Z):
-        out, cle, cge = b200.evaluate_directions_counts(z, data, U)
+        with contract_path(b200, path):
+            out, cle, cge = b200.evaluate_directions_counts(z, data, U)
         rcle, rcge = golden[f"{tag}_cle"][qi], golden[f"{tag}_cge"][qi]
         T = tie_zone(X, z, U)
         total_zone += int(T.sum())
@@ -75,16 +93,18 @@ def test_tier1_halfspace_counts(b200, golden, tag):
         ref_depth = golden[f"{tag}_halfspace"][qi]
         exact = (dle == 0) & (dge == 0)
         assert np.array_equal(out[exact], ref_depth[exact])
-    print(f"{tag}: tie-zone elements {total_zone}, directions using slack {used}")
+    print(f"{tag}/{path}: tie-zone elements {total_zone}, directions using slack {used}")
 
 
-def test_self_tie_in_sample(b200, golden):
+@pytest.mark.parametrize("path", PATHS)
+def test_self_tie_in_sample(b200, golden, path):
     """z = x_i: the query's own row projects to exactly 0 (difference form), so
     it is counted on both sides of every direction."""
     X, U = golden["ed_small_x"], golden["ed_small_U"]
     data = b200.Dataset(X)
     for i in (0, 7, 123):
-        _, cle, cge = b200.evaluate_directions_counts(X[i], data, U)
+        with contract_path(b200, path):
+            _, cle, cge = b200.evaluate_directions_counts(X[i], data, U)
         assert np.all(cle >= 1) and np.all(cge >= 1)
         assert np.all(cle + cge >= X.shape[0] + 1)
 
@@ -126,16 +146,18 @@ def test_degenerate_rows(b200, golden):
         assert np.array_equal(np.array(got), golden[f"degen_{name}"]), name
 
 
-def test_tier3_config1_all_points(b200, golden):
+@pytest.mark.parametrize("path", PATHS)
+def test_tier3_config1_all_points(b200, golden, path):
     """BASELINE config 1: halfspace, n=1000, d=5, k=1000, r=10, alpha=0.9, seed 1."""
     X = golden["c1_x"]
     data = b200.Dataset(X)
     cfg = b200.RrsConfig(total_directions=1000, refinements=10, shrink=0.9, notion="halfspace", seed=1)
-    depth, argmin, tr, cnt = b200.depth_batch_arrays(X, data, cfg, trace=True)
+    with contract_path(b200, path):
+        depth, argmin, tr, cnt = b200.depth_batch_arrays(X, data, cfg, trace=True)
     ref = golden["c1_depth"]
     same = np.mean(depth == ref)
     tau = kendalltau(depth, ref).statistic
-    print(f"config 1: {same:.4f} of depths identical, tau = {tau:.5f}")
+    print(f"config 1 ({path}): {same:.4f} of depths identical, tau = {tau:.5f}")
     assert tau >= 0.99
     assert same >= 0.98
     assert np.array_equal(np.rint(depth * X.shape[0]).astype(np.int64), cnt)
@@ -163,10 +185,12 @@ def test_tier3_small_rrs(b200, golden, notion):
         assert all(t.epsilon == (np.pi / 2) * 0.8**l for l, t in enumerate(r.trace))
 
 
-def test_config4_miniature_exact_counts(b200, golden):
+@pytest.mark.parametrize("path", PATHS)
+def test_config4_miniature_exact_counts(b200, golden, path):
     X, Z = golden["c4mini_x"], golden["c4mini_z"]
     cfg = b200.RrsConfig(total_directions=2000, refinements=20, shrink=0.9, notion="halfspace", seed=1)
-    depth, _, _, cnt = b200.depth_batch_arrays(Z, b200.Dataset(X), cfg)
+    with contract_path(b200, path):
+        depth, _, _, cnt = b200.depth_batch_arrays(Z, b200.Dataset(X), cfg)
     ref = golden["c4mini_depth"]
     n = X.shape[0]
     assert np.array_equal(cnt[:6], np.ones(6, dtype=np.int64))  # in-sample: self-tie only
@@ -205,6 +229,29 @@ def test_datadepth_wrappers(b200, golden):
         assert np.array_equal(got, ref)
     with pytest.raises(ValueError):
         b200.halfspace(Z, X, solver="neldermead")
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_paths_agree_on_counts(b200, path):
+    """Both contraction kernels against the FP64 oracle on random data with
+    off-sample queries (n not a multiple of the 128-point tile, m not a
+    multiple of the direction blocks)."""
+    from oracle import oracle
+
+    rng = np.random.default_rng(21)
+    X = rng.standard_normal((5000 + 77, 37))
+    U = rng.standard_normal((300, 37))
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    data = b200.Dataset(X)
+    slack = 0
+    for z in (X[5], 0.2 * X[9], rng.standard_normal(37)):
+        with contract_path(b200, path):
+            _, cle, cge = b200.evaluate_directions_counts(z, data, U)
+        _, rle, rge = oracle.evaluate_directions(z, X, U, "halfspace", with_counts=True)
+        T = tie_zone(X, z, U)
+        assert np.all(np.abs(cle - rle) <= T) and np.all(np.abs(cge - rge) <= T)
+        slack += int(np.count_nonzero((cle != rle) | (cge != rge)))
+    print(f"{path}: directions using tie-zone slack {slack} / 900")
 
 
 @pytest.mark.slow
