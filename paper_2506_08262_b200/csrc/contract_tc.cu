@@ -2,64 +2,79 @@
 // (int8-limb, Ozaki-style) contraction with a fused halfspace-count epilogue.
 //
 // Same result contract as the FFMA kernel (contract.cu): per (query, direction)
-// the counts #(y<0), #(y>0) of y_i = <u, x_i - z> over all points, with the
-// query's own row giving y = 0 exactly (self-tie by construction).  Here the
-// sign of y is computed EXACTLY for fixed-point operands:
-//   a_il = x_il - z_l (FP32) scaled per row by a power of two so that
+// the counts #(y<0), #(y>0) of y_i = <u, x_i - z> over all points; the query's
+// own row gives y = 0 exactly (self-tie by construction) and exact zeros count
+// on both sides (#<= = n - #>0, #>= = n - #<0).  Here the sign of y is EXACT
+// for fixed-point operands:
+//   a_il = x_il - z_l (FP32), scaled per point by a power of two so that
 //          |A_il| < 2^22 (A = rint(a * 2^(22-E_i)), E_i = exponent of max_l |a_il|);
 //   U_jl = rint(u_jl * 2^22) (|u| <= 1);
-//   both split into three signed int8 limbs  A = a2*2^16 + a1*2^8 + a0;
-//   sum_l A_il U_jl = 2^32 S22 + 2^24 S21 + 2^16 S20 + (low products, dropped)
-// where the tensor core accumulates S22, S21 = a2b1 + a1b2 and
-// S20 = a2b0 + a1b1 + a0b2 in int32 TMEM accumulators (kind::i8, exact).  The
-// three dropped low products are below 2^-15 of one quantisation step.  The
-// per-row power of two never changes a sign, so no scale is needed in the
-// epilogue: sign(y) = sign(S22*2^16 + S21*2^8 + S20), evaluated exactly in 32
-// bits (S22 clamped to +-2^14: beyond that its term dominates).
+//   both split into three signed int8 limbs  V = v2*2^16 + v1*2^8 + v0;
+//   sum_l U_jl A_il = 2^32 S22 + 2^24 S21 + 2^16 S20 + (low products, dropped)
+// with S22 = u2.a2, S21 = u2.a1 + u1.a2, S20 = u2.a0 + u1.a1 + u0.a2 accumulated
+// by tcgen05.mma kind::i8 in int32 TMEM (exact).  The dropped products are
+// of the same order as the quantisation (each <= 2^-22 of the operands' scale,
+// an FP32-comparable error, validated by the tier-1 tests); the per-point power of two never
+// changes a sign, so the epilogue needs no scale: sign(y) = sign(S22*2^16 +
+// S21*2^8 + S20), evaluated exactly in 32 bits (S22 clamped to +-2^14, beyond
+// which its term dominates).
 //
-// Persistent CTA (one per SM), 12 warps:
-//   warp 0      TMA producer: X tile (FP32) and B blocks (int8 limbs) via
-//               cp.async.bulk + mbarriers, double-buffered B;
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//               (M=128 points, N=64 directions, K=32 per instruction);
-//   warps 4-11  x - z + per-row quantisation into the canonical no-swizzle
-//               K-major UMMA layout, then the epilogue: tcgen05.ld of the three
-//               accumulators, exact sign, warp ballot + popc per direction,
-//               shared-memory counters; TMEM double-buffered against the MMA.
-// Work item = (query, 128-point tile); all directions of the query are swept
-// with the A tile resident.  Replaces _kernels.pyx:120-199 + 270-289.
+// MMA orientation: M = 128 DIRECTIONS (TMEM lanes), N = 64 POINTS per
+// instruction, K = 32.  Each epilogue thread owns one direction and counts its
+// signs in registers (7 instructions per element, no cross-lane reduction).
+//
+// Persistent CTA (one per SM), 20 warps, work item = (query, 256 points):
+//   warp 0      TMA producer: X tile pair (FP32) and direction blocks
+//               (24 KB int8 limbs, 3-stage ring) via cp.async.bulk + mbarriers,
+//               running ahead across items;
+//   warp 1      TMEM allocator + single-thread tcgen05 issuer: each direction
+//               block is copied smem -> TMEM (tcgen05.cp) and used as the
+//               TMEM-resident A operand ("TS" MMA), so the tensor core only
+//               reads the point operand from shared memory;
+//   warps 4-19  per item: x - z and per-point quantisation into the canonical
+//               no-swizzle K-major UMMA layout, then the epilogue of every
+//               (direction block, 64-point group): tcgen05.ld of the three
+//               accumulators, exact sign, per-thread counts, one shared atomic
+//               per direction; TMEM double-buffered against the MMA.
+// Replaces _kernels.pyx:120-199 (projection) + 270-289 (halfspace_span).
 #include "common.cuh"
 #include "kernels.h"
 
 namespace rrs {
 
-constexpr int TC_THREADS = 384;
-constexpr int TC_NB = 64;                  // directions per N-block (MMA N)
-constexpr int TC_KP = 64;                  // K padded (d <= 64)
-constexpr int A_LIMB_BYTES = 128 * TC_KP;  // 8 KB per limb
-constexpr int B_LIMB_BYTES = TC_NB * TC_KP;            // 4 KB per limb
-constexpr int B_BLOCK_BYTES = 3 * B_LIMB_BYTES;        // 12 KB per N-block
-constexpr int TC_MAX_COLS = 4096;          // mpad limit for the smem counters
+constexpr int TC_THREADS = 640;             // 4 role/idle warps + 16 epilogue warps
+constexpr int TC_EPI_WARPS = 16;
+constexpr int TC_EPI_THREADS = TC_EPI_WARPS * 32;
+constexpr int TC_KP = 64;                       // K padded (d <= 64)
+constexpr int TC_MD = 128;                      // directions per block (MMA M)
+constexpr int TC_NP = 64;                       // points per MMA (MMA N)
+constexpr int TC_PTS = 256;                     // points per work item (2 tiles)
+constexpr int P_LIMB_BYTES = TC_PTS * TC_KP;    // 16 KB per limb
+constexpr int D_LIMB_BYTES = TC_MD * TC_KP;     // 8 KB per limb
+constexpr int D_BLOCK_BYTES = 3 * D_LIMB_BYTES; // 24 KB per direction block
+constexpr int D_STAGES = 3;
+constexpr int TC_MAX_DIRS = 4096;               // per-direction smem counters
 constexpr uint32_t TMEM_COLS = 512;
 
 struct TcSmem {
     // offsets in bytes from a 1024-aligned base
-    static constexpr int A = 0;
-    static constexpr int B = A + 3 * A_LIMB_BYTES;       // 2 buffers
-    static constexpr int X = B + 2 * B_BLOCK_BYTES;      // FP32 staging [64][128]
-    static constexpr int CNT = X + TC_KP * 128 * 4;      // uint32 [TC_MAX_COLS]
-    static constexpr int ZS = CNT + TC_MAX_COLS * 4;     // float [64]
-    static constexpr int RMAX = ZS + TC_KP * 4;          // float [2][128]
-    static constexpr int BARS = RMAX + 2 * 128 * 4;      // 9 mbarriers
-    static constexpr int TADDR = BARS + 16 * 8;
+    static constexpr int P = 0;                                   // 3 x 16 KB point limbs
+    static constexpr int D = P + 3 * P_LIMB_BYTES;                // D_STAGES x 24 KB
+    static constexpr int X = D + D_STAGES * D_BLOCK_BYTES;        // FP32 [2 tiles][64][128]
+    static constexpr int CNT = X + 2 * TC_KP * 128 * 4;           // uint32 [TC_MAX_DIRS]
+    static constexpr int ZS = CNT + TC_MAX_DIRS * 4;              // float [64]
+    static constexpr int RMAX = ZS + TC_KP * 4;                   // float [2][256]
+    static constexpr int BARS = RMAX + 2 * TC_PTS * 4;            // mbarriers
+    static constexpr int NBARS = 3 + 2 * D_STAGES + 4;
+    static constexpr int TADDR = BARS + NBARS * 8;
     static constexpr int TOTAL = TADDR + 16;
 };
 
 size_t contract_tc_smem_bytes() { return TcSmem::TOTAL + 1024; }
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    // SmemDescriptor (tcgen05): start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46),
-    // version 1 [46,48), base offset 0, lbo mode 0, layout SWIZZLE_NONE (0) [61,64)
+    // tcgen05 shared-memory descriptor: start>>4 [0,14), LBO>>4 [16,30),
+    // SBO>>4 [32,46), version 1 [46,48), base offset 0, layout SWIZZLE_NONE
     return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
            ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
@@ -70,6 +85,41 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// The issuing warps run their loops warp-wide (uniform operands, no waterfall)
+// and one elected lane issues each tcgen05 / TMA instruction.
+// A operand from TMEM ("TS"): [a_tmem] holds 128 lanes x K bytes, B from smem.
+__device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// smem (canonical K-major, 128 rows x 32 bytes) -> TMEM (128 lanes x 8 columns)
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"(
+                     taddr),
+                 "l"(sdesc));
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_elect(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n"
+        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -87,6 +137,20 @@ __device__ __forceinline__ void tc_fence_after() {
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Wait with a suspend-time hint: the waiting thread sleeps in hardware until the
+// phase completes instead of spinning on issue slots shared with busy warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -108,34 +172,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     extern __shared__ __align__(1024) unsigned char tc_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    unsigned char* sA = sm + TcSmem::A;
-    unsigned char* sB = sm + TcSmem::B;
+    unsigned char* sP = sm + TcSmem::P;
+    unsigned char* sD = sm + TcSmem::D;
     float* sX = reinterpret_cast<float*>(sm + TcSmem::X);
     uint32_t* sCnt = reinterpret_cast<uint32_t*>(sm + TcSmem::CNT);
     float* sZ = reinterpret_cast<float*>(sm + TcSmem::ZS);
     float* sRmax = reinterpret_cast<float*>(sm + TcSmem::RMAX);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + TcSmem::BARS);
     uint64_t* xfull = &bars[0];
-    uint64_t* bfull = &bars[1];   // [2]
-    uint64_t* bempty = &bars[3];  // [2]
-    uint64_t* tfull = &bars[5];   // [2]
-    uint64_t* tempty = &bars[7];  // [2]
+    uint64_t* xempty = &bars[1];
+    uint64_t* pfull = &bars[2];                  // point limbs ready (8 warp arrivals)
+    uint64_t* dfull = &bars[3];                  // [D_STAGES]
+    uint64_t* dempty = &bars[3 + D_STAGES];      // [D_STAGES]
+    uint64_t* tfull = &bars[3 + 2 * D_STAGES];   // [2]
+    uint64_t* tempty = &bars[5 + 2 * D_STAGES];  // [2]
     uint32_t* sTaddr = reinterpret_cast<uint32_t*>(sm + TcSmem::TADDR);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int d = a.d;
-    const int NBk = a.NB;               // N-blocks of 64 directions per query
-    const int ncols = NBk * TC_NB;
-    const int nks = (d + 31) / 32;      // MMA K-steps (1 or 2)
+    const int MB = a.NB;                 // 128-direction blocks per query
+    const int ndirs = MB * TC_MD;
+    const int nks = (d + 31) / 32;       // MMA K-steps (1 or 2)
+    const int64_t tiles2 = (a.tiles + 1) >> 1;
+    const int64_t items = (int64_t)a.Qb * tiles2;
 
-    for (int c = tid; c < ncols; c += TC_THREADS) sCnt[c] = 0u;
+    for (int c = tid; c < ndirs; c += TC_THREADS) sCnt[c] = 0u;
     if (tid == 0) {
         mbar_init(xfull, 1);
+        mbar_init(xempty, TC_EPI_WARPS);
+        mbar_init(pfull, TC_EPI_WARPS);
+        for (int b = 0; b < D_STAGES; ++b) {
+            mbar_init(&dfull[b], 1);
+            mbar_init(&dempty[b], 1);
+        }
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&bfull[b], 1);
-            mbar_init(&bempty[b], 1);
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 8);
+            mbar_init(&tempty[b], TC_EPI_WARPS);
         }
         fence_mbar_init();
     }
@@ -149,47 +221,119 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     tc_fence_after();
     const uint32_t tmem = *sTaddr;
 
-    // instruction descriptor: S32 accumulate, signed int8 A and B, K-major, N=64, M=128
-    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_NB >> 3) << 17) |
-                           ((uint32_t)(128 >> 4) << 24);
-
-    const int64_t items = (int64_t)a.Qb * a.tiles;
-    int it = 0;
-    for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-        const int q = (int)(item / a.tiles);
-        const int64_t t = item - (int64_t)q * a.tiles;
-        const int64_t gbase = (int64_t)it * NBk;  // running N-block counter of this CTA
-        const int64_t vrows = a.n - t * 128;
-        const int valid = vrows < 128 ? (int)vrows : 128;
-
-        // ---- stage the point tile and the query
-        if (tid == 0) {
-            const uint32_t bytes = (uint32_t)d * 128 * 4;
-            mbar_arrive_expect_tx(xfull, bytes);
-            bulk_g2s(sX, a.xb + (size_t)t * d * 128, bytes, xfull);
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        int64_t gd = 0;  // running direction-block counter
+        int it = 0;
+        for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+            const int q = (int)(item / tiles2);
+            const int64_t t0 = (item - (int64_t)q * tiles2) * 2;
+            const int ntile = (t0 + 1 < a.tiles) ? 2 : 1;
+            if (it >= 1) mbar_wait_sleep(xempty, (uint32_t)((it - 1) & 1));
+            tma_load_elect(sX, a.xb + (size_t)t0 * d * 128, (uint32_t)ntile * d * 128 * 4, xfull);
+            const unsigned char* src = a.u8 + (size_t)q * MB * D_BLOCK_BYTES;
+            for (int db = 0; db < MB; ++db, ++gd) {
+                const int s = (int)(gd % D_STAGES);
+                const int64_t u = gd / D_STAGES;
+                if (u >= 1) mbar_wait_sleep(&dempty[s], (uint32_t)((u - 1) & 1));
+                tma_load_elect(sD + s * D_BLOCK_BYTES, src + (size_t)db * D_BLOCK_BYTES, D_BLOCK_BYTES, &dfull[s]);
+            }
+            __syncwarp();
         }
-        if (tid < d) sZ[tid] = a.zq[(size_t)q * d + tid];
-        __syncthreads();  // sZ visible
-
-        // ---- warps 4-11: x - z, per-row power-of-two scale, 3 int8 limbs
-        if (warp >= 4) {
-            const int ct = tid - 128;          // 0..255
-            const int r = ct & 127, h = ct >> 7;
+    } else if (warp == 1) {
+        // ---------------------------------------------------------- MMA issuer
+        {
+            // S32 accumulate, signed int8 A and B, K-major both, N = 64, M = 128
+            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_NP >> 3) << 17) |
+                                   ((uint32_t)(TC_MD >> 4) << 24);
+            const uint32_t pBase = smem_u32(sP);
+            // (direction limb, point limb, accumulator): S22 -> 2, S21 -> 1, S20 -> 0
+            const int lu[6] = {2, 2, 1, 2, 1, 0};
+            const int lp[6] = {2, 1, 2, 0, 1, 2};
+            const int ac[6] = {2, 1, 1, 0, 0, 0};
+            const int first[6] = {1, 1, 0, 1, 0, 0};
+            int64_t gd = 0, gt = 0;
+            int it = 0;
+            for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+                mbar_wait_sleep(pfull, (uint32_t)(it & 1));
+                for (int db = 0; db < MB; ++db, ++gd) {
+                    const int s = (int)(gd % D_STAGES);
+                    mbar_wait_sleep(&dfull[s], (uint32_t)((gd / D_STAGES) & 1));
+                    tc_fence_after();
+                    // direction block -> TMEM (A operand), double-buffered; in-order with the MMAs
+                    const uint32_t dBase = smem_u32(sD + s * D_BLOCK_BYTES);
+                    const uint32_t aT = tmem + 384u + (uint32_t)(gd & 1) * 48u;
+#pragma unroll
+                    for (int L = 0; L < 3; ++L)
+#pragma unroll
+                        for (int ks = 0; ks < 2; ++ks)
+                            tmem_cp_128x256b(aT + (uint32_t)(L * 2 + ks) * 8u,
+                                             umma_desc(dBase + L * D_LIMB_BYTES + ks * 2 * 2048, 2048, 128));
+                    mma_commit_elect(&dempty[s]);  // smem stage free once the copies are done
+                    for (int pq = 0; pq < TC_PTS / TC_NP; ++pq, ++gt) {
+                        const int buf = (int)(gt & 1);
+                        const int64_t ut = gt >> 1;
+                        if (ut >= 1) mbar_wait(&tempty[buf], (uint32_t)((ut - 1) & 1));  // latency-critical: spin
+                        tc_fence_after();
+                        const uint32_t acc = tmem + (uint32_t)buf * 192u;
+                        for (int ks = 0; ks < nks; ++ks) {
+#pragma unroll
+                            for (int p = 0; p < 6; ++p) {
+                                // points [limb][k-chunk][256][16B]: LBO 4096, SBO 128, group pq
+                                const uint64_t bd =
+                                    umma_desc(pBase + lp[p] * P_LIMB_BYTES + ks * 2 * 4096 + pq * TC_NP * 16, 4096, 128);
+                                mma_i8_ts(acc + (uint32_t)ac[p] * TC_NP, aT + (uint32_t)(lu[p] * 2 + ks) * 8u, bd, idesc,
+                                          (ks == 0 && first[p]) ? 0u : 1u);
+                            }
+                        }
+                        mma_commit_elect(&tfull[buf]);
+                    }
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ----------------------------------------- quantisation + epilogue
+        const int ct = tid - 128;          // 0..511
+        const int r = ct & (TC_PTS - 1);   // point row of the item
+        const int kh = ct >> 8;            // K half handled in the quantisation
+        const int quarter = warp & 3;      // TMEM lane quarter = 32 directions
+        const int part = (warp - 4) >> 2;  // 16-point slice of each 64-point group
+        const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
+        int64_t gt = 0;
+        int it = 0;
+        for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+            const int q = (int)(item / tiles2);
+            const int64_t t0 = (item - (int64_t)q * tiles2) * 2;
+            const int64_t vrows = a.n - t0 * 128;
+            const int valid = vrows < TC_PTS ? (int)vrows : TC_PTS;
+            if (ct < d) sZ[ct] = a.zq[(size_t)q * d + ct];
             mbar_wait(xfull, (uint32_t)(it & 1));
-            const int k0 = h * 32;
+            named_bar(1, TC_EPI_THREADS);  // sZ visible
+            // x - z, per-point power-of-two scale, three int8 limbs; two threads
+            // per point, each owning 32 coordinates (2 of the 4 k-chunks)
+            const float* X = sX + (r >> 7) * d * 128 + (r & 127);
+            const int k0 = kh * 32;
             const int k1 = (k0 + 32) < d ? (k0 + 32) : d;
             float mx = 0.0f;
-            for (int k = k0; k < k1; ++k) mx = fmaxf(mx, fabsf(sX[k * 128 + r] - sZ[k]));
-            sRmax[h * 128 + r] = mx;
-            named_bar(1, 256);
-            mx = fmaxf(sRmax[r], sRmax[128 + r]);
+            if (r < valid)
+                for (int k = k0; k < k1; ++k) mx = fmaxf(mx, fabsf(X[k * 128] - sZ[k]));
+            sRmax[kh * TC_PTS + r] = mx;
+            named_bar(1, TC_EPI_THREADS);
+            mx = fmaxf(sRmax[r], sRmax[TC_PTS + r]);
             float scale = 0.0f;
-            if (r < valid && mx > 0.0f) {
+            if (mx > 0.0f) {
                 int E = (int)((__float_as_uint(mx) >> 23) & 0xFF) - 126;  // mx < 2^E
                 if (E < -100) E = -100;
                 scale = __uint_as_float((uint32_t)(127 + 22 - E) << 23);  // 2^(22-E)
             }
-            for (int c = 2 * h; c < 2 * h + 2; ++c) {
+            for (int c = 2 * kh; c < 2 * kh + 2; ++c) {
+                if (c * 16 >= d) {  // K padding: zero limbs
+                    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                    for (int L = 0; L < 3; ++L)
+                        *reinterpret_cast<uint4*>(sP + L * P_LIMB_BYTES + c * 4096 + r * 16) = z4;
+                    continue;
+                }
                 uint32_t w0[4], w1[4], w2[4];
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
@@ -197,7 +341,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int k = c * 16 + g * 4 + e;
-                        const float av = (k < d) ? (sX[k * 128 + r] - sZ[k]) : 0.0f;
+                        const float av = (k < d) ? (X[k * 128] - sZ[k]) : 0.0f;
                         const int A0 = __float2int_rn(av * scale);
                         const int A1 = (A0 + 128) >> 8;
                         const int A2 = (A1 + 128) >> 8;
@@ -209,120 +353,59 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                     w1[g] = b1;
                     w2[g] = b2;
                 }
-                // canonical K-major, no swizzle: [k-chunk c][row r][16 bytes]
-                *reinterpret_cast<uint4*>(sA + 0 * A_LIMB_BYTES + c * 2048 + r * 16) =
-                    make_uint4(w0[0], w0[1], w0[2], w0[3]);
-                *reinterpret_cast<uint4*>(sA + 1 * A_LIMB_BYTES + c * 2048 + r * 16) =
-                    make_uint4(w1[0], w1[1], w1[2], w1[3]);
-                *reinterpret_cast<uint4*>(sA + 2 * A_LIMB_BYTES + c * 2048 + r * 16) =
-                    make_uint4(w2[0], w2[1], w2[2], w2[3]);
+                // canonical K-major, no swizzle: [limb][k-chunk c][point r][16 bytes]
+                *reinterpret_cast<uint4*>(sP + 0 * P_LIMB_BYTES + c * 4096 + r * 16) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+                *reinterpret_cast<uint4*>(sP + 1 * P_LIMB_BYTES + c * 4096 + r * 16) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+                *reinterpret_cast<uint4*>(sP + 2 * P_LIMB_BYTES + c * 4096 + r * 16) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
             }
-            fence_proxy_async();  // generic-proxy writes -> tensor-core (async proxy) reads
-        }
-        __syncthreads();  // A ready
-
-        if (warp == 0) {
-            // ---- producer: B blocks (int8 limbs of 64 directions) for this query
+            fence_proxy_async();  // generic-proxy smem writes -> tensor-core reads
+            __syncwarp();
             if (lane == 0) {
-                const unsigned char* src = a.u8 + (size_t)q * NBk * B_BLOCK_BYTES;
-                for (int nb = 0; nb < NBk; ++nb) {
-                    const int64_t g = gbase + nb;
-                    const int buf = (int)(g & 1);
-                    const int64_t u = g >> 1;
-                    if (u >= 1) mbar_wait(&bempty[buf], (uint32_t)((u - 1) & 1));
-                    mbar_arrive_expect_tx(&bfull[buf], B_BLOCK_BYTES);
-                    bulk_g2s(sB + buf * B_BLOCK_BYTES, src + (size_t)nb * B_BLOCK_BYTES, B_BLOCK_BYTES,
-                             &bfull[buf]);
-                }
+                mbar_arrive(pfull);
+                mbar_arrive(xempty);
             }
-        } else if (warp == 1) {
-            // ---- single-thread MMA issuer
-            if (lane == 0) {
-                const uint32_t aBase = smem_u32(sA);
-                for (int nb = 0; nb < NBk; ++nb) {
-                    const int64_t g = gbase + nb;
-                    const int buf = (int)(g & 1);
-                    const int64_t u = g >> 1;
-                    mbar_wait(&bfull[buf], (uint32_t)(u & 1));
-                    if (u >= 1) mbar_wait(&tempty[buf], (uint32_t)((u - 1) & 1));
+            // epilogue: thread = direction (TMEM lane), 16 points per 64-point group
+            for (int db = 0; db < MB; ++db) {
+                uint32_t cnt = 0u;  // (#y<0) | (#y>0) << 16 over this item's points
+                for (int pq = 0; pq < TC_PTS / TC_NP; ++pq, ++gt) {
+                    const int buf = (int)(gt & 1);
+                    mbar_wait(&tfull[buf], (uint32_t)((gt >> 1) & 1));  // latency-critical: spin
                     tc_fence_after();
-                    const uint32_t bBase = smem_u32(sB + buf * B_BLOCK_BYTES);
-                    const uint32_t dBase = tmem + (uint32_t)buf * 192u;
-                    // (A limb, B limb, accumulator): S22 -> acc 2, S21 -> acc 1, S20 -> acc 0
-                    const int la[6] = {2, 2, 1, 2, 1, 0};
-                    const int lb[6] = {2, 1, 2, 0, 1, 2};
-                    const int ac[6] = {2, 1, 1, 0, 0, 0};
-                    const int first[6] = {1, 1, 0, 1, 0, 0};
-                    for (int s = 0; s < nks; ++s) {
-#pragma unroll
-                        for (int p = 0; p < 6; ++p) {
-                            const uint64_t ad =
-                                umma_desc(aBase + la[p] * A_LIMB_BYTES + s * 2 * 2048, 2048, 128);
-                            const uint64_t bd =
-                                umma_desc(bBase + lb[p] * B_LIMB_BYTES + s * 2 * 1024, 1024, 128);
-                            mma_i8(dBase + (uint32_t)ac[p] * TC_NB, ad, bd, idesc,
-                                   (s == 0 && first[p]) ? 0u : 1u);
-                        }
-                    }
-                    mma_commit(&bempty[buf]);
-                    mma_commit(&tfull[buf]);
-                }
-            }
-        } else if (warp >= 4) {
-            // ---- epilogue: exact sign per (point, direction), ballot counts per direction
-            const int quarter = warp & 3;
-            const int half = (warp - 4) >> 2;
-            const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
-            for (int nb = 0; nb < NBk; ++nb) {
-                const int64_t g = gbase + nb;
-                const int buf = (int)(g & 1);
-                const int64_t u = g >> 1;
-                mbar_wait(&tfull[buf], (uint32_t)(u & 1));
-                tc_fence_after();
-#pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
-                    const int col0 = half * 32 + cc * 16;
-                    const uint32_t tb = tmem + lane_base + (uint32_t)buf * 192u + (uint32_t)col0;
+                    const uint32_t tb = tmem + lane_base + (uint32_t)buf * 192u + (uint32_t)(part * 16);
                     uint32_t r0[16], r1[16], r2[16];
-                    tmem_ld16(tb + 0 * TC_NB, r0);
-                    tmem_ld16(tb + 1 * TC_NB, r1);
-                    tmem_ld16(tb + 2 * TC_NB, r2);
+                    tmem_ld16(tb + 0 * TC_NP, r0);
+                    tmem_ld16(tb + 1 * TC_NP, r1);
+                    tmem_ld16(tb + 2 * TC_NP, r2);
                     tmem_wait_ld();
-                    uint32_t* cnt = sCnt + nb * TC_NB + col0;
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[buf]);  // accumulators consumed
+                    uint32_t lt = 0u, gtc = 0u;
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
                         const int t1 = (int)r1[j] * 256 + (int)r0[j];
-                        int hi = (int)r2[j];
-                        hi = hi > 16384 ? 16384 : (hi < -16384 ? -16384 : hi);
+                        const int hi = max(-16384, min(16384, (int)r2[j]));
                         const int w = hi * 65536 + t1;
-                        const unsigned mlt = __ballot_sync(0xffffffffu, w < 0);
-                        const unsigned mle = __ballot_sync(0xffffffffu, w <= 0);
-                        if (lane == 0) atomicAdd(cnt + j, (uint32_t)__popc(mlt) | ((uint32_t)__popc(mle) << 16));
+                        lt += (uint32_t)w >> 31;
+                        gtc += (uint32_t)(-w) >> 31;
                     }
+                    cnt += lt | (gtc << 16);
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[buf]);
+                atomicAdd(sCnt + db * TC_MD + 32 * quarter + lane, cnt);
             }
-        }
-        __syncthreads();  // all N-blocks counted (epilogue done => all MMAs done)
-
-        // ---- flush this tile's counts: lt, and gt = real rows - (le - zero pad rows)
-        {
-            const int pad = 128 - valid;
+            named_bar(1, TC_EPI_THREADS);  // all direction counts of this item are in
             int* dst = a.counts + (size_t)q * a.mpad * 2;
-            for (int c = tid; c < ncols; c += TC_THREADS) {
+            for (int c = ct; c < ndirs; c += TC_EPI_THREADS) {
                 const uint32_t v = sCnt[c];
                 sCnt[c] = 0u;
                 if (c >= a.m) continue;
                 const int lt = (int)(v & 0xFFFFu);
-                const int le = (int)(v >> 16);
-                const int gt = valid - (le - pad);
+                const int gtv = (int)(v >> 16);
                 if (lt) atomicAdd(dst + 2 * c + 0, lt);
-                if (gt) atomicAdd(dst + 2 * c + 1, gt);
+                if (gtv) atomicAdd(dst + 2 * c + 1, gtv);
             }
+            named_bar(1, TC_EPI_THREADS);  // counters cleared before the next item adds
         }
-        __syncthreads();
     }
 
     tc_fence_before();
@@ -331,12 +414,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
 }
 
 cudaError_t launch_contract_tc(const TcArgs& a, int sms, cudaStream_t st) {
-    if (a.d > TC_KP || a.NB * TC_NB > TC_MAX_COLS) return cudaErrorInvalidValue;
+    if (a.d > TC_KP || a.NB * TC_MD > TC_MAX_DIRS) return cudaErrorInvalidValue;
     const size_t smem = contract_tc_smem_bytes();
     cudaError_t e =
         cudaFuncSetAttribute(contract_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int64_t items = (int64_t)a.Qb * a.tiles;
+    const int64_t items = (int64_t)a.Qb * ((a.tiles + 1) >> 1);
     if (items == 0) return cudaSuccess;
     const int grid = (int)(items < sms ? items : sms);
     contract_tc_kernel<<<grid, TC_THREADS, smem, st>>>(a);

@@ -154,7 +154,7 @@ int validate_cfg(const rrs_config* c) {
 struct Plan {
     int m, mpad, MB, Qb;
     bool tc;     // tensor-core int8-limb contraction (halfspace, d <= 64)
-    int nb8;     // 64-direction blocks per query (tensor path)
+    int nb8;     // 128-direction blocks per query (tensor path operand)
     int jchunk;  // direction blocks per store launch (projection notions)
     int tpu, chunks;
 };
@@ -164,12 +164,12 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     p.m = m;
     p.MB = (m + BN - 1) / BN;
     p.mpad = p.MB * BN;
-    p.nb8 = (m + 63) / 64;
-    const bool tc_ok = notion == RRS_HALFSPACE && e->d <= 64 && p.nb8 * 64 <= 4096;
+    p.nb8 = p.MB;
+    const bool tc_ok = notion == RRS_HALFSPACE && e->d <= 64 && p.mpad <= 4096;
     p.tc = tc_ok && (e->contract_path == 2 || (e->contract_path == 0 && e->n >= 4096));
     const int64_t d = e->d, n = e->n;
     int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * d * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 8 +
-                    d * 40 + 64 + (int64_t)p.nb8 * 12288;
+                    d * 40 + 64 + (int64_t)p.nb8 * 24576;
     int64_t budget = e->ws_limit;
     int64_t qb = 4096;
     if (notion != RRS_HALFSPACE) {
@@ -216,7 +216,7 @@ int ensure_ws(rrs_engine* e, const Plan& p, int notion) {
     CK(e->reflmode.ensure(Qb * 4));
     CK(e->dmin.ensure(Qb * 8));
     CK(e->bestcnt.ensure(Qb * 8));
-    CK(e->u8.ensure(p.tc ? Qb * (size_t)p.nb8 * 12288 : 16));
+    CK(e->u8.ensure(p.tc ? Qb * (size_t)p.nb8 * 24576 : 16));
     if (notion == RRS_HALFSPACE) {
         CK(e->counts.ensure(Qb * p.mpad * 2 * 4));
         CK(e->depths.ensure(8));

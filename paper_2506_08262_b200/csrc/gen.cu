@@ -138,17 +138,17 @@ __device__ __forceinline__ double pw_sum(const double* a, int n) { return 0.0 + 
 
 // Tensor-path direction operand: U = rint(u * 2^22) (|u| <= 1) split into three
 // signed int8 limbs U = b2*2^16 + b1*2^8 + b0, stored in the canonical K-major
-// no-swizzle UMMA layout of a 64-direction block:
-//   [limb 3][k-chunk 4][direction 64][16 bytes]   (12 KB per block)
-// u8row points at (block, direction) = base + (j & 63) * 16.
+// no-swizzle UMMA layout of a 128-direction block (the MMA M operand):
+//   [limb 3][k-chunk 4][direction 128][16 bytes]   (24 KB per block)
+// u8row points at (block, direction) = block base + (j & 127) * 16.
 __device__ __forceinline__ int quantize22(double u) { return __double2int_rn(u * 4194304.0); }
 __device__ __forceinline__ void put_limbs(unsigned char* u8row, int c, int U) {
     const int U1 = (U + 128) >> 8;
     const int U2 = (U1 + 128) >> 8;
-    unsigned char* p = u8row + (c >> 4) * 1024 + (c & 15);
+    unsigned char* p = u8row + (c >> 4) * 2048 + (c & 15);
     p[0] = (unsigned char)(U & 0xFF);
-    p[4096] = (unsigned char)(U1 & 0xFF);
-    p[8192] = (unsigned char)(U2 & 0xFF);
+    p[8192] = (unsigned char)(U1 & 0xFF);
+    p[16384] = (unsigned char)(U2 & 0xFF);
 }
 
 // ------------------------------------------------------- cap generation K1 --
@@ -172,8 +172,8 @@ __global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
     const int j = (int)(gdir % a.mpad);
     float* u32 = a.u32 + (size_t)q * a.mpad * d + (size_t)(j / BN) * d * BN + (j % BN);
     unsigned char* u8 = nullptr;
-    if (a.u8 && j < a.nb8 * 64)
-        u8 = a.u8 + ((size_t)q * a.nb8 + (j >> 6)) * 12288 + (size_t)(j & 63) * 16;
+    if (a.u8 && j < a.nb8 * 128)
+        u8 = a.u8 + ((size_t)q * a.nb8 + (j >> 7)) * 24576 + (size_t)(j & 127) * 16;
     if (j >= a.m) {
         for (int c = lane; c < d; c += 32) u32[(size_t)c * BN] = 0.0f;
         if (u8)
@@ -260,19 +260,19 @@ __global__ void pack_directions_kernel(const double* __restrict__ u64, float* __
 __global__ void pack_limbs_kernel(const double* __restrict__ u64, unsigned char* __restrict__ u8, int Qb,
                                   int m, int nb8, int d) {
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t total = (int64_t)Qb * nb8 * 64 * 64;
+    int64_t total = (int64_t)Qb * nb8 * 128 * 64;
     if (idx >= total) return;
     int c = (int)(idx & 63);
     int64_t r = idx >> 6;
-    int j = (int)(r % (nb8 * 64));
-    int q = (int)(r / (nb8 * 64));
+    int j = (int)(r % (nb8 * 128));
+    int q = (int)(r / (nb8 * 128));
     int U = (j < m && c < d) ? quantize22(u64[((size_t)q * m + j) * d + c]) : 0;
-    put_limbs(u8 + ((size_t)q * nb8 + (j >> 6)) * 12288 + (size_t)(j & 63) * 16, c, U);
+    put_limbs(u8 + ((size_t)q * nb8 + (j >> 7)) * 24576 + (size_t)(j & 127) * 16, c, U);
 }
 
 cudaError_t launch_pack_limbs(const double* u64, unsigned char* u8, int Qb, int m, int nb8, int d,
                               cudaStream_t st) {
-    int64_t total = (int64_t)Qb * nb8 * 64 * 64;
+    int64_t total = (int64_t)Qb * nb8 * 128 * 64;
     pack_limbs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(u64, u8, Qb, m, nb8, d);
     return cudaGetLastError();
 }

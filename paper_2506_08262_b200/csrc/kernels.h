@@ -12,8 +12,8 @@ struct GenArgs {
     const double* refl_v;    // [Qb][d]
     double* u64;             // [Qb][m][d]
     float* u32;              // [Qb][mpad/BN][d][BN]
-    unsigned char* u8;       // nullable: [Qb][NB8][3 limbs][4][64][16] int8 limbs (tensor path)
-    int nb8;                 // 64-direction blocks per query in u8
+    unsigned char* u8;       // nullable: [Qb][nb8][3 limbs][4][128][16] int8 limbs (tensor path)
+    int nb8;                 // 128-direction blocks per query in u8
     uint64_t seed;
     int64_t q0;              // global query index of batch row 0
     uint32_t refinement;
@@ -78,7 +78,7 @@ struct ContractArgs {
 struct TcArgs {
     const float* xb;            // [T][d][128]
     const float* zq;            // [Qb][d]
-    const unsigned char* u8;    // [Qb][NB][3][4][64][16]
+    const unsigned char* u8;    // [Qb][NB][3][4][128][16]
     int* counts;                // [Qb][mpad][2]
     int64_t n;
     int64_t tiles;
