@@ -16,8 +16,9 @@
 // of the same order as the quantisation (each <= 2^-22 of the operands' scale,
 // an FP32-comparable error, validated by the tier-1 tests); the per-point power of two never
 // changes a sign, so the epilogue needs no scale: sign(y) = sign(S22*2^16 +
-// S21*2^8 + S20), evaluated exactly in 32 bits (S22 clamped to +-2^14, beyond
-// which its term dominates).
+// S21*2^8 + S20), evaluated exactly in 32 bits as the sign of
+// (S22*2^8 + S21)*2^7 + floor(S20/2) (4 instructions per element).  Only
+// #(y<0) is counted per element; #(y>0) = rows - coinciding rows - #(y<0).
 //
 // MMA orientation: M = 128 DIRECTIONS (TMEM lanes), N = 64 POINTS per
 // instruction, K = 32.  Each epilogue thread owns one direction and counts its
@@ -64,7 +65,8 @@ struct TcSmem {
     static constexpr int CNT = X + 2 * TC_KP * 128 * 4;           // uint32 [TC_MAX_DIRS]
     static constexpr int ZS = CNT + TC_MAX_DIRS * 4;              // float [64]
     static constexpr int RMAX = ZS + TC_KP * 4;                   // float [2][256]
-    static constexpr int BARS = RMAX + 2 * TC_PTS * 4;            // mbarriers
+    static constexpr int ZROWS = RMAX + 2 * TC_PTS * 4;           // uint32 (+ pad)
+    static constexpr int BARS = ZROWS + 16;                       // mbarriers
     static constexpr int NBARS = 3 + 2 * D_STAGES + 4;
     static constexpr int TADDR = BARS + NBARS * 8;
     static constexpr int TOTAL = TADDR + 16;
@@ -178,6 +180,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     uint32_t* sCnt = reinterpret_cast<uint32_t*>(sm + TcSmem::CNT);
     float* sZ = reinterpret_cast<float*>(sm + TcSmem::ZS);
     float* sRmax = reinterpret_cast<float*>(sm + TcSmem::RMAX);
+    uint32_t* sZrows = reinterpret_cast<uint32_t*>(sm + TcSmem::ZROWS);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + TcSmem::BARS);
     uint64_t* xfull = &bars[0];
     uint64_t* xempty = &bars[1];
@@ -197,6 +200,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     const int64_t items = (int64_t)a.Qb * tiles2;
 
     for (int c = tid; c < ndirs; c += TC_THREADS) sCnt[c] = 0u;
+    if (tid == 0) *sZrows = 0u;
     if (tid == 0) {
         mbar_init(xfull, 1);
         mbar_init(xempty, TC_EPI_WARPS);
@@ -320,6 +324,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
             sRmax[kh * TC_PTS + r] = mx;
             named_bar(1, TC_EPI_THREADS);
             mx = fmaxf(sRmax[r], sRmax[TC_PTS + r]);
+            {
+                // rows that coincide with the query (x - z == 0): ties on both sides
+                const unsigned zb = __ballot_sync(0xffffffffu, kh == 0 && r < valid && mx == 0.0f);
+                if (lane == 0 && zb) atomicAdd(sZrows, (uint32_t)__popc(zb));
+            }
             float scale = 0.0f;
             if (mx > 0.0f) {
                 int E = (int)((__float_as_uint(mx) >> 23) & 0xFF) - 126;  // mx < 2^E
@@ -366,7 +375,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
             }
             // epilogue: thread = direction (TMEM lane), 16 points per 64-point group
             for (int db = 0; db < MB; ++db) {
-                uint32_t cnt = 0u;  // (#y<0) | (#y>0) << 16 over this item's points
+                uint32_t cnt = 0u;  // #(y<0) over this item's points
                 for (int pq = 0; pq < TC_PTS / TC_NP; ++pq, ++gt) {
                     const int buf = (int)(gt & 1);
                     mbar_wait(&tfull[buf], (uint32_t)((gt >> 1) & 1));  // latency-critical: spin
@@ -380,30 +389,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[buf]);  // accumulators consumed
-                    uint32_t lt = 0u, gtc = 0u;
+                    // 2w = S22*2^16 + S21*2^8 + 2*floor(S20/2) = v - (S20 & 1), so
+                    // sign(w) == sign(v) exactly; |w| < 2^31 for d <= 64 (|S22| < 2^15.2)
+                    uint32_t lt = 0u;
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
-                        const int t1 = (int)r1[j] * 256 + (int)r0[j];
-                        const int hi = max(-16384, min(16384, (int)r2[j]));
-                        const int w = hi * 65536 + t1;
+                        const int x = (int)r2[j] * 256 + (int)r1[j];
+                        const int w = x * 128 + ((int)r0[j] >> 1);
                         lt += (uint32_t)w >> 31;
-                        gtc += (uint32_t)(-w) >> 31;
                     }
-                    cnt += lt | (gtc << 16);
+                    cnt += lt;
                 }
                 atomicAdd(sCnt + db * TC_MD + 32 * quarter + lane, cnt);
             }
             named_bar(1, TC_EPI_THREADS);  // all direction counts of this item are in
+            // #(y>0) = real rows - coinciding rows - #(y<0); an exact zero from a
+            // non-coinciding row (|y| below the quantisation error, inside the tie
+            // zone) lands on the positive side
+            const int zrows = (int)*sZrows;
             int* dst = a.counts + (size_t)q * a.mpad * 2;
             for (int c = ct; c < ndirs; c += TC_EPI_THREADS) {
-                const uint32_t v = sCnt[c];
+                const int lt = (int)sCnt[c];
                 sCnt[c] = 0u;
                 if (c >= a.m) continue;
-                const int lt = (int)(v & 0xFFFFu);
-                const int gtv = (int)(v >> 16);
+                const int gtv = valid - zrows - lt;
                 if (lt) atomicAdd(dst + 2 * c + 0, lt);
                 if (gtv) atomicAdd(dst + 2 * c + 1, gtv);
             }
+            named_bar(1, TC_EPI_THREADS);
+            if (ct == 0) *sZrows = 0u;
             named_bar(1, TC_EPI_THREADS);  // counters cleared before the next item adds
         }
     }
