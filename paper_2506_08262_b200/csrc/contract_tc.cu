@@ -25,32 +25,34 @@
 // signs in registers (7 instructions per element, no cross-lane reduction).
 //
 // Persistent CTA (one per SM), 20 warps, work item = (query, 256 points):
-//   warp 0      TMA producer: X tile pair (FP32) and direction blocks
-//               (24 KB int8 limbs, 3-stage ring) via cp.async.bulk + mbarriers,
-//               running ahead across items;
+//   warp 0      TMA producer: direction blocks (24 KB int8 limbs, 3-stage ring)
+//               via cp.async.bulk + mbarriers, running ahead across items;
+//   warps 2-3   converters: x - z (read from L2) and per-point quantisation
+//               into a double-buffered point operand, one item ahead of the MMA;
 //   warp 1      TMEM allocator + single-thread tcgen05 issuer: each direction
 //               block is copied smem -> TMEM (tcgen05.cp) and used as the
 //               TMEM-resident A operand ("TS" MMA), so the tensor core only
 //               reads the point operand from shared memory;
-//   warps 4-19  per item: x - z and per-point quantisation into the canonical
-//               no-swizzle K-major UMMA layout, then the epilogue of every
-//               (direction block, 64-point group): tcgen05.ld of the three
-//               accumulators, exact sign, per-thread counts, one shared atomic
-//               per direction; TMEM double-buffered against the MMA.
+//   warps 4-19  epilogue of every (direction block, 64-point group):
+//               tcgen05.ld of the three accumulators, exact sign, per-thread
+//               counts, one shared atomic per direction; TMEM double-buffered
+//               against the MMA.
 // Replaces _kernels.pyx:120-199 (projection) + 270-289 (halfspace_span).
 #include "common.cuh"
 #include "kernels.h"
 
 namespace rrs {
 
-constexpr int TC_THREADS = 640;             // 4 role/idle warps + 16 epilogue warps
+constexpr int TC_THREADS = 640;                 // 4 role warps + 16 epilogue warps
 constexpr int TC_EPI_WARPS = 16;
 constexpr int TC_EPI_THREADS = TC_EPI_WARPS * 32;
+constexpr int TC_CONV_THREADS = 64;             // warps 2-3 quantise the point operand
 constexpr int TC_KP = 64;                       // K padded (d <= 64)
 constexpr int TC_MD = 128;                      // directions per block (MMA M)
 constexpr int TC_NP = 64;                       // points per MMA (MMA N)
 constexpr int TC_PTS = 256;                     // points per work item (2 tiles)
 constexpr int P_LIMB_BYTES = TC_PTS * TC_KP;    // 16 KB per limb
+constexpr int P_BUF_BYTES = 3 * P_LIMB_BYTES;   // 48 KB per point operand
 constexpr int D_LIMB_BYTES = TC_MD * TC_KP;     // 8 KB per limb
 constexpr int D_BLOCK_BYTES = 3 * D_LIMB_BYTES; // 24 KB per direction block
 constexpr int D_STAGES = 3;
@@ -59,15 +61,12 @@ constexpr uint32_t TMEM_COLS = 512;
 
 struct TcSmem {
     // offsets in bytes from a 1024-aligned base
-    static constexpr int P = 0;                                   // 3 x 16 KB point limbs
-    static constexpr int D = P + 3 * P_LIMB_BYTES;                // D_STAGES x 24 KB
-    static constexpr int X = D + D_STAGES * D_BLOCK_BYTES;        // FP32 [2 tiles][64][128]
-    static constexpr int CNT = X + 2 * TC_KP * 128 * 4;           // uint32 [TC_MAX_DIRS]
-    static constexpr int ZS = CNT + TC_MAX_DIRS * 4;              // float [64]
-    static constexpr int RMAX = ZS + TC_KP * 4;                   // float [2][256]
-    static constexpr int ZROWS = RMAX + 2 * TC_PTS * 4;           // uint32 (+ pad)
+    static constexpr int P = 0;                                   // 2 x 48 KB point operands
+    static constexpr int D = P + 2 * P_BUF_BYTES;                 // D_STAGES x 24 KB
+    static constexpr int CNT = D + D_STAGES * D_BLOCK_BYTES;      // uint32 [TC_MAX_DIRS]
+    static constexpr int ZROWS = CNT + TC_MAX_DIRS * 4;           // uint32 [4] coinciding rows per item slot
     static constexpr int BARS = ZROWS + 16;                       // mbarriers
-    static constexpr int NBARS = 3 + 2 * D_STAGES + 4;
+    static constexpr int NBARS = 4 + 2 * D_STAGES + 4;
     static constexpr int TADDR = BARS + NBARS * 8;
     static constexpr int TOTAL = TADDR + 16;
 };
@@ -176,19 +175,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
         (reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     unsigned char* sP = sm + TcSmem::P;
     unsigned char* sD = sm + TcSmem::D;
-    float* sX = reinterpret_cast<float*>(sm + TcSmem::X);
     uint32_t* sCnt = reinterpret_cast<uint32_t*>(sm + TcSmem::CNT);
-    float* sZ = reinterpret_cast<float*>(sm + TcSmem::ZS);
-    float* sRmax = reinterpret_cast<float*>(sm + TcSmem::RMAX);
     uint32_t* sZrows = reinterpret_cast<uint32_t*>(sm + TcSmem::ZROWS);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + TcSmem::BARS);
-    uint64_t* xfull = &bars[0];
-    uint64_t* xempty = &bars[1];
-    uint64_t* pfull = &bars[2];                  // point limbs ready (8 warp arrivals)
-    uint64_t* dfull = &bars[3];                  // [D_STAGES]
-    uint64_t* dempty = &bars[3 + D_STAGES];      // [D_STAGES]
-    uint64_t* tfull = &bars[3 + 2 * D_STAGES];   // [2]
-    uint64_t* tempty = &bars[5 + 2 * D_STAGES];  // [2]
+    uint64_t* pfull = &bars[0];                  // [2] point operand quantised (2 converter warps)
+    uint64_t* pempty = &bars[2];                 // [2] MMAs reading it completed
+    uint64_t* dfull = &bars[4];                  // [D_STAGES]
+    uint64_t* dempty = &bars[4 + D_STAGES];      // [D_STAGES]
+    uint64_t* tfull = &bars[4 + 2 * D_STAGES];   // [2]
+    uint64_t* tempty = &bars[6 + 2 * D_STAGES];  // [2]
     uint32_t* sTaddr = reinterpret_cast<uint32_t*>(sm + TcSmem::TADDR);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -200,18 +195,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     const int64_t items = (int64_t)a.Qb * tiles2;
 
     for (int c = tid; c < ndirs; c += TC_THREADS) sCnt[c] = 0u;
-    if (tid == 0) *sZrows = 0u;
+    if (tid < 4) sZrows[tid] = 0u;
     if (tid == 0) {
-        mbar_init(xfull, 1);
-        mbar_init(xempty, TC_EPI_WARPS);
-        mbar_init(pfull, TC_EPI_WARPS);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&pfull[b], 2);
+            mbar_init(&pempty[b], 1);
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], TC_EPI_WARPS);
+        }
         for (int b = 0; b < D_STAGES; ++b) {
             mbar_init(&dfull[b], 1);
             mbar_init(&dempty[b], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], TC_EPI_WARPS);
         }
         fence_mbar_init();
     }
@@ -226,15 +220,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     const uint32_t tmem = *sTaddr;
 
     if (warp == 0) {
-        // ------------------------------------------------------------ producer
-        int64_t gd = 0;  // running direction-block counter
-        int it = 0;
-        for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        // ------------------------------------------- producer: direction blocks
+        int64_t gd = 0;
+        for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
             const int q = (int)(item / tiles2);
-            const int64_t t0 = (item - (int64_t)q * tiles2) * 2;
-            const int ntile = (t0 + 1 < a.tiles) ? 2 : 1;
-            if (it >= 1) mbar_wait_sleep(xempty, (uint32_t)((it - 1) & 1));
-            tma_load_elect(sX, a.xb + (size_t)t0 * d * 128, (uint32_t)ntile * d * 128 * 4, xfull);
             const unsigned char* src = a.u8 + (size_t)q * MB * D_BLOCK_BYTES;
             for (int db = 0; db < MB; ++db, ++gd) {
                 const int s = (int)(gd % D_STAGES);
@@ -245,61 +234,120 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
             __syncwarp();
         }
     } else if (warp == 1) {
-        // ---------------------------------------------------------- MMA issuer
-        {
-            // S32 accumulate, signed int8 A and B, K-major both, N = 64, M = 128
-            const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_NP >> 3) << 17) |
-                                   ((uint32_t)(TC_MD >> 4) << 24);
-            const uint32_t pBase = smem_u32(sP);
-            // (direction limb, point limb, accumulator): S22 -> 2, S21 -> 1, S20 -> 0
-            const int lu[6] = {2, 2, 1, 2, 1, 0};
-            const int lp[6] = {2, 1, 2, 0, 1, 2};
-            const int ac[6] = {2, 1, 1, 0, 0, 0};
-            const int first[6] = {1, 1, 0, 1, 0, 0};
-            int64_t gd = 0, gt = 0;
-            int it = 0;
-            for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-                mbar_wait_sleep(pfull, (uint32_t)(it & 1));
-                for (int db = 0; db < MB; ++db, ++gd) {
-                    const int s = (int)(gd % D_STAGES);
-                    mbar_wait_sleep(&dfull[s], (uint32_t)((gd / D_STAGES) & 1));
+        // -------------------------------------------------------- MMA issuer
+        // S32 accumulate, signed int8 A and B, K-major both, N = 64, M = 128
+        const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_NP >> 3) << 17) |
+                               ((uint32_t)(TC_MD >> 4) << 24);
+        // (direction limb, point limb, accumulator): S22 -> 2, S21 -> 1, S20 -> 0
+        const int lu[6] = {2, 2, 1, 2, 1, 0};
+        const int lp[6] = {2, 1, 2, 0, 1, 2};
+        const int ac[6] = {2, 1, 1, 0, 0, 0};
+        const int first[6] = {1, 1, 0, 1, 0, 0};
+        int64_t gd = 0, gt = 0;
+        int it = 0;
+        for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+            const int pb = it & 1;
+            mbar_wait_sleep(&pfull[pb], (uint32_t)((it >> 1) & 1));
+            const uint32_t pBase = smem_u32(sP + pb * P_BUF_BYTES);
+            for (int db = 0; db < MB; ++db, ++gd) {
+                const int s = (int)(gd % D_STAGES);
+                mbar_wait_sleep(&dfull[s], (uint32_t)((gd / D_STAGES) & 1));
+                tc_fence_after();
+                // direction block -> TMEM (A operand), double-buffered; in order with the MMAs
+                const uint32_t dBase = smem_u32(sD + s * D_BLOCK_BYTES);
+                const uint32_t aT = tmem + 384u + (uint32_t)(gd & 1) * 48u;
+#pragma unroll
+                for (int L = 0; L < 3; ++L)
+#pragma unroll
+                    for (int ks = 0; ks < 2; ++ks)
+                        tmem_cp_128x256b(aT + (uint32_t)(L * 2 + ks) * 8u,
+                                         umma_desc(dBase + L * D_LIMB_BYTES + ks * 2 * 2048, 2048, 128));
+                mma_commit_elect(&dempty[s]);  // smem stage free once the copies are done
+                for (int pq = 0; pq < TC_PTS / TC_NP; ++pq, ++gt) {
+                    const int buf = (int)(gt & 1);
+                    const int64_t ut = gt >> 1;
+                    if (ut >= 1) mbar_wait(&tempty[buf], (uint32_t)((ut - 1) & 1));
                     tc_fence_after();
-                    // direction block -> TMEM (A operand), double-buffered; in-order with the MMAs
-                    const uint32_t dBase = smem_u32(sD + s * D_BLOCK_BYTES);
-                    const uint32_t aT = tmem + 384u + (uint32_t)(gd & 1) * 48u;
+                    const uint32_t acc = tmem + (uint32_t)buf * 192u;
+                    for (int ks = 0; ks < nks; ++ks) {
 #pragma unroll
-                    for (int L = 0; L < 3; ++L)
-#pragma unroll
-                        for (int ks = 0; ks < 2; ++ks)
-                            tmem_cp_128x256b(aT + (uint32_t)(L * 2 + ks) * 8u,
-                                             umma_desc(dBase + L * D_LIMB_BYTES + ks * 2 * 2048, 2048, 128));
-                    mma_commit_elect(&dempty[s]);  // smem stage free once the copies are done
-                    for (int pq = 0; pq < TC_PTS / TC_NP; ++pq, ++gt) {
-                        const int buf = (int)(gt & 1);
-                        const int64_t ut = gt >> 1;
-                        if (ut >= 1) mbar_wait(&tempty[buf], (uint32_t)((ut - 1) & 1));  // latency-critical: spin
-                        tc_fence_after();
-                        const uint32_t acc = tmem + (uint32_t)buf * 192u;
-                        for (int ks = 0; ks < nks; ++ks) {
-#pragma unroll
-                            for (int p = 0; p < 6; ++p) {
-                                // points [limb][k-chunk][256][16B]: LBO 4096, SBO 128, group pq
-                                const uint64_t bd =
-                                    umma_desc(pBase + lp[p] * P_LIMB_BYTES + ks * 2 * 4096 + pq * TC_NP * 16, 4096, 128);
-                                mma_i8_ts(acc + (uint32_t)ac[p] * TC_NP, aT + (uint32_t)(lu[p] * 2 + ks) * 8u, bd, idesc,
-                                          (ks == 0 && first[p]) ? 0u : 1u);
-                            }
+                        for (int p = 0; p < 6; ++p) {
+                            // points [limb][k-chunk][256][16B]: LBO 4096, SBO 128, group pq
+                            const uint64_t bd =
+                                umma_desc(pBase + lp[p] * P_LIMB_BYTES + ks * 2 * 4096 + pq * TC_NP * 16, 4096, 128);
+                            mma_i8_ts(acc + (uint32_t)ac[p] * TC_NP, aT + (uint32_t)(lu[p] * 2 + ks) * 8u, bd, idesc,
+                                      (ks == 0 && first[p]) ? 0u : 1u);
                         }
-                        mma_commit_elect(&tfull[buf]);
                     }
+                    mma_commit_elect(&tfull[buf]);
                 }
             }
+            mma_commit_elect(&pempty[pb]);  // point operand free once this item's MMAs are done
         }
-    } else if (warp >= 4) {
-        // ----------------------------------------- quantisation + epilogue
+    } else if (warp < 4) {
+        // ------------------------- converters: x - z -> per-point scale -> int8 limbs
+        const int ct = tid - 64;  // 0..63, rows ct, ct+64, ct+128, ct+192
+        int it = 0;
+        for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+            const int pb = it & 1;
+            if (it >= 2) mbar_wait_sleep(&pempty[pb], (uint32_t)(((it >> 1) - 1) & 1));
+            const int q = (int)(item / tiles2);
+            const int64_t t0 = (item - (int64_t)q * tiles2) * 2;
+            const int64_t vrows = a.n - t0 * 128;
+            const int valid = vrows < TC_PTS ? (int)vrows : TC_PTS;
+            const float* zq = a.zq + (size_t)q * d;
+            unsigned char* P = sP + pb * P_BUF_BYTES;
+            uint32_t zcount = 0;
+            for (int rr = 0; rr < TC_PTS / TC_CONV_THREADS; ++rr) {
+                const int r = ct + rr * TC_CONV_THREADS;
+                // tile-blocked [T][d][128]: coalesced over r for each coordinate k
+                const float* X = a.xb + ((size_t)(t0 + (r >> 7)) * d) * 128 + (r & 127);
+                float mx = 0.0f;
+                if (r < valid)
+                    for (int k = 0; k < d; ++k) mx = fmaxf(mx, fabsf(__ldg(X + k * 128) - __ldg(zq + k)));
+                zcount += (r < valid && mx == 0.0f) ? 1u : 0u;
+                float scale = 0.0f;
+                if (mx > 0.0f) {
+                    int E = (int)((__float_as_uint(mx) >> 23) & 0xFF) - 126;  // mx < 2^E
+                    if (E < -100) E = -100;
+                    scale = __uint_as_float((uint32_t)(127 + 22 - E) << 23);  // 2^(22-E)
+                }
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t w0[4], w1[4], w2[4];
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        uint32_t b0 = 0, b1 = 0, b2 = 0;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int k = c * 16 + g * 4 + e;
+                            const float av = (k < d && scale != 0.0f) ? (__ldg(X + k * 128) - __ldg(zq + k)) : 0.0f;
+                            const int A0 = __float2int_rn(av * scale);
+                            const int A1 = (A0 + 128) >> 8;
+                            const int A2 = (A1 + 128) >> 8;
+                            b0 |= ((uint32_t)A0 & 0xFFu) << (8 * e);
+                            b1 |= ((uint32_t)A1 & 0xFFu) << (8 * e);
+                            b2 |= ((uint32_t)A2 & 0xFFu) << (8 * e);
+                        }
+                        w0[g] = b0;
+                        w1[g] = b1;
+                        w2[g] = b2;
+                    }
+                    // canonical K-major, no swizzle: [limb][k-chunk c][point r][16 bytes]
+                    *reinterpret_cast<uint4*>(P + 0 * P_LIMB_BYTES + c * 4096 + r * 16) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
+                    *reinterpret_cast<uint4*>(P + 1 * P_LIMB_BYTES + c * 4096 + r * 16) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+                    *reinterpret_cast<uint4*>(P + 2 * P_LIMB_BYTES + c * 4096 + r * 16) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+                }
+            }
+            // coinciding rows (x - z == 0) of this item: ties on both sides
+            zcount = __reduce_add_sync(0xffffffffu, zcount);
+            if (lane == 0 && zcount) atomicAdd(&sZrows[it & 3], zcount);
+            fence_proxy_async();  // generic-proxy smem writes -> tensor-core reads
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pfull[pb]);
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
         const int ct = tid - 128;          // 0..511
-        const int r = ct & (TC_PTS - 1);   // point row of the item
-        const int kh = ct >> 8;            // K half handled in the quantisation
         const int quarter = warp & 3;      // TMEM lane quarter = 32 directions
         const int part = (warp - 4) >> 2;  // 16-point slice of each 64-point group
         const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
@@ -310,75 +358,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
             const int64_t t0 = (item - (int64_t)q * tiles2) * 2;
             const int64_t vrows = a.n - t0 * 128;
             const int valid = vrows < TC_PTS ? (int)vrows : TC_PTS;
-            if (ct < d) sZ[ct] = a.zq[(size_t)q * d + ct];
-            mbar_wait(xfull, (uint32_t)(it & 1));
-            named_bar(1, TC_EPI_THREADS);  // sZ visible
-            // x - z, per-point power-of-two scale, three int8 limbs; two threads
-            // per point, each owning 32 coordinates (2 of the 4 k-chunks)
-            const float* X = sX + (r >> 7) * d * 128 + (r & 127);
-            const int k0 = kh * 32;
-            const int k1 = (k0 + 32) < d ? (k0 + 32) : d;
-            float mx = 0.0f;
-            if (r < valid)
-                for (int k = k0; k < k1; ++k) mx = fmaxf(mx, fabsf(X[k * 128] - sZ[k]));
-            sRmax[kh * TC_PTS + r] = mx;
-            named_bar(1, TC_EPI_THREADS);
-            mx = fmaxf(sRmax[r], sRmax[TC_PTS + r]);
-            {
-                // rows that coincide with the query (x - z == 0): ties on both sides
-                const unsigned zb = __ballot_sync(0xffffffffu, kh == 0 && r < valid && mx == 0.0f);
-                if (lane == 0 && zb) atomicAdd(sZrows, (uint32_t)__popc(zb));
-            }
-            float scale = 0.0f;
-            if (mx > 0.0f) {
-                int E = (int)((__float_as_uint(mx) >> 23) & 0xFF) - 126;  // mx < 2^E
-                if (E < -100) E = -100;
-                scale = __uint_as_float((uint32_t)(127 + 22 - E) << 23);  // 2^(22-E)
-            }
-            for (int c = 2 * kh; c < 2 * kh + 2; ++c) {
-                if (c * 16 >= d) {  // K padding: zero limbs
-                    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-                    for (int L = 0; L < 3; ++L)
-                        *reinterpret_cast<uint4*>(sP + L * P_LIMB_BYTES + c * 4096 + r * 16) = z4;
-                    continue;
-                }
-                uint32_t w0[4], w1[4], w2[4];
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    uint32_t b0 = 0, b1 = 0, b2 = 0;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int k = c * 16 + g * 4 + e;
-                        const float av = (k < d) ? (X[k * 128] - sZ[k]) : 0.0f;
-                        const int A0 = __float2int_rn(av * scale);
-                        const int A1 = (A0 + 128) >> 8;
-                        const int A2 = (A1 + 128) >> 8;
-                        b0 |= ((uint32_t)A0 & 0xFFu) << (8 * e);
-                        b1 |= ((uint32_t)A1 & 0xFFu) << (8 * e);
-                        b2 |= ((uint32_t)A2 & 0xFFu) << (8 * e);
-                    }
-                    w0[g] = b0;
-                    w1[g] = b1;
-                    w2[g] = b2;
-                }
-                // canonical K-major, no swizzle: [limb][k-chunk c][point r][16 bytes]
-                *reinterpret_cast<uint4*>(sP + 0 * P_LIMB_BYTES + c * 4096 + r * 16) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-                *reinterpret_cast<uint4*>(sP + 1 * P_LIMB_BYTES + c * 4096 + r * 16) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
-                *reinterpret_cast<uint4*>(sP + 2 * P_LIMB_BYTES + c * 4096 + r * 16) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
-            }
-            fence_proxy_async();  // generic-proxy smem writes -> tensor-core reads
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(pfull);
-                mbar_arrive(xempty);
-            }
-            // epilogue: thread = direction (TMEM lane), 16 points per 64-point group
             for (int db = 0; db < MB; ++db) {
                 uint32_t cnt = 0u;  // #(y<0) over this item's points
                 for (int pq = 0; pq < TC_PTS / TC_NP; ++pq, ++gt) {
                     const int buf = (int)(gt & 1);
-                    mbar_wait(&tfull[buf], (uint32_t)((gt >> 1) & 1));  // latency-critical: spin
+                    mbar_wait_sleep(&tfull[buf], (uint32_t)((gt >> 1) & 1));
                     tc_fence_after();
                     const uint32_t tb = tmem + lane_base + (uint32_t)buf * 192u + (uint32_t)(part * 16);
                     uint32_t r0[16], r1[16], r2[16];
@@ -406,7 +390,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
             // #(y>0) = real rows - coinciding rows - #(y<0); an exact zero from a
             // non-coinciding row (|y| below the quantisation error, inside the tie
             // zone) lands on the positive side
-            const int zrows = (int)*sZrows;
+            const int zrows = (int)sZrows[it & 3];
             int* dst = a.counts + (size_t)q * a.mpad * 2;
             for (int c = ct; c < ndirs; c += TC_EPI_THREADS) {
                 const int lt = (int)sCnt[c];
@@ -417,8 +401,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                 if (gtv) atomicAdd(dst + 2 * c + 1, gtv);
             }
             named_bar(1, TC_EPI_THREADS);
-            if (ct == 0) *sZrows = 0u;
-            named_bar(1, TC_EPI_THREADS);  // counters cleared before the next item adds
+            if (ct == 0) sZrows[it & 3] = 0u;
         }
     }
 
