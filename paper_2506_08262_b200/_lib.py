@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "librrs_b200.so")
+# RRS_B200_LIB: development override (kernel variants built under build/)
+LIB_PATH = os.environ.get("RRS_B200_LIB") or os.path.join(_HERE, "_lib", "librrs_b200.so")
 
 RRS_OK, RRS_ERR_INVALID, RRS_ERR_DIM, RRS_ERR_CUDA, RRS_ERR_NOMEM, RRS_ERR_STATE = range(6)
 NOTION_CODES = {"halfspace": 0, "projection": 1, "asym_projection": 2}
