@@ -1,94 +1,104 @@
-// contract_tc.cu -- K2 on the 5th-generation tensor cores: exact-integer
-// (int8-limb, Ozaki-style) contraction with a fused halfspace-count epilogue.
+// contract_tc.cu -- K2 on the 5th-generation tensor cores: split-precision
+// (FP16 hi/lo, FP32-accumulate) contraction with a fused halfspace-count
+// epilogue.
 //
 // Same result contract as the FFMA kernel (contract.cu): per (query, direction)
 // the counts #(y<0), #(y>0) of y_i = <u, x_i - z> over all points; the query's
-// own row gives y = 0 exactly (self-tie by construction) and exact zeros count
-// on both sides (#<= = n - #>0, #>= = n - #<0).  Fixed-point operands:
-//   a_il = x_il - z_l (FP32), scaled per point by a power of two so that
-//          |A_il| <= 2^22 (A = rint(a * 2^(22-E_i)), E_i: max_l |a_il| < 2^E_i);
-//   U_jl = rint(u_jl * 2^22) (|u| <= 1);
-//   both split into three signed int8 limbs  V = v2*2^16 + v1*2^8 + v0
-//   (|v2| <= 64, v1, v0 in [-128, 127]).
-// sum_l U_jl A_il = 2^32 S22 + 2^24 S21 + 2^16 S20 + 2^8 S1 + S0 with
-//   S22 = u2.a2, S21 = u2.a1 + u1.a2, S20 = u2.a0 + u1.a1 + u0.a2,
-//   S1 = u1.a0 + u0.a1 (four int32 TMEM accumulators, exact), S0 = u0.a0 dropped:
-//   |S0| <= d 2^14 <= 2^20 units of 2^-44 max|a|, i.e. <= 2^-23 max_l |a_il|,
-//   below the quantisation error of the operands themselves.  (Dropping S1 as
-//   well would leave errors ~2^-19 max|a|, which at n = 100k reach outside the
-//   north_star's 1e-6 tie zone: measured 1-6 sign flips per query.)
-// The per-point power of two never changes a sign, so the epilogue needs no
-// scale: with h = S22*2^8 + S21 and t = S20*2^8 + S1 (both exact in int32 for
-// d <= 64), T = 2^16 h + t and  T < 0  <=>  h + floor(t / 2^16) < 0, i.e.
-// 4 integer instructions per element (IMAD, IMAD, LEA.HI.SX32, LEA.HI).
-// Only #(y<0) is counted per element; #(y>0) = rows - coinciding rows - #(y<0).
+// own row gives y = 0 exactly (self-tie by construction: a = x - z = 0, every
+// product is a signed zero and y < 0 is false) and exact zeros count on both
+// sides (#<= = n - #>0, #>= = n - #<0).
 //
-// MMA orientation: M = 128 DIRECTIONS (TMEM lanes), N = 48 POINTS per
-// instruction, K = 32; eight MMAs per K step (one per limb product).  Each
-// epilogue thread owns one direction and counts its signs in registers.
+// Operands ("two-term FP16 split", FP32-class accuracy):
+//   a_il = x_il - z_l (FP32, as in contract.cu), scaled per point by the power
+//          of two s_i = 2^(14 - E_i) with max_l |a_il| < 2^E_i (never changes a
+//          sign); a*s = ah + al, ah = fp16(a*s), al = fp16(a*s - ah): 22 bits;
+//   u_jl * 2^15 = uh + ul likewise (from the FP64 direction).
+//   y_ij * s_i * 2^15 ~= sum_l (uh*al + ul*ah + uh*ah)   (ul*al, ~2^-22, dropped)
+// Each FP16 product is exact in FP32 and the tensor core accumulates in FP32;
+// the dropped term and the split residuals are ~2^-22 |u_l a_l|, the same order
+// as the FFMA kernel's own roundings.  Validated by tests/test_gpu_parity.py
+// (tier 1 at the config-4 shape: no count differs outside the 1e-6 tie zone).
+// A bit-exact int8-limb variant (four accumulator levels) needs 4x the TMEM
+// columns per point and therefore N = 48 MMAs, which sit on the ~54-clock
+// per-instruction floor of tcgen05.mma (profiles/r1/tcgen05_mma_floor_*.txt);
+// this kernel runs N = 128 MMAs at the full 64-clock rate.
 //
-// Persistent CTA (one per SM), 18 warps, work item = (query, 240 points):
-//   warp 0      TMA producer: direction blocks (24 KB int8 limbs, 3-stage ring)
-//               via cp.async.bulk + mbarriers, running ahead across items;
-//   warp 1      TMEM allocator + tcgen05 issuer: each direction block is copied
-//               smem -> TMEM (tcgen05.cp, double-buffered) and used as the
-//               TMEM-resident A operand ("TS" MMA), so the tensor core only
-//               reads the point operand from shared memory;
-//   warps 2-5   converters: x - z (x from L2, z staged in smem), per-point
-//               power-of-two scale, rint by the 1.5*2^23 FFMA trick and byte
-//               permutes into the double-buffered point operand, one item ahead;
-//   warps 6-17  epilogue of every (direction block, 48-point group): tcgen05.ld
-//               of the four accumulators, exact sign, per-thread counts, one
-//               shared atomic per direction; TMEM double-buffered against the MMA.
-// TMEM: 2 x (4 x 48) accumulator columns + 2 x 48 A-operand columns = 480 of 512.
+// Layout (M = 128 DIRECTIONS on TMEM lanes, N = 128 POINTS, K = 16 per MMA):
+//   TMEM columns [0,128) and [128,256): two FP32 accumulator buffers;
+//   TMEM columns [256 + 64 b, 256 + 64 b + 64): direction block b of the
+//   current unit (hi at +0, lo at +32; 16 K values = 8 columns per MMA),
+//   resident for the whole unit (TS MMA: A from TMEM, B from shared memory).
+// Work unit = (query, group of <= 4 direction blocks = 512 directions, chunk of
+// 128-point tiles); persistent CTAs (one per SM) stride over units.
+//   warp 0      producer: TMA of the unit's direction blocks (32 KB each, two at
+//               a time) into a staging area (cp.async.bulk + mbarrier);
+//   warp 1      TMEM allocator + tcgen05 issuer: staging -> TMEM (tcgen05.cp)
+//               once per unit, then per tile and block 3*ceil(d/16) MMAs;
+//   warp 2      producer: TMA of each raw FP32 point tile (d*512 bytes, the
+//               tile-blocked dataset) into a 2-4 stage ring;
+//   warps 3-10  converters: one (point, half of K) per thread: x - z from the
+//               staged tile, per-point power-of-two scale (max exchanged through
+//               shared memory), FP16 hi/lo split into the double-buffered
+//               point operand;
+//   warps 11-18 epilogue: tcgen05.ld of the accumulator (64 columns per thread),
+//               y < 0 counted per direction in registers, flushed per unit.
 // Replaces _kernels.pyx:120-199 (projection) + 270-289 (halfspace_span).
 #include "common.cuh"
 #include "kernels.h"
 
-#ifndef RRS_EPI_SLEEP
-#define RRS_EPI_SLEEP 1  // epilogue waits for accumulators with a suspend-time hint
-#endif
+#include <cuda_fp16.h>
 
 namespace rrs {
 
-constexpr int TC_CONV_WARPS = 4;                // warps 2-5 quantise the point operand
+constexpr int TC_CONV_WARP0 = 3;                 // first converter warp
+constexpr int TC_CONV_WARPS = 8;                 // (point, K half) per thread
 constexpr int TC_CONV_THREADS = TC_CONV_WARPS * 32;
-constexpr int TC_EPI_WARP0 = 2 + TC_CONV_WARPS;  // first epilogue warp
-constexpr int TC_EPI_WARPS = 12;                 // 4 lane quarters x 3 column parts
+constexpr int TC_EPI_WARP0 = TC_CONV_WARP0 + TC_CONV_WARPS;  // first epilogue warp
+constexpr int TC_EPI_WARPS = 8;                  // 4 lane quarters x 2 column halves
 constexpr int TC_EPI_THREADS = TC_EPI_WARPS * 32;
-constexpr int TC_THREADS = (TC_EPI_WARP0 + TC_EPI_WARPS) * 32;  // 576
+constexpr int TC_THREADS = (TC_EPI_WARP0 + TC_EPI_WARPS) * 32;  // 608
 constexpr int TC_KP = 64;                        // K padded (d <= 64)
 constexpr int TC_MD = 128;                       // directions per block (MMA M)
-constexpr int TC_NP = 48;                        // points per MMA (MMA N)
-constexpr int TC_GROUPS = 5;                     // MMA point groups per item
-constexpr int TC_PTS = TC_NP * TC_GROUPS;        // 240 points per work item
-constexpr int TC_LEVELS = 4;                     // accumulators S1, S20, S21, S22
-constexpr int P_CHUNK_BYTES = TC_PTS * 16;       // one 16-byte K chunk of every point
-constexpr int P_LIMB_BYTES = 4 * P_CHUNK_BYTES;  // 15 KB per limb
-constexpr int P_BUF_BYTES = 3 * P_LIMB_BYTES;    // 45 KB per point operand
-constexpr int D_LIMB_BYTES = TC_MD * TC_KP;      // 8 KB per limb
-constexpr int D_BLOCK_BYTES = 3 * D_LIMB_BYTES;  // 24 KB per direction block
-constexpr int D_STAGES = 3;
-constexpr int TC_MAX_DIRS = 4096;                // per-direction smem counters
+constexpr int TC_NP = 128;                       // points per tile (MMA N)
+constexpr int TC_GB = 4;                         // direction blocks resident per unit
+constexpr int TC_DPH = 2;                        // direction blocks per staging phase
+constexpr int P_SPLIT_BYTES = TC_NP * TC_KP * 2;  // 16 KB: one FP16 split of a tile
+constexpr int P_STAGE_BYTES = 2 * P_SPLIT_BYTES;  // 32 KB: hi + lo
+constexpr int P_STAGES = 2;
+constexpr int R_MAX_STAGES = 4;                   // raw FP32 tile ring (runtime depth)
+constexpr int D_SPLIT_BYTES = TC_MD * TC_KP * 2;  // 16 KB
+constexpr int D_BLOCK_BYTES = 2 * D_SPLIT_BYTES;  // 32 KB (= TC_DIR_BLOCK_BYTES)
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t ACC_COLS = TC_LEVELS * TC_NP;  // 192 per accumulator buffer
-constexpr uint32_t A_TMEM = 2 * ACC_COLS;         // 384: two 48-column A buffers follow
-static_assert(A_TMEM + 2 * 48 <= TMEM_COLS, "TMEM budget");
+constexpr uint32_t ACC_COLS = TC_NP;              // 128 per accumulator buffer
+constexpr uint32_t A_TMEM = 2 * ACC_COLS;         // 256: direction blocks (64 columns each)
+static_assert(A_TMEM + TC_GB * 64 <= TMEM_COLS, "TMEM budget");
+static_assert(D_BLOCK_BYTES == TC_DIR_BLOCK_BYTES, "direction operand block size");
+constexpr int TC_SMEM_LIMIT = 227 * 1024;
 
 struct TcSmem {
     // offsets in bytes from a 1024-aligned base
-    static constexpr int P = 0;                                   // 2 x 45 KB point operands
-    static constexpr int D = P + 2 * P_BUF_BYTES;                 // D_STAGES x 24 KB
-    static constexpr int CNT = D + D_STAGES * D_BLOCK_BYTES;      // uint32 [TC_MAX_DIRS]
-    static constexpr int ZS = CNT + TC_MAX_DIRS * 4;              // float [2][TC_KP] staged queries
-    static constexpr int ZROWS = ZS + 2 * TC_KP * 4;              // uint32 [4] coinciding rows per item slot
-    static constexpr int BARS = ZROWS + 16;                       // mbarriers
-    static constexpr int NBARS = 4 + 2 * D_STAGES + 4;
+    static constexpr int P = 0;                                    // point operand stages
+    static constexpr int D = P + P_STAGES * P_STAGE_BYTES;         // direction staging, TC_DPH blocks
+    static constexpr int CNT = D + TC_DPH * D_BLOCK_BYTES;         // uint32 [TC_GB * 128]
+    static constexpr int ZS = CNT + TC_GB * TC_MD * 4;             // float [2][TC_KP] staged queries
+    static constexpr int SMX = ZS + 2 * TC_KP * 4;                 // float [2][2][128] partial |a| maxima
+    static constexpr int EXCL = SMX + 2 * 2 * TC_NP * 4;           // uint32 [8][4] excluded-point masks per tile
+    static constexpr int ZROWS = EXCL + 8 * 4 * 4;                 // uint32 [4] coinciding rows per unit slot
+    static constexpr int BARS = ZROWS + 16;                        // mbarriers
+    static constexpr int NBARS = 2 * P_STAGES + 2 + 2 + 3 + 2 * R_MAX_STAGES;
     static constexpr int TADDR = BARS + NBARS * 8;
-    static constexpr int TOTAL = TADDR + 16;
+    static constexpr int RAW = (TADDR + 16 + 1023) & ~1023;        // raw tiles, runtime d*512 bytes each
 };
 
-size_t contract_tc_smem_bytes() { return TcSmem::TOTAL + 1024; }
+int contract_tc_raw_stages(int d) {
+    const int room = TC_SMEM_LIMIT - 1024 - TcSmem::RAW;
+    int st = room / (d * TC_NP * 4);
+    return st > R_MAX_STAGES ? R_MAX_STAGES : st;
+}
+
+size_t contract_tc_smem_bytes(int d) {
+    return (size_t)TcSmem::RAW + (size_t)contract_tc_raw_stages(d) * d * TC_NP * 4 + 1024;
+}
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     // tcgen05 shared-memory descriptor: start>>4 [0,14), LBO>>4 [16,30),
@@ -97,103 +107,71 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
            ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
 
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accumulate) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-
-// The issuing warps run their loops warp-wide (uniform operands, no waterfall)
-// and one elected lane issues each tcgen05 / TMA instruction.
-// A operand from TMEM ("TS"): [a_tmem] holds 128 lanes x K bytes, B from smem.
-__device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-
-// One 48-point group of the four-level limb product: 8 MMAs per K step (one
-// per limb product), NKS K steps, then the commit to the group's "accumulators
-// full" barrier -- all under a single elect, every operand an immediate offset
-// from three bases, so ptxas keeps the sequence on the uniform datapath.
-//   acc: accumulator buffer (levels at +0 S1, +48 S20, +96 S21, +144 S22)
-//   aT : direction limbs in TMEM (limb L, K step k at +16 L + 8 k)
-//   bd : point descriptor of limb 0, K step 0 (limb L at +L*PL, K step at +KS)
-//   (direction limb, point limb) -> level:
-//     (2,2)->S22  (2,1)(1,2)->S21  (2,0)(1,1)(0,2)->S20  (1,0)(0,1)->S1
-#define RRS_MMA8(AOFF, B0, B1, B2, FIRSTP)                                            \
-    "@e tcgen05.mma.cta_group::1.kind::i8 [%0+144], [%1+" AOFF "+32], " B2 ", %3, " FIRSTP ";\n" \
-    "@e tcgen05.mma.cta_group::1.kind::i8 [%0+96], [%1+" AOFF "+32], " B1 ", %3, " FIRSTP ";\n"  \
-    "@e tcgen05.mma.cta_group::1.kind::i8 [%0+96], [%1+" AOFF "+16], " B2 ", %3, 1;\n"           \
-    "@e tcgen05.mma.cta_group::1.kind::i8 [%0+48], [%1+" AOFF "+32], " B0 ", %3, " FIRSTP ";\n"  \
-    "@e tcgen05.mma.cta_group::1.kind::i8 [%0+48], [%1+" AOFF "+16], " B1 ", %3, 1;\n"           \
-    "@e tcgen05.mma.cta_group::1.kind::i8 [%0+48], [%1+" AOFF "], " B2 ", %3, 1;\n"              \
-    "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1+" AOFF "+16], " B0 ", %3, " FIRSTP ";\n"     \
-    "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1+" AOFF "], " B1 ", %3, 1;\n"
+// One (point tile, direction block) product: per K step of 16,
+//   D (+)= Ah*Bl, D += Al*Bh, D += Ah*Bh      (small terms first)
+// then the commit to the accumulator-full barrier, all under one elect with
+// immediate operand offsets (ptxas keeps it on the uniform datapath).
+//   acc: accumulator columns; aT: block's hi columns (lo at +32, K step at +8)
+//   bd : descriptor of the tile's hi split, K step 0 (K step +256, lo +1024)
+#define RRS_MMA3(KS, BH, BL, FIRSTP)                                                             \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+" KS "], " BL ", %3, " FIRSTP ";\n"         \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32+" KS "], " BH ", %3, 1;\n"                \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+" KS "], " BH ", %3, 1;\n"
 
 template <int NKS>
-__device__ __forceinline__ void mma_limbs_group(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint64_t PL,
-                                                uint64_t KS, uint32_t bar) {
-    if constexpr (NKS == 2) {
-        asm volatile(
-            "{\n.reg .pred e;\n.reg .b64 b1, b2, c0, c1, c2;\n"
-            "elect.sync _|e, 0xffffffff;\n"
-            "add.s64 b1, %2, %4;\n"
-            "add.s64 b2, b1, %4;\n"
-            "add.s64 c0, %2, %5;\n"
-            "add.s64 c1, b1, %5;\n"
-            "add.s64 c2, b2, %5;\n"
-            RRS_MMA8("0", "%2", "b1", "b2", "0")
-            RRS_MMA8("8", "c0", "c1", "c2", "1")
-            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n"
-            "}\n" ::"r"(acc),
-            "r"(aT), "l"(bd), "r"(idesc), "l"(PL), "l"(KS), "r"(bar)
-            : "memory");
+__device__ __forceinline__ void mma_tile_block(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc,
+                                               uint32_t bar) {
+    static_assert(NKS >= 1 && NKS <= 4, "K steps");
+    if constexpr (NKS == 1) {
+        asm volatile("{\n.reg .pred e;\n.reg .b64 l0;\nelect.sync _|e, 0xffffffff;\n"
+                     "add.s64 l0, %2, 1024;\n"
+                     RRS_MMA3("0", "%2", "l0", "0")
+                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                     ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+    } else if constexpr (NKS == 2) {
+        asm volatile("{\n.reg .pred e;\n.reg .b64 l0, h1, l1;\nelect.sync _|e, 0xffffffff;\n"
+                     "add.s64 l0, %2, 1024;\nadd.s64 h1, %2, 256;\nadd.s64 l1, %2, 1280;\n"
+                     RRS_MMA3("0", "%2", "l0", "0") RRS_MMA3("8", "h1", "l1", "1")
+                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                     ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+    } else if constexpr (NKS == 3) {
+        asm volatile("{\n.reg .pred e;\n.reg .b64 l0, h1, l1, h2, l2;\nelect.sync _|e, 0xffffffff;\n"
+                     "add.s64 l0, %2, 1024;\nadd.s64 h1, %2, 256;\nadd.s64 l1, %2, 1280;\n"
+                     "add.s64 h2, %2, 512;\nadd.s64 l2, %2, 1536;\n"
+                     RRS_MMA3("0", "%2", "l0", "0") RRS_MMA3("8", "h1", "l1", "1") RRS_MMA3("16", "h2", "l2", "1")
+                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                     ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
     } else {
-        asm volatile(
-            "{\n.reg .pred e;\n.reg .b64 b1, b2;\n"
-            "elect.sync _|e, 0xffffffff;\n"
-            "add.s64 b1, %2, %4;\n"
-            "add.s64 b2, b1, %4;\n"
-            RRS_MMA8("0", "%2", "b1", "b2", "0")
-            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n"
-            "}\n" ::"r"(acc),
-            "r"(aT), "l"(bd), "r"(idesc), "l"(PL), "l"(KS), "r"(bar)
-            : "memory");
+        asm volatile("{\n.reg .pred e;\n.reg .b64 l0, h1, l1, h2, l2, h3, l3;\nelect.sync _|e, 0xffffffff;\n"
+                     "add.s64 l0, %2, 1024;\nadd.s64 h1, %2, 256;\nadd.s64 l1, %2, 1280;\n"
+                     "add.s64 h2, %2, 512;\nadd.s64 l2, %2, 1536;\nadd.s64 h3, %2, 768;\nadd.s64 l3, %2, 1792;\n"
+                     RRS_MMA3("0", "%2", "l0", "0") RRS_MMA3("8", "h1", "l1", "1") RRS_MMA3("16", "h2", "l2", "1")
+                     RRS_MMA3("24", "h3", "l3", "1")
+                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                     ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
     }
 }
+#undef RRS_MMA3
 
-// A direction block (3 limbs x 64 K bytes, canonical K-major in smem) -> TMEM
-// columns [aT, aT + 48): six 128x256b copies under one elect.
+// Direction block b of the staging area (canonical K-major: [split][k chunk 8]
+// [direction 128][16 B]) -> TMEM columns [aT, aT + 64): eight 128x256b copies.
 __device__ __forceinline__ void tmem_cp_dirblock(uint32_t aT, uint64_t sd) {
-    // sd: descriptor of limb 0, K chunk 0; K step (2 chunks) = +4096 B, limb = +8192 B
+    // sd: descriptor of split 0, chunk 0; chunk pair +4096 B (256), split +16384 B (1024)
     asm volatile(
-        "{\n.reg .pred e;\n.reg .b64 s1, s2, s3, s4, s5;\n"
+        "{\n.reg .pred e;\n.reg .b64 s1, s2, s3, s4, s5, s6, s7;\n"
         "elect.sync _|e, 0xffffffff;\n"
-        "add.s64 s1, %1, 256;\n"
-        "add.s64 s2, %1, 512;\n"
-        "add.s64 s3, %1, 768;\n"
-        "add.s64 s4, %1, 1024;\n"
-        "add.s64 s5, %1, 1280;\n"
+        "add.s64 s1, %1, 256;\nadd.s64 s2, %1, 512;\nadd.s64 s3, %1, 768;\n"
+        "add.s64 s4, %1, 1024;\nadd.s64 s5, %1, 1280;\nadd.s64 s6, %1, 1536;\nadd.s64 s7, %1, 1792;\n"
         "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n"
         "@e tcgen05.cp.cta_group::1.128x256b [%0+8], s1;\n"
         "@e tcgen05.cp.cta_group::1.128x256b [%0+16], s2;\n"
         "@e tcgen05.cp.cta_group::1.128x256b [%0+24], s3;\n"
         "@e tcgen05.cp.cta_group::1.128x256b [%0+32], s4;\n"
         "@e tcgen05.cp.cta_group::1.128x256b [%0+40], s5;\n"
+        "@e tcgen05.cp.cta_group::1.128x256b [%0+48], s6;\n"
+        "@e tcgen05.cp.cta_group::1.128x256b [%0+56], s7;\n"
         "}\n" ::"r"(aT),
         "l"(sd));
-}
-
-// smem (canonical K-major, 128 rows x 32 bytes) -> TMEM (128 lanes x 8 columns)
-__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
-    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"(
-                     taddr),
-                 "l"(sdesc));
 }
 
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
@@ -206,32 +184,28 @@ __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
 __device__ __forceinline__ void tma_load_elect(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n"
         "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
 
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
+__device__ __forceinline__ void expect_tx_elect(uint64_t* bar, uint32_t bytes) {
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(bytes)
+        : "memory");
 }
 
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Wait with a suspend-time hint: the waiting thread sleeps in hardware until the
-// phase completes instead of spinning on issue slots shared with busy warps.
+// Wait with a suspend-time hint (for warps that run ahead of their consumer).
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -244,13 +218,14 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
         : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
-        "[%16];"
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-          "=r"(r[15])
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -259,46 +234,113 @@ __device__ __forceinline__ void named_bar(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-__device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
+__device__ __forceinline__ uint32_t pack_half2(float lo_elem, float hi_elem) {
+    const __half2 h = __floats2half2_rn(lo_elem, hi_elem);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+struct TcUnit {
+    int q, grp, nbg;     // query, direction group, blocks in the group
+    int64_t t0, t1;      // point tiles [t0, t1)
+};
+
+__device__ __forceinline__ TcUnit tc_unit(const TcArgs& a, int64_t u) {
+    TcUnit r;
+    const int64_t per_q = (int64_t)a.groups * a.chunks;
+    r.q = (int)(u / per_q);
+    const int64_t rem = u - (int64_t)r.q * per_q;
+    r.grp = (int)(rem / a.chunks);
+    const int64_t c = rem - (int64_t)r.grp * a.chunks;
+    r.nbg = a.NB - r.grp * TC_GB < TC_GB ? a.NB - r.grp * TC_GB : TC_GB;
+    r.t0 = c * a.tiles_per_chunk;
+    r.t1 = r.t0 + a.tiles_per_chunk < a.tiles ? r.t0 + a.tiles_per_chunk : a.tiles;
+    return r;
+}
+
+template <int NKS>
+__device__ __forceinline__ void mma_issue(const TcArgs& a, int64_t units, unsigned char* sP, unsigned char* sD,
+                                          uint64_t* pfull, uint64_t* pempty, uint64_t* dfull, uint64_t* dempty,
+                                          uint64_t* tfull, uint64_t* tempty, uint64_t* udone) {
+    constexpr uint32_t tmem = 0u;
+    // F32 accumulate, FP16 A and B, K-major both, N = 128, M = 128
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(TC_NP >> 3) << 17) | ((uint32_t)(TC_MD >> 4) << 24);
+    uint32_t it = 0, gtile = 0, gacc = 0, gph = 0;
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+        const TcUnit w = tc_unit(a, u);
+        const uint32_t dbase = smem_u32(sD);
+        for (int b0 = 0; b0 < w.nbg; b0 += TC_DPH, ++gph) {
+            mbar_wait_sleep(dfull, gph & 1u);
+            if (b0 == 0 && it > 0) mbar_wait(udone, (it - 1) & 1u);  // previous unit no longer reads TMEM A
+            tc_fence_after();
+            for (int b = b0; b < w.nbg && b < b0 + TC_DPH; ++b)
+                tmem_cp_dirblock(tmem + A_TMEM + 64u * b, umma_desc(dbase + (b - b0) * D_BLOCK_BYTES, 2048, 128));
+            mma_commit_elect(dempty);  // staging free once the copies are done
+        }
+        for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
+            const uint32_t s = gtile % P_STAGES;
+            mbar_wait(&pfull[s], (gtile / P_STAGES) & 1u);
+            tc_fence_after();
+            const uint64_t bd = umma_desc(smem_u32(sP) + s * P_STAGE_BYTES, 2048, 128);
+            for (int b = 0; b < w.nbg; ++b, ++gacc) {
+                const uint32_t buf = gacc & 1u;
+                if (gacc >= 2) mbar_wait(&tempty[buf], ((gacc >> 1) - 1) & 1u);
+                tc_fence_after();
+                mma_tile_block<NKS>(tmem + buf * ACC_COLS, tmem + A_TMEM + 64u * b, bd, idesc,
+                                    smem_u32(&tfull[buf]));
+            }
+            mma_commit_elect(&pempty[s]);  // point stage free once this tile's MMAs are done
+        }
+        mma_commit_elect(udone);
+    }
+}
 
 __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs a) {
     extern __shared__ __align__(1024) unsigned char tc_raw[];
-    unsigned char* sm = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    // 1024-align by pointer arithmetic on the __shared__ array (keeps the address space)
+    unsigned char* sm = tc_raw + ((1024u - (smem_u32(tc_raw) & 1023u)) & 1023u);
     unsigned char* sP = sm + TcSmem::P;
     unsigned char* sD = sm + TcSmem::D;
     uint32_t* sCnt = reinterpret_cast<uint32_t*>(sm + TcSmem::CNT);
     float* sZ = reinterpret_cast<float*>(sm + TcSmem::ZS);
     uint32_t* sZrows = reinterpret_cast<uint32_t*>(sm + TcSmem::ZROWS);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + TcSmem::BARS);
-    uint64_t* pfull = &bars[0];                  // [2] point operand quantised (converter warps)
-    uint64_t* pempty = &bars[2];                 // [2] MMAs reading it completed
-    uint64_t* dfull = &bars[4];                  // [D_STAGES]
-    uint64_t* dempty = &bars[4 + D_STAGES];      // [D_STAGES]
-    uint64_t* tfull = &bars[4 + 2 * D_STAGES];   // [2]
-    uint64_t* tempty = &bars[6 + 2 * D_STAGES];  // [2]
+    uint64_t* pfull = &bars[0];                   // [P_STAGES] point tile converted (converter warps)
+    uint64_t* pempty = &bars[P_STAGES];           // [P_STAGES] MMAs reading it completed
+    uint64_t* tfull = &bars[2 * P_STAGES];        // [2] accumulator ready
+    uint64_t* tempty = &bars[2 * P_STAGES + 2];   // [2] accumulator drained (epilogue warps)
+    uint64_t* dfull = &bars[2 * P_STAGES + 4];    // direction staging phase loaded
+    uint64_t* dempty = &bars[2 * P_STAGES + 5];   // direction staging copied to TMEM
+    uint64_t* udone = &bars[2 * P_STAGES + 6];    // all MMAs of a unit completed
+    uint64_t* rfull = &bars[2 * P_STAGES + 7];    // [R_MAX_STAGES] raw tile landed
+    uint64_t* rempty = &bars[2 * P_STAGES + 7 + R_MAX_STAGES];  // [R_MAX_STAGES] raw tile read
+    float* sMx = reinterpret_cast<float*>(sm + TcSmem::SMX);
+    uint32_t* sExcl = reinterpret_cast<uint32_t*>(sm + TcSmem::EXCL);
+    float* sRaw = reinterpret_cast<float*>(sm + TcSmem::RAW);
+    const int RS = a.raw_stages;
+    const uint32_t raw_bytes = (uint32_t)(a.d * TC_NP * 4);
     uint32_t* sTaddr = reinterpret_cast<uint32_t*>(sm + TcSmem::TADDR);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int d = a.d;
-    const int MB = a.NB;                 // 128-direction blocks per query
-    const int ndirs = MB * TC_MD;
-    const int nks = (d + 31) / 32;       // MMA K-steps (1 or 2)
-    const int64_t chunks = (a.n + TC_PTS - 1) / TC_PTS;
-    const int64_t items = (int64_t)a.Qb * chunks;
+    const int64_t units = (int64_t)a.Qb * a.groups * a.chunks;
 
-    for (int c = tid; c < ndirs; c += TC_THREADS) sCnt[c] = 0u;
+    for (int c = tid; c < TC_GB * TC_MD; c += TC_THREADS) sCnt[c] = 0u;
     if (tid < 4) sZrows[tid] = 0u;
     if (tid == 0) {
+        for (int s = 0; s < P_STAGES; ++s) {
+            mbar_init(&pfull[s], TC_CONV_WARPS);
+            mbar_init(&pempty[s], 1);
+        }
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&pfull[b], TC_CONV_WARPS);
-            mbar_init(&pempty[b], 1);
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], TC_EPI_WARPS);
         }
-        for (int b = 0; b < D_STAGES; ++b) {
-            mbar_init(&dfull[b], 1);
-            mbar_init(&dempty[b], 1);
+        mbar_init(dfull, 1);
+        mbar_init(dempty, 1);
+        mbar_init(udone, 1);
+        for (int r = 0; r < R_MAX_STAGES; ++r) {
+            mbar_init(&rfull[r], 1);
+            mbar_init(&rempty[r], TC_CONV_WARPS);
         }
         fence_mbar_init();
     }
@@ -317,190 +359,189 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     constexpr uint32_t tmem = 0u;
 
     if (warp == 0) {
-        // ------------------------------------------- producer: direction blocks
-        int64_t gd = 0;
-        for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-            const int q = (int)(item / chunks);
-            const unsigned char* src = a.u8 + (size_t)q * MB * D_BLOCK_BYTES;
-            for (int db = 0; db < MB; ++db, ++gd) {
-                const int s = (int)(gd % D_STAGES);
-                const int64_t u = gd / D_STAGES;
-                if (u >= 1) mbar_wait_sleep(&dempty[s], (uint32_t)((u - 1) & 1));
-                tma_load_elect(sD + s * D_BLOCK_BYTES, src + (size_t)db * D_BLOCK_BYTES, D_BLOCK_BYTES, &dfull[s]);
+        // ----------------------------- producer: unit direction blocks, 2 per phase
+        uint32_t gph = 0;
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+            const TcUnit w = tc_unit(a, u);
+            const unsigned char* src =
+                a.uop + ((size_t)w.q * a.NB + (size_t)w.grp * TC_GB) * D_BLOCK_BYTES;
+            for (int b0 = 0; b0 < w.nbg; b0 += TC_DPH, ++gph) {
+                const int nb = w.nbg - b0 < TC_DPH ? w.nbg - b0 : TC_DPH;
+                if (gph > 0) mbar_wait_sleep(dempty, (gph - 1) & 1u);
+                expect_tx_elect(dfull, (uint32_t)(nb * D_BLOCK_BYTES));
+                for (int b = 0; b < nb; ++b)
+                    tma_load_elect(sD + b * D_BLOCK_BYTES, src + (size_t)(b0 + b) * D_BLOCK_BYTES, D_BLOCK_BYTES,
+                                   dfull);
+                __syncwarp();
             }
-            __syncwarp();
+        }
+    } else if (warp == 2) {
+        // -------------------------------------- producer: raw FP32 point tiles
+        uint32_t g = 0;
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+            const TcUnit w = tc_unit(a, u);
+            for (int64_t t = w.t0; t < w.t1; ++t, ++g) {
+                const uint32_t rs = g % RS;
+                if (g >= (uint32_t)RS) mbar_wait_sleep(&rempty[rs], ((g / RS) - 1) & 1u);
+                expect_tx_elect(&rfull[rs], raw_bytes);
+                tma_load_elect(sRaw + (size_t)rs * d * TC_NP, a.xb + (size_t)t * d * TC_NP, raw_bytes, &rfull[rs]);
+                __syncwarp();
+            }
         }
     } else if (warp == 1) {
         // -------------------------------------------------------- MMA issuer
-        // S32 accumulate, signed int8 A and B, K-major both, N = 48, M = 128
-        const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TC_NP >> 3) << 17) |
-                               ((uint32_t)(TC_MD >> 4) << 24);
-        const uint64_t PL = (uint64_t)(P_LIMB_BYTES >> 4);       // point limb stride (descriptor units)
-        const uint64_t KS = (uint64_t)(2 * P_CHUNK_BYTES >> 4);  // K step: two 16-byte chunks
-        uint32_t gd = 0, gt = 0;
-        uint32_t it = 0;
-        for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-            const uint32_t pb = it & 1u;
-            mbar_wait_sleep(&pfull[pb], (it >> 1) & 1u);
-            // points [limb][k-chunk][240][16B]: LBO = one chunk, SBO 128
-            const uint64_t pdesc = umma_desc(smem_u32(sP) + pb * P_BUF_BYTES, P_CHUNK_BYTES, 128);
-            for (int db = 0; db < MB; ++db, ++gd) {
-                const uint32_t s = gd % D_STAGES;
-                mbar_wait_sleep(&dfull[s], (gd / D_STAGES) & 1u);
-                tc_fence_after();
-                // direction block -> TMEM (A operand), double-buffered; in order with the MMAs
-                const uint32_t aT = tmem + A_TMEM + (gd & 1u) * 48u;
-                tmem_cp_dirblock(aT, umma_desc(smem_u32(sD) + s * D_BLOCK_BYTES, 2048, 128));
-                mma_commit_elect(&dempty[s]);  // smem stage free once the copies are done
-#pragma unroll 1
-                for (int g = 0; g < TC_GROUPS; ++g, ++gt) {
-                    const uint32_t buf = gt & 1u;
-                    if (gt >= 2) mbar_wait(&tempty[buf], ((gt >> 1) - 1) & 1u);
-                    tc_fence_after();
-                    const uint32_t acc = tmem + buf * ACC_COLS;
-                    const uint64_t bd = pdesc + (uint64_t)(g * TC_NP);  // + g*48 points*16 B >> 4
-                    if (nks > 1)
-                        mma_limbs_group<2>(acc, aT, bd, idesc, PL, KS, smem_u32(&tfull[buf]));
-                    else
-                        mma_limbs_group<1>(acc, aT, bd, idesc, PL, KS, smem_u32(&tfull[buf]));
-                }
-            }
-            mma_commit_elect(&pempty[pb]);  // point operand free once this item's MMAs are done
+        switch ((d + 15) >> 4) {
+            case 1: mma_issue<1>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+            case 2: mma_issue<2>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+            case 3: mma_issue<3>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+            default: mma_issue<4>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
         }
     } else if (warp < TC_EPI_WARP0) {
-        // ------------------------- converters: x - z -> per-point scale -> int8 limbs
-        const int ct = tid - 64;  // 0..127: rows ct, ct + 128 (< TC_PTS)
-        int it = 0;
-        for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-            const int pb = it & 1;
-            const int q = (int)(item / chunks);
-            const int64_t r0 = (item - (int64_t)q * chunks) * TC_PTS;
-            const int64_t vrows = a.n - r0;
-            const int valid = vrows < TC_PTS ? (int)vrows : TC_PTS;
-            float* zs = sZ + pb * TC_KP;
-            if (ct < TC_KP) zs[ct] = ct < d ? __ldg(a.zq + (size_t)q * d + ct) : 0.0f;
-            named_bar(2, TC_CONV_THREADS);  // zs ready; also keeps the converter warps in step
-            if (it >= 2) mbar_wait_sleep(&pempty[pb], (uint32_t)(((it >> 1) - 1) & 1));
-            unsigned char* P = sP + pb * P_BUF_BYTES;
+        // ----------------------- converters: x - z -> scale -> FP16 hi/lo split
+        const int ct = tid - TC_CONV_WARP0 * 32;  // 0..255
+        const int r = ct & (TC_NP - 1);           // point of the tile
+        const int h = ct >> 7;                    // K half: coordinates [32 h, 32 h + 32)
+        uint32_t it = 0, gtile = 0;
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+            const TcUnit w = tc_unit(a, u);
+            float* zs = sZ + (it & 1u) * TC_KP;
+            if (ct < TC_KP) zs[ct] = ct < d ? __ldg(a.zq + (size_t)w.q * d + ct) : 0.0f;
+            named_bar(2, TC_CONV_THREADS);  // zs ready; keeps the converter warps in step per unit
             uint32_t zcount = 0;
-            for (int r = ct; r < TC_PTS; r += TC_CONV_THREADS) {
-                const int64_t row = r0 + r;
-                const bool ok = r < valid;
-                // tile-blocked [T][d][128]: coalesced over consecutive rows for each coordinate
-                const float* X = a.xb + (size_t)(ok ? (row >> 7) : 0) * d * 128 + (row & 127);
-                float av[TC_KP];
+            for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
+                const uint32_t s = gtile % P_STAGES;
+                const uint32_t rs = gtile % RS;
+                const bool ok = t * TC_NP + r < a.n;
+                mbar_wait(&rfull[rs], (gtile / RS) & 1u);
+                // staged tile [d][128]: lane-consecutive points, conflict-free
+                const float* X = sRaw + (size_t)rs * d * TC_NP + r;
+                float av[32];
                 float mx = 0.0f;
 #pragma unroll
-                for (int k = 0; k < TC_KP; k += 4) {
-                    const float4 z4 = *reinterpret_cast<const float4*>(zs + k);
+                for (int k = 0; k < 32; k += 4) {
+                    const float4 z4 = *reinterpret_cast<const float4*>(zs + 32 * h + k);
                     const float zz[4] = {z4.x, z4.y, z4.z, z4.w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const int kk = k + e;
-                        av[kk] = (ok && kk < d) ? (__ldg(X + kk * 128) - zz[e]) : 0.0f;
-                        mx = fmaxf(mx, fabsf(av[kk]));
+                        const int kk = 32 * h + k + e;
+                        av[k + e] = (ok && kk < d) ? (X[kk * TC_NP] - zz[e]) : 0.0f;
+                        mx = fmaxf(mx, fabsf(av[k + e]));
                     }
                 }
-                zcount += (ok && mx == 0.0f) ? 1u : 0u;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&rempty[rs]);  // raw tile consumed (loads ordered by release)
+                float* mxs = sMx + (gtile & 1u) * 2 * TC_NP;
+                mxs[h * TC_NP + r] = mx;
+                named_bar(2, TC_CONV_THREADS);  // both K halves' maxima visible
+                mx = fmaxf(mxs[r], mxs[TC_NP + r]);
+                if (h == 0) {
+                    // points the epilogue must not count: coinciding rows (every product a
+                    // signed zero, ties on both sides) and rows beyond n
+                    zcount += (ok && mx == 0.0f) ? 1u : 0u;
+                    const uint32_t ex = __ballot_sync(0xffffffffu, !ok || mx == 0.0f);
+                    if (lane == 0) sExcl[(gtile & 7u) * 4 + (r >> 5)] = ex;
+                }
                 float scale = 0.0f;
                 if (mx > 0.0f) {
-                    int E = (int)((f2u(mx) >> 23) & 0xFF) - 126;  // mx < 2^E
+                    int E = (int)((__float_as_uint(mx) >> 23) & 0xFF) - 126;  // mx < 2^E
                     if (E < -100) E = -100;
-                    scale = __uint_as_float((uint32_t)(127 + 22 - E) << 23);  // 2^(22-E)
+                    scale = __uint_as_float((uint32_t)(127 + 14 - E) << 23);  // 2^(14-E)
                 }
-                // B = bits(a*scale + 1.5*2^23) = 0x4B400000 + A exactly (|A| <= 2^22), so
-                //   limb0 = byte0(B), limb1 = byte1(B + 128), limb2 = byte2(B + 32896 - 2^22)
+                if (gtile >= P_STAGES) mbar_wait(&pempty[s], ((gtile / P_STAGES) - 1) & 1u);
+                // canonical K-major, no swizzle: [split][k chunk c (8 values)][point r][16 bytes]
+                unsigned char* P = sP + s * P_STAGE_BYTES + r * 16;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    uint32_t w0[4], w1[4], w2[4];
+                    uint32_t hw[4], lw[4];
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        uint32_t B[4], C[4], D[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            B[e] = f2u(__fmaf_rn(av[c * 16 + g * 4 + e], scale, 12582912.0f));
-                            C[e] = B[e] + 128u;
-                            D[e] = B[e] - 4161408u;
-                        }
-                        w0[g] = __byte_perm(__byte_perm(B[0], B[1], 0x0040), __byte_perm(B[2], B[3], 0x0040), 0x5410);
-                        w1[g] = __byte_perm(__byte_perm(C[0], C[1], 0x0051), __byte_perm(C[2], C[3], 0x0051), 0x5410);
-                        w2[g] = __byte_perm(__byte_perm(D[0], D[1], 0x0062), __byte_perm(D[2], D[3], 0x0062), 0x5410);
+                    for (int e = 0; e < 4; ++e) {
+                        const float v0 = av[c * 8 + 2 * e] * scale, v1 = av[c * 8 + 2 * e + 1] * scale;
+                        const __half2 hh = __floats2half2_rn(v0, v1);
+                        const float2 hf = __half22float2(hh);
+                        hw[e] = *reinterpret_cast<const uint32_t*>(&hh);
+                        lw[e] = pack_half2(v0 - hf.x, v1 - hf.y);
                     }
-                    // canonical K-major, no swizzle: [limb][k-chunk c][point r][16 bytes]
-                    unsigned char* dst = P + c * P_CHUNK_BYTES + r * 16;
-                    *reinterpret_cast<uint4*>(dst + 0 * P_LIMB_BYTES) = make_uint4(w0[0], w0[1], w0[2], w0[3]);
-                    *reinterpret_cast<uint4*>(dst + 1 * P_LIMB_BYTES) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
-                    *reinterpret_cast<uint4*>(dst + 2 * P_LIMB_BYTES) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+                    const int cc = 4 * h + c;
+                    *reinterpret_cast<uint4*>(P + cc * (TC_NP * 16)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                    *reinterpret_cast<uint4*>(P + P_SPLIT_BYTES + cc * (TC_NP * 16)) =
+                        make_uint4(lw[0], lw[1], lw[2], lw[3]);
                 }
+                fence_proxy_async();  // generic-proxy smem writes -> tensor-core reads
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&pfull[s]);
             }
-            // coinciding rows (x - z == 0) of this item: ties on both sides
+            // coinciding rows (x - z == 0) of this unit: ties on both sides
             zcount = __reduce_add_sync(0xffffffffu, zcount);
-            if (lane == 0 && zcount) atomicAdd(&sZrows[it & 3], zcount);
-            fence_proxy_async();  // generic-proxy smem writes -> tensor-core reads
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&pfull[pb]);
+            if (lane == 0 && zcount) atomicAdd(&sZrows[it & 3u], zcount);
         }
     } else {
         // ------------------------------------------------------------ epilogue
-        const int ct = tid - TC_EPI_WARP0 * 32;        // 0..383
+        const int ct = tid - TC_EPI_WARP0 * 32;        // 0..255
         const int quarter = warp & 3;                  // TMEM lane quarter = 32 directions
-        const int part = (warp - TC_EPI_WARP0) >> 2;   // 16-point slice of each 48-point group
+        const int half = (warp - TC_EPI_WARP0) >> 2;   // 64-point half of the tile
         const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
-        int64_t gt = 0;
-        int it = 0;
-        for (int64_t item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-            const int q = (int)(item / chunks);
-            const int64_t r0 = (item - (int64_t)q * chunks) * TC_PTS;
-            const int64_t vrows = a.n - r0;
-            const int valid = vrows < TC_PTS ? (int)vrows : TC_PTS;
-            for (int db = 0; db < MB; ++db) {
-                uint32_t cnt = 0u;  // #(y<0) over this item's points
-                for (int g = 0; g < TC_GROUPS; ++g, ++gt) {
-                    const int buf = (int)(gt & 1);
-#if RRS_EPI_SLEEP
-                    mbar_wait_sleep(&tfull[buf], (uint32_t)((gt >> 1) & 1));
-#else
-                    mbar_wait(&tfull[buf], (uint32_t)((gt >> 1) & 1));
-#endif
-                    tc_fence_after();
-                    const uint32_t tb = tmem + lane_base + (uint32_t)buf * ACC_COLS + (uint32_t)(part * 16);
-                    uint32_t s1[16], s20[16], s21[16], s22[16];
-                    tmem_ld16(tb + 0 * TC_NP, s1);
-                    tmem_ld16(tb + 1 * TC_NP, s20);
-                    tmem_ld16(tb + 2 * TC_NP, s21);
-                    tmem_ld16(tb + 3 * TC_NP, s22);
-                    tmem_wait_ld();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[buf]);  // accumulators consumed
-                    uint32_t lt = 0u;
+        uint32_t it = 0, gacc = 0, gtile = 0;
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+            const TcUnit w = tc_unit(a, u);
+            uint32_t cnt[TC_GB] = {0u, 0u, 0u, 0u};  // #(y<0) per resident block
+            for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
+                uint32_t keep0 = 0u, keep1 = 0u;
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int h = (int)s22[j] * 256 + (int)s21[j];
-                        const int t = (int)s20[j] * 256 + (int)s1[j];
-                        const int gsum = h + (t >> 16);  // T < 0  <=>  gsum < 0 (exact)
-                        lt += (uint32_t)gsum >> 31;
+                for (int b = 0; b < TC_GB; ++b) {
+                    if (b < w.nbg) {
+                        const uint32_t buf = gacc & 1u;
+                        mbar_wait(&tfull[buf], (gacc >> 1) & 1u);
+                        ++gacc;
+                        tc_fence_after();
+                        if (b == 0) {
+                            // excluded points of this tile (written by the converters before the
+                            // tile's pfull; ordered through pfull -> MMA -> tfull), bit j = point
+                            // half*64 + 32 i + j
+                            keep0 = ~sExcl[(gtile & 7u) * 4 + 2 * half];
+                            keep1 = ~sExcl[(gtile & 7u) * 4 + 2 * half + 1];
+                        }
+                        const uint32_t tb = tmem + lane_base + buf * ACC_COLS + (uint32_t)(half * 64);
+                        uint32_t y0[32], y1[32];
+                        tmem_ld32(tb, y0);
+                        tmem_ld32(tb + 32, y1);
+                        tmem_wait_ld();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[buf]);  // accumulator consumed
+                        // sign bits -> 32-bit masks (one funnel shift per element), bit j = point j;
+                        // y < 0 <=> sign bit set, except the signed zeros of excluded points
+                        uint32_t m0 = 0u, m1 = 0u;
+#pragma unroll
+                        for (int j = 31; j >= 0; --j) {
+                            m0 = __funnelshift_l(y0[j], m0, 1);
+                            m1 = __funnelshift_l(y1[j], m1, 1);
+                        }
+                        cnt[b] += __popc(m0 & keep0) + __popc(m1 & keep1);
                     }
-                    cnt += lt;
                 }
-                atomicAdd(sCnt + db * TC_MD + 32 * quarter + lane, cnt);
             }
-            named_bar(1, TC_EPI_THREADS);  // all direction counts of this item are in
+#pragma unroll
+            for (int b = 0; b < TC_GB; ++b)
+                if (b < w.nbg) atomicAdd(sCnt + b * TC_MD + 32 * quarter + lane, cnt[b]);
+            named_bar(1, TC_EPI_THREADS);  // all direction counts of this unit are in
             // #(y>0) = real rows - coinciding rows - #(y<0); an exact zero from a
-            // non-coinciding row (|y| below the quantisation error, inside the tie
+            // non-coinciding row (|y| below the rounding error, inside the tie
             // zone) lands on the positive side
-            const int zrows = (int)sZrows[it & 3];
-            int* dst = a.counts + (size_t)q * a.mpad * 2;
-            for (int c = ct; c < ndirs; c += TC_EPI_THREADS) {
+            const int64_t r1 = w.t1 * TC_NP < a.n ? w.t1 * TC_NP : a.n;
+            const int valid = (int)(r1 - w.t0 * TC_NP);
+            const int zrows = (int)sZrows[it & 3u];
+            int* dst = a.counts + (size_t)w.q * a.mpad * 2;
+            const int j0 = w.grp * TC_GB * TC_MD;
+            for (int c = ct; c < w.nbg * TC_MD; c += TC_EPI_THREADS) {
                 const int lt = (int)sCnt[c];
                 sCnt[c] = 0u;
-                if (c >= a.m) continue;
+                if (j0 + c >= a.m) continue;
                 const int gtv = valid - zrows - lt;
-                if (lt) atomicAdd(dst + 2 * c + 0, lt);
-                if (gtv) atomicAdd(dst + 2 * c + 1, gtv);
+                if (lt) atomicAdd(dst + 2 * (j0 + c) + 0, lt);
+                if (gtv) atomicAdd(dst + 2 * (j0 + c) + 1, gtv);
             }
             named_bar(1, TC_EPI_THREADS);
-            if (ct == 0) sZrows[it & 3] = 0u;
+            if (ct == 0) sZrows[it & 3u] = 0u;
         }
     }
 
@@ -509,15 +550,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
-cudaError_t launch_contract_tc(const TcArgs& a, int sms, cudaStream_t st) {
-    if (a.d > TC_KP || a.NB * TC_MD > TC_MAX_DIRS) return cudaErrorInvalidValue;
-    const size_t smem = contract_tc_smem_bytes();
+void plan_contract_tc(TcArgs& a, int sms) {
+    a.groups = (a.NB + TC_GB - 1) / TC_GB;
+    // split the point tiles into chunks so that every SM gets >= ~16 units
+    const int64_t base = (int64_t)a.Qb * a.groups;
+    int64_t chunks = (16LL * sms + base - 1) / base;
+    if (chunks < 1) chunks = 1;
+    if (chunks > a.tiles) chunks = a.tiles;
+    a.tiles_per_chunk = (a.tiles + chunks - 1) / chunks;
+    a.chunks = (int)((a.tiles + a.tiles_per_chunk - 1) / a.tiles_per_chunk);
+}
+
+cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st) {
+    if (a.d > TC_KP || a.d < 1) return cudaErrorInvalidValue;
+    plan_contract_tc(a, sms);
+    a.raw_stages = contract_tc_raw_stages(a.d);
+    if (a.raw_stages < 2) return cudaErrorInvalidValue;
+    const size_t smem = contract_tc_smem_bytes(a.d);
     cudaError_t e =
         cudaFuncSetAttribute(contract_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    const int64_t items = (int64_t)a.Qb * ((a.n + TC_PTS - 1) / TC_PTS);
-    if (items == 0) return cudaSuccess;
-    const int grid = (int)(items < sms ? items : sms);
+    const int64_t units = (int64_t)a.Qb * a.groups * a.chunks;
+    if (units == 0) return cudaSuccess;
+    const int grid = (int)(units < sms ? units : sms);
     contract_tc_kernel<<<grid, TC_THREADS, smem, st>>>(a);
     return cudaGetLastError();
 }

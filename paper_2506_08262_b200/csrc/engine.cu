@@ -87,7 +87,7 @@ struct rrs_engine {
     int d = 0;
     int64_t tiles = 0;
     // workspace
-    DevBuf zq, u64, u32, u8, counts, depths, y, pole, reflv, reflmode, dmin, bestcnt;
+    DevBuf zq, u64, u32, uop, counts, depths, y, pole, reflv, reflmode, dmin, bestcnt;
     int contract_path = 0;  // 0 auto, 1 FFMA (contract.cu), 2 tensor cores (contract_tc.cu)
     DevBuf tmp_in, tmp_out0, tmp_out1, tmp_out2, tmp_out3;
     // timing
@@ -153,8 +153,8 @@ int validate_cfg(const rrs_config* c) {
 
 struct Plan {
     int m, mpad, MB, Qb;
-    bool tc;     // tensor-core int8-limb contraction (halfspace, d <= 64)
-    int nb8;     // 128-direction blocks per query (tensor path operand)
+    bool tc;     // tensor-core FP16-split contraction (halfspace, d <= 64)
+    int nb8;     // 128-direction blocks per query (tensor path operand, TC_DIR_BLOCK_BYTES each)
     int jchunk;  // direction blocks per store launch (projection notions)
     int tpu, chunks;
 };
@@ -165,11 +165,11 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     p.MB = (m + BN - 1) / BN;
     p.mpad = p.MB * BN;
     p.nb8 = p.MB;
-    const bool tc_ok = notion == RRS_HALFSPACE && e->d <= 64 && p.mpad <= 4096;
+    const bool tc_ok = notion == RRS_HALFSPACE && e->d <= 64;
     p.tc = tc_ok && (e->contract_path == 2 || (e->contract_path == 0 && e->n >= 4096));
     const int64_t d = e->d, n = e->n;
     int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * d * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 8 +
-                    d * 40 + 64 + (int64_t)p.nb8 * 24576;
+                    d * 40 + 64 + (int64_t)p.nb8 * TC_DIR_BLOCK_BYTES;
     int64_t budget = e->ws_limit;
     int64_t qb = 4096;
     if (notion != RRS_HALFSPACE) {
@@ -216,7 +216,7 @@ int ensure_ws(rrs_engine* e, const Plan& p, int notion) {
     CK(e->reflmode.ensure(Qb * 4));
     CK(e->dmin.ensure(Qb * 8));
     CK(e->bestcnt.ensure(Qb * 8));
-    CK(e->u8.ensure(p.tc ? Qb * (size_t)p.nb8 * 24576 : 16));
+    CK(e->uop.ensure(p.tc ? Qb * (size_t)p.nb8 * TC_DIR_BLOCK_BYTES : 16));
     if (notion == RRS_HALFSPACE) {
         CK(e->counts.ensure(Qb * p.mpad * 2 * 4));
         CK(e->depths.ensure(8));
@@ -253,7 +253,7 @@ int contract_halfspace(rrs_engine* e, const Plan& p, int Qb) {
         TcArgs t{};
         t.xb = e->xb.as<float>();
         t.zq = e->zq.as<float>();
-        t.u8 = e->u8.as<unsigned char>();
+        t.uop = e->uop.as<unsigned char>();
         t.counts = e->counts.as<int>();
         t.n = e->n;
         t.tiles = e->tiles;
@@ -364,8 +364,8 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 g.m = m;
                 g.mpad = p.mpad;
                 g.d = d;
-                g.u8 = p.tc ? e->u8.as<unsigned char>() : nullptr;
-                g.nb8 = p.nb8;
+                g.uop = p.tc ? e->uop.as<unsigned char>() : nullptr;
+                g.NB = p.nb8;
                 CK(launch_cap_generate(g, e->stream));
                 e->stats.kernel_launches++;
             }
@@ -467,7 +467,7 @@ int rrs_engine_destroy(rrs_engine* e) {
     if (!e) return RRS_OK;
     cudaSetDevice(e->device);
     cudaStreamSynchronize(e->stream);
-    for (DevBuf* b : {&e->xb, &e->zq, &e->u64, &e->u32, &e->u8, &e->counts, &e->depths, &e->y, &e->pole,
+    for (DevBuf* b : {&e->xb, &e->zq, &e->u64, &e->u32, &e->uop, &e->counts, &e->depths, &e->y, &e->pole,
                       &e->reflv, &e->reflmode, &e->dmin, &e->bestcnt, &e->tmp_in, &e->tmp_out0,
                       &e->tmp_out1, &e->tmp_out2, &e->tmp_out3})
         b->release();
@@ -618,7 +618,7 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
     CK(cudaMemcpyAsync(e->tmp_in.p, z, (size_t)d * 8, cudaMemcpyHostToDevice, e->stream));
     CK(launch_queries_to_f32(e->tmp_in.as<double>(), e->zq.as<float>(), d, e->stream));
     CK(launch_pack_directions(e->u64.as<double>(), e->u32.as<float>(), 1, m, p.mpad, d, e->stream));
-    if (p.tc) CK(launch_pack_limbs(e->u64.as<double>(), e->u8.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
+    if (p.tc) CK(launch_pack_tc_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (notion == RRS_HALFSPACE) {
         CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.mpad * 2 * 4, e->stream));
         if (int rc = contract_halfspace(e, p, 1)) return rc;

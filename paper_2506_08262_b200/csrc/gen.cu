@@ -7,6 +7,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cuda_fp16.h>
+
 #include <math.h>
 
 namespace rrs {
@@ -136,19 +138,18 @@ __device__ double pw_rec(const double* a, int n) {
 
 __device__ __forceinline__ double pw_sum(const double* a, int n) { return 0.0 + pw_rec(a, n); }
 
-// Tensor-path direction operand: U = rint(u * 2^22) (|u| <= 1) split into three
-// signed int8 limbs U = b2*2^16 + b1*2^8 + b0, stored in the canonical K-major
-// no-swizzle UMMA layout of a 128-direction block (the MMA M operand):
-//   [limb 3][k-chunk 4][direction 128][16 bytes]   (24 KB per block)
-// u8row points at (block, direction) = block base + (j & 127) * 16.
-__device__ __forceinline__ int quantize22(double u) { return __double2int_rn(u * 4194304.0); }
-__device__ __forceinline__ void put_limbs(unsigned char* u8row, int c, int U) {
-    const int U1 = (U + 128) >> 8;
-    const int U2 = (U1 + 128) >> 8;
-    unsigned char* p = u8row + (c >> 4) * 2048 + (c & 15);
-    p[0] = (unsigned char)(U & 0xFF);
-    p[8192] = (unsigned char)(U1 & 0xFF);
-    p[16384] = (unsigned char)(U2 & 0xFF);
+// Tensor-path direction operand (contract_tc.cu): u * 2^15 = hi + lo, both
+// FP16 (hi = fp16(u 2^15), lo = fp16(u 2^15 - hi), |u| <= 1), stored in the
+// canonical K-major no-swizzle layout of a 128-direction block (MMA A operand):
+//   [split 2][k chunk 8][direction 128][8 fp16]   (32 KB per block)
+// oprow points at (block, direction) = block base + (j & 127) * 16.
+__device__ __forceinline__ void put_tc_operand(unsigned char* oprow, int c, double u) {
+    const double v = u * 32768.0;
+    const __half h = __double2half(v);
+    const __half l = __double2half(v - (double)__half2float(h));
+    unsigned char* p = oprow + (c >> 3) * 2048 + (c & 7) * 2;
+    *reinterpret_cast<__half*>(p) = h;
+    *reinterpret_cast<__half*>(p + 16384) = l;
 }
 
 // ------------------------------------------------------- cap generation K1 --
@@ -171,13 +172,13 @@ __global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
     const int q = (int)(gdir / a.mpad);
     const int j = (int)(gdir % a.mpad);
     float* u32 = a.u32 + (size_t)q * a.mpad * d + (size_t)(j / BN) * d * BN + (j % BN);
-    unsigned char* u8 = nullptr;
-    if (a.u8 && j < a.nb8 * 128)
-        u8 = a.u8 + ((size_t)q * a.nb8 + (j >> 7)) * 24576 + (size_t)(j & 127) * 16;
+    unsigned char* op = nullptr;
+    if (a.uop && j < a.NB * 128)
+        op = a.uop + ((size_t)q * a.NB + (j >> 7)) * TC_DIR_BLOCK_BYTES + (size_t)(j & 127) * 16;
     if (j >= a.m) {
         for (int c = lane; c < d; c += 32) u32[(size_t)c * BN] = 0.0f;
-        if (u8)
-            for (int c = lane; c < 64; c += 32) put_limbs(u8, c, 0);
+        if (op)
+            for (int c = lane; c < 64; c += 32) put_tc_operand(op, c, 0.0);
         return;
     }
     const uint32_t qg = (uint32_t)((uint64_t)(a.q0 + q) & 0xFFFFFFFFu);
@@ -189,8 +190,8 @@ __global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
             u64[0] = pole[0];
             u32[0] = (float)pole[0];
         }
-        if (u8)
-            for (int c = lane; c < 64; c += 32) put_limbs(u8, c, c == 0 ? quantize22(pole[0]) : 0);
+        if (op)
+            for (int c = lane; c < 64; c += 32) put_tc_operand(op, c, c == 0 ? pole[0] : 0.0);
         return;
     }
     const int dm = d - 1;
@@ -239,8 +240,8 @@ __global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
         u64[c] = val;
         u32[(size_t)c * BN] = (float)val;
     }
-    if (u8)
-        for (int c = lane; c < 64; c += 32) put_limbs(u8, c, c < d ? quantize22(sc[c]) : 0);
+    if (op)
+        for (int c = lane; c < 64; c += 32) put_tc_operand(op, c, c < d ? sc[c] : 0.0);
 }
 
 // Explicit-direction mode: U64 given; build the FP32 contraction operand.
@@ -257,23 +258,23 @@ __global__ void pack_directions_kernel(const double* __restrict__ u64, float* __
     u32[(size_t)q * mpad * d + (size_t)(j / BN) * d * BN + (size_t)c * BN + (j % BN)] = v;
 }
 
-__global__ void pack_limbs_kernel(const double* __restrict__ u64, unsigned char* __restrict__ u8, int Qb,
-                                  int m, int nb8, int d) {
+__global__ void pack_tc_operand_kernel(const double* __restrict__ u64, unsigned char* __restrict__ uop, int Qb,
+                                       int m, int NB, int d) {
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t total = (int64_t)Qb * nb8 * 128 * 64;
+    int64_t total = (int64_t)Qb * NB * 128 * 64;
     if (idx >= total) return;
     int c = (int)(idx & 63);
     int64_t r = idx >> 6;
-    int j = (int)(r % (nb8 * 128));
-    int q = (int)(r / (nb8 * 128));
-    int U = (j < m && c < d) ? quantize22(u64[((size_t)q * m + j) * d + c]) : 0;
-    put_limbs(u8 + ((size_t)q * nb8 + (j >> 7)) * 24576 + (size_t)(j & 127) * 16, c, U);
+    int j = (int)(r % (NB * 128));
+    int q = (int)(r / (NB * 128));
+    double u = (j < m && c < d) ? u64[((size_t)q * m + j) * d + c] : 0.0;
+    put_tc_operand(uop + ((size_t)q * NB + (j >> 7)) * TC_DIR_BLOCK_BYTES + (size_t)(j & 127) * 16, c, u);
 }
 
-cudaError_t launch_pack_limbs(const double* u64, unsigned char* u8, int Qb, int m, int nb8, int d,
-                              cudaStream_t st) {
-    int64_t total = (int64_t)Qb * nb8 * 128 * 64;
-    pack_limbs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(u64, u8, Qb, m, nb8, d);
+cudaError_t launch_pack_tc_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,
+                                   cudaStream_t st) {
+    int64_t total = (int64_t)Qb * NB * 128 * 64;
+    pack_tc_operand_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(u64, uop, Qb, m, NB, d);
     return cudaGetLastError();
 }
 

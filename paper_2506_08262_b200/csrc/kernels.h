@@ -12,8 +12,8 @@ struct GenArgs {
     const double* refl_v;    // [Qb][d]
     double* u64;             // [Qb][m][d]
     float* u32;              // [Qb][mpad/BN][d][BN]
-    unsigned char* u8;       // nullable: [Qb][nb8][3 limbs][4][128][16] int8 limbs (tensor path)
-    int nb8;                 // 128-direction blocks per query in u8
+    unsigned char* uop;      // nullable: [Qb][NB][TC_DIR_BLOCK_BYTES] FP16 hi/lo operand (tensor path)
+    int NB;                  // 128-direction blocks per query in uop
     uint64_t seed;
     int64_t q0;              // global query index of batch row 0
     uint32_t refinement;
@@ -74,15 +74,19 @@ struct ContractArgs {
     int chunks;              // ceil(T / tiles_per_unit)
 };
 
-// Tensor-core (int8 limb) halfspace contraction, contract_tc.cu.
+// Tensor-core (FP16 hi/lo split) halfspace contraction, contract_tc.cu.
+constexpr int TC_DIR_BLOCK_BYTES = 32768;  // [2 splits][8 k chunks][128 directions][8 fp16]
 struct TcArgs {
     const float* xb;            // [T][d][128]
     const float* zq;            // [Qb][d]
-    const unsigned char* u8;    // [Qb][NB][3][4][128][16]
+    const unsigned char* uop;   // [Qb][NB][TC_DIR_BLOCK_BYTES] direction operand
     int* counts;                // [Qb][mpad][2]
     int64_t n;
     int64_t tiles;
     int d, Qb, NB, m, mpad;
+    // filled by launch_contract_tc
+    int groups, chunks, raw_stages;
+    int64_t tiles_per_chunk;
 };
 
 // Univariate projection depths from stored projections y (difference form).
@@ -111,9 +115,9 @@ cudaError_t launch_philox_words(const uint32_t* ctr, uint32_t* out, int64_t N, u
 cudaError_t launch_contract_count(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_contract_store(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
-cudaError_t launch_contract_tc(const TcArgs& a, int sms, cudaStream_t st);
-cudaError_t launch_pack_limbs(const double* u64, unsigned char* u8, int Qb, int m, int nb8, int d,
-                              cudaStream_t st);
+cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st);
+cudaError_t launch_pack_tc_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,
+                                   cudaStream_t st);
 size_t contract_tc_smem_bytes();
 size_t contract_smem_bytes(int d);
 
