@@ -355,7 +355,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 g.refl_mode = e->reflmode.as<int>();
                 g.refl_v = e->reflv.as<double>();
                 g.u64 = e->u64.as<double>();
-                g.u32 = e->u32.as<float>();
+                g.u32 = p.tc ? nullptr : e->u32.as<float>();  // the tensor path reads uop only
                 g.seed = cfg->seed;
                 g.q0 = q0 + b0;
                 g.refinement = (uint32_t)l;

@@ -81,20 +81,25 @@ __device__ __forceinline__ double p1evl(double x, const double* c, int deg) {
     return a;
 }
 
-__device__ double ndtri(double y0) {
-    const double s2pi = 2.50662827463100050242E0;
-    const double e2 = 0.13533528323661269189;  // exp(-2)
+constexpr double NDTRI_S2PI = 2.50662827463100050242E0;
+constexpr double NDTRI_E2 = 0.13533528323661269189;  // exp(-2)
+
+// ndtri's branch for exp(-2) < y0 <= 1 - exp(-2)
+__device__ __forceinline__ bool ndtri_is_central(double y0) {
+    return !(y0 > 1.0 - NDTRI_E2) && y0 > NDTRI_E2;
+}
+__device__ __forceinline__ double ndtri_central(double y0) {
+    double y = y0 - 0.5;
+    double y2 = y * y;
+    double x = y + y * (y2 * polevl(y2, c_P0, 4) / p1evl(y2, c_Q0, 8));
+    return x * NDTRI_S2PI;
+}
+__device__ __forceinline__ double ndtri_tail(double y0) {
     bool negate = true;
     double y = y0;
-    if (y > 1.0 - e2) {
+    if (y > 1.0 - NDTRI_E2) {
         y = 1.0 - y;
         negate = false;
-    }
-    if (y > e2) {
-        y = y - 0.5;
-        double y2 = y * y;
-        double x = y + y * (y2 * polevl(y2, c_P0, 4) / p1evl(y2, c_Q0, 8));
-        return x * s2pi;
     }
     double x = sqrt(-2.0 * log(y));
     double x0 = x - log(x) / x;
@@ -103,6 +108,9 @@ __device__ double ndtri(double y0) {
                           : z * polevl(z, c_P2, 8) / p1evl(z, c_Q2, 8);
     x = x0 - x1;
     return negate ? -x : x;
+}
+__device__ __forceinline__ double ndtri(double y0) {
+    return ndtri_is_central(y0) ? ndtri_central(y0) : ndtri_tail(y0);
 }
 
 // numpy float64 add.reduce over a contiguous row = 0.0 + pairwise sum
@@ -160,23 +168,19 @@ __device__ __forceinline__ void put_tc_operand(unsigned char* oprow, int c, doub
 // reflection vector prepared by the update kernel (directions.py:150-164).
 // Writes U64[q][j][d] (pole candidates) and U32[q][jb][d][BN] (contraction
 // operand, FP32, K-major per direction block); padded directions j >= m get 0.
-__global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
-    extern __shared__ double gsm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// One direction gdir (over Qb * mpad) on one warp; g, sc: 2*d doubles of scratch.
+__device__ void gen_direction_warp(const GenArgs& a, int64_t gdir, double* g, double* sc) {
+    const int lane = threadIdx.x & 31;
     const int d = a.d;
-    double* g = gsm + (size_t)warp * 2 * d;  // d values + d scratch
-    double* sc = g + d;
-    const int64_t gdir = (int64_t)blockIdx.x * 8 + warp;  // over Qb * mpad
-    const int64_t total = (int64_t)a.Qb * a.mpad;
-    if (gdir >= total) return;
     const int q = (int)(gdir / a.mpad);
     const int j = (int)(gdir % a.mpad);
-    float* u32 = a.u32 + (size_t)q * a.mpad * d + (size_t)(j / BN) * d * BN + (j % BN);
+    float* u32 = a.u32 ? a.u32 + (size_t)q * a.mpad * d + (size_t)(j / BN) * d * BN + (j % BN) : nullptr;
     unsigned char* op = nullptr;
     if (a.uop && j < a.NB * 128)
         op = a.uop + ((size_t)q * a.NB + (j >> 7)) * TC_DIR_BLOCK_BYTES + (size_t)(j & 127) * 16;
     if (j >= a.m) {
-        for (int c = lane; c < d; c += 32) u32[(size_t)c * BN] = 0.0f;
+        if (u32)
+            for (int c = lane; c < d; c += 32) u32[(size_t)c * BN] = 0.0f;
         if (op)
             for (int c = lane; c < 64; c += 32) put_tc_operand(op, c, 0.0);
         return;
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
     if (d == 1) {  // directions.py:172-173
         if (lane == 0) {
             u64[0] = pole[0];
-            u32[0] = (float)pole[0];
+            if (u32) u32[0] = (float)pole[0];
         }
         if (op)
             for (int c = lane; c < 64; c += 32) put_tc_operand(op, c, c == 0 ? pole[0] : 0.0);
@@ -238,10 +242,206 @@ __global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
     for (int c = lane; c < d; c += 32) {
         double val = sc[c];
         u64[c] = val;
-        u32[(size_t)c * BN] = (float)val;
+        if (u32) u32[(size_t)c * BN] = (float)val;
     }
     if (op)
         for (int c = lane; c < 64; c += 32) put_tc_operand(op, c, c < d ? sc[c] : 0.0);
+}
+
+__global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
+    extern __shared__ double gsm[];
+    const int warp = threadIdx.x >> 5;
+    const int64_t gdir = (int64_t)blockIdx.x * 8 + warp;  // over Qb * mpad
+    if (gdir >= (int64_t)a.Qb * a.mpad) return;
+    double* g = gsm + (size_t)warp * 2 * a.d;  // d values + d scratch
+    gen_direction_warp(a, gdir, g, g + a.d);
+}
+
+// K1 v2 (2 <= d <= 128): a block of GV_DIRS = 32 directions of one query,
+// element-parallel with the same FP64 operation sequence as the warp kernel:
+//   1. Philox uniforms of every (direction, coordinate) and the theta uniform;
+//   2. ndtri, with the central and tail elements compacted into separate lists
+//      so that no warp executes both branches (the tail branch is ~4x longer);
+//   3. squared norms in numpy's pairwise order, the 8 running partials on 8
+//      lanes and the ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree by shuffles;
+//   4. row = [cos theta, sqrt(1-cos^2) * g/|g|]; reflection (mode 1: negate
+//      e1, mode 2: Householder with f = 2 * pairwise(row . v));
+//   5. coalesced stores: U64 rows, U32 K-major block columns (FFMA / store
+//      paths only), the FP16 hi/lo tensor operand in 16-byte chunks.
+// A zero-norm normal row (the reference's redraw branch, directions.py:113-135)
+// cannot occur for 53-bit uniforms (ndtri(u) = 0 only at u = 0.5, which is not
+// on the (k + 0.5) 2^-53 grid); such a direction is regenerated by the warp path.
+constexpr int GV_DIRS = 32;
+constexpr int GV_THREADS = 256;
+constexpr int GV_MAX_D = 128;
+
+__device__ __forceinline__ double pw8_partial_tree(double r) {
+    // lanes k = 0..7 of an aligned 8-lane group hold r_k; lane 0 returns the tree sum
+    r += __shfl_down_sync(0xffffffffu, r, 1, 8);
+    r += __shfl_down_sync(0xffffffffu, r, 2, 8);
+    r += __shfl_down_sync(0xffffffffu, r, 4, 8);
+    return r;
+}
+
+// pairwise_sum(f(i), i < n) for n <= 128 on the 8-lane group of lane k (valid on k == 0);
+// F(i) produces element i (evaluated exactly as in the serial code).  Must be
+// called by all 32 lanes of the warp (full-mask shuffles).
+template <typename F>
+__device__ __forceinline__ double pw_sum8(int n, int k, F f) {
+    double res;
+    if (n < 8) {
+        res = 0.0;
+        if (k == 0)
+            for (int i = 0; i < n; ++i) res += f(i);
+        res = __shfl_sync(0xffffffffu, res, (threadIdx.x & 31) & ~7);
+    } else {
+        double r = f(k);
+        int i = 8;
+        for (; i < n - (n % 8); i += 8) r += f(i + k);
+        res = pw8_partial_tree(r);
+        if (k == 0)
+            for (; i < n; ++i) res += f(i);
+    }
+    return 0.0 + res;
+}
+
+__global__ void __launch_bounds__(GV_THREADS) cap_generate_v2_kernel(GenArgs a) {
+    extern __shared__ double vsm[];
+    const int d = a.d, dm = d - 1;
+    double* val = vsm;                          // [GV_DIRS][d] uniforms -> normals -> row
+    double* s_th = val + GV_DIRS * d;           // [GV_DIRS] theta uniform -> u1
+    double* s_nrm = s_th + GV_DIRS;             // [GV_DIRS]
+    uint16_t* list = reinterpret_cast<uint16_t*>(s_nrm + GV_DIRS);  // [GV_DIRS * dm]
+    __shared__ int s_nc, s_nt, s_zero;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t gdir0 = (int64_t)blockIdx.x * GV_DIRS;
+    const int q = (int)(gdir0 / a.mpad);
+    const int j0 = (int)(gdir0 % a.mpad);       // GV_DIRS | 128 | mpad: one query, one 128-block
+    const int nval = a.m - j0 < GV_DIRS ? (a.m - j0 > 0 ? a.m - j0 : 0) : GV_DIRS;
+    const uint32_t qg = (uint32_t)((uint64_t)(a.q0 + q) & 0xFFFFFFFFu);
+    const uint32_t l = a.refinement;
+    const int E = nval * dm;
+    if (tid == 0) {
+        s_nc = 0;
+        s_nt = 0;
+        s_zero = 0;
+    }
+    // 1. uniforms
+    for (int e = tid; e < E; e += GV_THREADS) {
+        const int jj = e / dm, c = e - jj * dm;
+        val[jj * d + 1 + c] = uniform1(a.seed, 1u + (uint32_t)c, (uint32_t)(j0 + jj), l, qg);
+    }
+    if (tid < nval) s_th[tid] = uniform1(a.seed, 0u, (uint32_t)(j0 + tid), l, qg);
+    __syncthreads();
+    // 2. ndtri: compact central / tail elements, then evaluate each list densely
+    for (int e0 = 0; e0 < E; e0 += GV_THREADS) {
+        const int e = e0 + tid;
+        bool cen = false, tl = false;
+        if (e < E) {
+            const int jj = e / dm;
+            const bool c_ = ndtri_is_central(val[jj * d + 1 + (e - jj * dm)]);
+            cen = c_;
+            tl = !c_;
+        }
+        const uint32_t bc = __ballot_sync(0xffffffffu, cen), bt = __ballot_sync(0xffffffffu, tl);
+        int pc = 0, pt = 0;
+        if (lane == 0) {
+            pc = atomicAdd(&s_nc, __popc(bc));
+            pt = atomicAdd(&s_nt, __popc(bt));
+        }
+        pc = __shfl_sync(0xffffffffu, pc, 0);
+        pt = __shfl_sync(0xffffffffu, pt, 0);
+        const uint32_t below = (1u << lane) - 1u;
+        if (cen) list[pc + __popc(bc & below)] = (uint16_t)e;
+        if (tl) list[E - 1 - (pt + __popc(bt & below))] = (uint16_t)e;
+    }
+    __syncthreads();
+    const int nc = s_nc, nt = s_nt;
+    for (int i = tid; i < nc; i += GV_THREADS) {
+        const int e = list[i], jj = e / dm;
+        double* p = &val[jj * d + 1 + (e - jj * dm)];
+        *p = ndtri_central(*p);
+    }
+    for (int i = tid; i < nt; i += GV_THREADS) {
+        const int e = list[E - 1 - i], jj = e / dm;
+        double* p = &val[jj * d + 1 + (e - jj * dm)];
+        *p = ndtri_tail(*p);
+    }
+    __syncthreads();
+    // 3. norms (8 lanes per direction), theta
+    {
+        const int jj = tid >> 3, k = tid & 7;
+        const double* g = val + jj * d + 1;
+        // every lane takes part in the shuffles; directions past nval sum zeros
+        const bool live = jj < nval;
+        const double nrm = sqrt(pw_sum8(dm, k, [&](int i) { return live ? g[i] * g[i] : 0.0; }));
+        if (k == 0 && jj < nval) {
+            s_nrm[jj] = nrm;
+            s_th[jj] = cos(s_th[jj] * a.eps);  // u1 = cos(theta)
+            if (nrm == 0.0) s_zero = 1;
+        }
+    }
+    __syncthreads();
+    const int mode = a.refl_mode[q];
+    const double* v = a.refl_v + (size_t)q * d;
+    // 4. row = [u1, s * (g / |g|)]
+    for (int e = tid; e < E; e += GV_THREADS) {
+        const int jj = e / dm;
+        const double u1 = s_th[jj], sf = sqrt(1.0 - u1 * u1);
+        double* p = &val[jj * d + 1 + (e - jj * dm)];
+        *p = sf * (*p / s_nrm[jj]);
+    }
+    if (tid < nval) val[tid * d] = (mode == 1) ? -s_th[tid] : s_th[tid];
+    __syncthreads();
+    if (mode == 2) {
+        const int jj = tid >> 3, k = tid & 7;
+        const bool live = jj < nval;
+        double f = 2.0 * pw_sum8(d, k, [&](int i) { return live ? val[jj * d + i] * v[i] : 0.0; });
+        f = __shfl_sync(0xffffffffu, f, lane & ~7);
+        __syncwarp();
+        if (jj < nval)
+            for (int c = k; c < d; c += 8) val[jj * d + c] = val[jj * d + c] - f * v[c];
+        __syncthreads();
+    }
+    // 5. stores
+    double* u64 = a.u64 + ((size_t)q * a.m + j0) * d;
+    for (int e = tid; e < nval * d; e += GV_THREADS) u64[e] = val[e];
+    if (a.u32) {
+        float* u32 = a.u32 + (size_t)q * a.mpad * d + (size_t)(j0 / BN) * d * BN + (j0 % BN);
+        for (int e = tid; e < GV_DIRS * d; e += GV_THREADS) {
+            const int c = e / GV_DIRS, jj = e - c * GV_DIRS;
+            u32[(size_t)c * BN + jj] = jj < nval ? (float)val[jj * d + c] : 0.0f;
+        }
+    }
+    if (a.uop) {
+        const int jj = tid & (GV_DIRS - 1), cc = tid >> 5;  // 32 directions x 8 k chunks
+        unsigned char* base = a.uop + ((size_t)q * a.NB + (j0 >> 7)) * TC_DIR_BLOCK_BYTES + cc * 2048 +
+                              (size_t)((j0 & 127) + jj) * 16;
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            __half h2[2], l2[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const int c = cc * 8 + 2 * e + t;
+                const double w = (jj < nval && c < d) ? val[jj * d + c] * 32768.0 : 0.0;
+                h2[t] = __double2half(w);
+                l2[t] = __double2half(w - (double)__half2float(h2[t]));
+            }
+            hw[e] = (uint32_t)__half_as_ushort(h2[0]) | ((uint32_t)__half_as_ushort(h2[1]) << 16);
+            lw[e] = (uint32_t)__half_as_ushort(l2[0]) | ((uint32_t)__half_as_ushort(l2[1]) << 16);
+        }
+        *reinterpret_cast<uint4*>(base) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(base + 16384) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+    if (s_zero) {
+        // unreachable for 53-bit uniforms: regenerate zero-norm directions on the warp
+        // path, which redraws exactly like the reference (all stores above are overwritten)
+        __syncthreads();
+        double* scratch = vsm + (size_t)warp * 2 * d;  // val is no longer needed
+        for (int jj = warp; jj < nval; jj += GV_THREADS / 32)
+            if (s_nrm[jj] == 0.0) gen_direction_warp(a, gdir0 + jj, scratch, scratch + d);
+    }
 }
 
 // Explicit-direction mode: U64 given; build the FP32 contraction operand.
@@ -458,6 +658,16 @@ __global__ void philox_words_kernel(const uint32_t* __restrict__ ctr, uint32_t* 
 // ----------------------------------------------------------------- launch --
 cudaError_t launch_cap_generate(const GenArgs& a, cudaStream_t st) {
     int64_t total = (int64_t)a.Qb * a.mpad;
+    if (a.d >= 2 && a.d <= GV_MAX_D && a.mpad % GV_DIRS == 0) {
+        const size_t smem = (size_t)GV_DIRS * a.d * 8 + 2 * GV_DIRS * 8 + (size_t)GV_DIRS * (a.d - 1) * 2 + 16;
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(cap_generate_v2_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+        }
+        cap_generate_v2_kernel<<<(unsigned)(total / GV_DIRS), GV_THREADS, smem, st>>>(a);
+        return cudaGetLastError();
+    }
     int blocks = (int)((total + 7) / 8);
     size_t smem = (size_t)8 * 2 * a.d * sizeof(double);
     if (smem > 48 * 1024) {

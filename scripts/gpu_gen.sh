@@ -1,0 +1,6 @@
+# profile the direction-generation kernel (K1) at the config-4 shape
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:cap_generate -c 1 -o gpurun_out/gen_c4 -f python scripts/profile_contract.py --q 1024 --r 1 > gpurun_out/ncu_gen.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:update_kernel -c 1 -o gpurun_out/upd_c4 -f python scripts/profile_contract.py --q 1024 --r 1 > gpurun_out/ncu_upd.log 2>&1
+echo done
