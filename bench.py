@@ -258,6 +258,7 @@ def main():
     launches = 0
     contract_ms = 0.0
     contract_launches = 0
+    tensor_launches = 0
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -270,6 +271,7 @@ def main():
         launches += st["kernel_launches"]
         contract_ms += st["ms_contract_total"]
         contract_launches += st["contract_launches"]
+        tensor_launches += st["tensor_contract_launches"]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -282,20 +284,42 @@ def main():
     ms_max = float(t.item())
     value = world * B * args.steps / (ms_max / 1e3)
 
-    # roofline of the dominant kernel (K2 contraction): algorithmic FLOPs per launch
-    flops_total = 2.0 * n * d * m * r * B * args.steps
-    avg_launch_ms = contract_ms / max(contract_launches, 1)
-    flops_per_launch = flops_total / max(contract_launches, 1)
+    # roofline of the dominant kernel (K2 contraction)
+    flops_total = 2.0 * n * d * m * r * B * args.steps  # algorithmic: 2 n d m per (query, refinement)
+    nl = max(contract_launches, 1)
+    avg_launch_ms = contract_ms / nl
+    flops_per_launch = flops_total / nl
     achieved = flops_per_launch / (avg_launch_ms / 1e3) / 1e12
+    peaks = measured_peaks()
     traffic = profile_traffic(wl)
-    roofline = {"bound": "fp32", "achieved": achieved, "peak": FP32_NOMINAL_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP32_NOMINAL_TFLOPS, "traffic": traffic,
-                "kernel": "contract_kernel<count>" if notion == "halfspace" else "contract_kernel<store>",
-                "peak_source": "nominal FP32 FFMA (148 SMs x 128 lanes x 2 x 1.965 GHz); MEASURED_PEAKS.json "
-                               "has no FP32 entry",
-                "flops_per_launch": flops_per_launch, "avg_launch_ms": avg_launch_ms,
-                "kernel_share_of_step": contract_ms / ms if ms else None,
-                "hbm_peak_measured_gbs": measured_peaks().get("hbm_gbs")}
+    tensor = tensor_launches == contract_launches and contract_launches > 0
+    if tensor:
+        # tcgen05 FP16-split path: executed tensor work = ns K-steps of M128 x N128 x K16 per
+        # (128-point tile, 128-direction block); peak = measured dense bf16 (same rate as fp16)
+        L_ns = 3 * (d // 16) + (3 * (d % 16) + 15) // 16
+        tiles, blocks = -(-n // 128), -(-m // 128)
+        exec_per_launch = 2.0 * 128 * 128 * 16 * L_ns * tiles * blocks * (B * args.steps * r / nl)
+        executed = exec_per_launch / (avg_launch_ms / 1e3) / 1e12
+        peak = peaks.get("bf16_tflops") or 2250.0
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": traffic, "kernel": "contract_tc_kernel",
+                    "peak_source": ("MEASURED_PEAKS.json bf16_tflops (dense, burst; fp16 runs at the bf16 rate)"
+                                    if peaks.get("bf16_tflops") else "nominal 2.25 PFLOP/s dense fp16"),
+                    "achieved_is": "algorithmic FLOPs 2*n*d*m per (query, refinement) / kernel time",
+                    "executed_tensor_tflops": executed, "executed_frac": executed / peak,
+                    "executed_note": f"split-precision work: {L_ns} MMA K-steps (3 products, packed K) per "
+                                     f"128x128 tile, directions padded to {blocks * 128}",
+                    "north_star_fp32": {"peak": FP32_NOMINAL_TFLOPS, "frac": achieved / FP32_NOMINAL_TFLOPS,
+                                        "note": "north_star roofline: n*d*K FLOPs at the FP32 FFMA peak"}}
+    else:
+        roofline = {"bound": "fp32", "achieved": achieved, "peak": FP32_NOMINAL_TFLOPS, "unit": "TFLOP/s",
+                    "frac": achieved / FP32_NOMINAL_TFLOPS, "traffic": traffic,
+                    "kernel": "contract_kernel<count>" if notion == "halfspace" else "contract_kernel<store>",
+                    "peak_source": "nominal FP32 FFMA (148 SMs x 128 lanes x 2 x 1.965 GHz); MEASURED_PEAKS.json "
+                                   "has no FP32 entry"}
+    roofline.update({"flops_per_launch": flops_per_launch, "avg_launch_ms": avg_launch_ms,
+                     "kernel_share_of_step": contract_ms / ms if ms else None,
+                     "hbm_peak_measured_gbs": peaks.get("hbm_gbs")})
 
     # e2e through the public API with host buffers (H2D of data + queries, D2H of results)
     e2e = None
@@ -336,7 +360,8 @@ def main():
         line = {
             "metric": "query-depths/s (RRS, all n points)", "value": value, "unit": "query-depths/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f16x2-split/f32-acc" if tensor else "f32",
             "data": "synthetic (reference generators: Toeplitz Gaussian / Student-t seed 0)",
             "config": {"workload": WORKLOAD_TEXT[wl], "notion": notion, "n": n, "d": d, "NRandom": k,
                        "n_refinements": r, "directions_per_refinement": m, "sphcap_shrink": alpha,

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define RRS_ABI_VERSION 1
+#define RRS_ABI_VERSION 2
 
 typedef enum {
     RRS_OK = 0,
@@ -107,8 +107,8 @@ int rrs_philox4x32_host(rrs_engine* e, const uint32_t* ctr, int64_t N, uint32_t 
                         uint32_t key1, uint32_t* out);
 
 /* Halfspace contraction kernel: 0 = auto (tensor cores when d <= 64 and
- * n >= 4096), 1 = FP32 FFMA (contract.cu), 2 = tcgen05 int8-limb exact
- * integer (contract_tc.cu; halfspace, d <= 64, m <= 4096). */
+ * n >= 4096), 1 = FP32 FFMA (contract.cu), 2 = tcgen05 FP16 hi/lo split with
+ * FP32 accumulation (contract_tc.cu; halfspace, d <= 64). */
 int rrs_engine_set_contract_path(rrs_engine* e, int32_t path);
 
 /* Diagnostics for the last batch: device time (ms) of each stage summed over
@@ -118,6 +118,7 @@ typedef struct {
     int64_t kernel_launches;
     int64_t contract_launches;
     double ms_contract_total; /* sum of contraction-kernel durations */
+    int64_t tensor_contract_launches; /* of contract_launches, on the tcgen05 kernel */
 } rrs_stats;
 int rrs_engine_stats(rrs_engine* e, rrs_stats* out);
 int rrs_engine_enable_timing(rrs_engine* e, int32_t on);

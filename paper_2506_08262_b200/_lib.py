@@ -47,6 +47,7 @@ class RrsStatsC(ctypes.Structure):
         ("kernel_launches", ctypes.c_int64),
         ("contract_launches", ctypes.c_int64),
         ("ms_contract_total", ctypes.c_double),
+        ("tensor_contract_launches", ctypes.c_int64),
     ]
 
 
@@ -100,7 +101,7 @@ def load_library():
                 fn = getattr(L, name)
                 fn.restype = res
                 fn.argtypes = args
-            if L.rrs_abi_version() != 1:
+            if L.rrs_abi_version() != 2:
                 raise RuntimeError("librrs_b200.so ABI version mismatch")
             _lib = L
     return _lib

@@ -8,7 +8,8 @@
 // product is a signed zero and y < 0 is false) and exact zeros count on both
 // sides (#<= = n - #>0, #>= = n - #<0).
 //
-// Operands ("two-term FP16 split", FP32-class accuracy):
+// Operands ("two-term FP16 split", FP32-class accuracy; packed along K as in
+// kernels.h tc_layout: d = 50 takes 10 K steps of 16 instead of 3 x 4):
 //   a_il = x_il - z_l (FP32, as in contract.cu), scaled per point by the power
 //          of two s_i = 2^(14 - E_i) with max_l |a_il| < 2^E_i (never changes a
 //          sign); a*s = ah + al, ah = fp16(a*s), al = fp16(a*s - ah): 22 bits;
@@ -23,23 +24,25 @@
 // per-instruction floor of tcgen05.mma (profiles/r1/tcgen05_mma_floor_*.txt);
 // this kernel runs N = 128 MMAs at the full 64-clock rate.
 //
-// Layout (M = 128 DIRECTIONS on TMEM lanes, N = 128 POINTS, K = 16 per MMA):
+// Layout (M = 128 DIRECTIONS on TMEM lanes, N = 128 POINTS, K = 16 per MMA,
+// ns = tc_layout(d).ns K steps per (tile, block)):
 //   TMEM columns [0,128) and [128,256): two FP32 accumulator buffers;
-//   TMEM columns [256 + 64 b, 256 + 64 b + 64): direction block b of the
-//   current unit (hi at +0, lo at +32; 16 K values = 8 columns per MMA),
-//   resident for the whole unit (TS MMA: A from TMEM, B from shared memory).
-// Work unit = (query, group of <= 4 direction blocks = 512 directions, chunk of
-// 128-point tiles); persistent CTAs (one per SM) stride over units.
-//   warp 0      producer: TMA of the unit's direction blocks (32 KB each, two at
-//               a time) into a staging area (cp.async.bulk + mbarrier);
+//   TMEM columns [256 + 8 ns b, 256 + 8 ns (b + 1)): direction block b of the
+//   current unit (8 columns = 16 K values per step), resident for the whole
+//   unit (TS MMA: A from TMEM, B from shared memory); gb = 256 / (8 ns) blocks
+//   (3 at d = 50).
+// Work unit = (query, group of gb direction blocks, chunk of 128-point tiles);
+// persistent CTAs (one per SM) stride over units.
+//   warp 0      producer: TMA of the unit's direction blocks (ns * 4 KB each, one
+//               at a time) into a staging area (cp.async.bulk + mbarrier);
 //   warp 1      TMEM allocator + tcgen05 issuer: staging -> TMEM (tcgen05.cp)
-//               once per unit, then per tile and block 3*ceil(d/16) MMAs;
+//               once per unit, then per tile and block ns MMAs;
 //   warp 2      producer: TMA of each raw FP32 point tile (d*512 bytes, the
 //               tile-blocked dataset) into a 2-4 stage ring;
 //   warps 3-10  converters: one (point, half of K) per thread: x - z from the
 //               staged tile, per-point power-of-two scale (max exchanged through
-//               shared memory), FP16 hi/lo split into the double-buffered
-//               point operand;
+//               shared memory), FP16 hi/lo split, placed at the packed K
+//               positions of the double-buffered point operand;
 //   warps 11-18 epilogue: tcgen05.ld of the accumulator (64 columns per thread),
 //               y < 0 counted per direction in registers, flushed per unit.
 // Replaces _kernels.pyx:120-199 (projection) + 270-289 (halfspace_span).
@@ -57,48 +60,42 @@ constexpr int TC_EPI_WARP0 = TC_CONV_WARP0 + TC_CONV_WARPS;  // first epilogue w
 constexpr int TC_EPI_WARPS = 8;                  // 4 lane quarters x 2 column halves
 constexpr int TC_EPI_THREADS = TC_EPI_WARPS * 32;
 constexpr int TC_THREADS = (TC_EPI_WARP0 + TC_EPI_WARPS) * 32;  // 608
-constexpr int TC_KP = 64;                        // K padded (d <= 64)
+constexpr int TC_MAXD = 64;                      // coordinates handled per point (2 x 32)
+constexpr int TC_MAXNS = 12;                     // K steps at d = 64
 constexpr int TC_MD = 128;                       // directions per block (MMA M)
 constexpr int TC_NP = 128;                       // points per tile (MMA N)
-constexpr int TC_GB = 4;                         // direction blocks resident per unit
-constexpr int TC_DPH = 2;                        // direction blocks per staging phase
-constexpr int P_SPLIT_BYTES = TC_NP * TC_KP * 2;  // 16 KB: one FP16 split of a tile
-constexpr int P_STAGE_BYTES = 2 * P_SPLIT_BYTES;  // 32 KB: hi + lo
+constexpr int TC_GB_MAX = 8;                     // direction blocks resident per unit (max)
 constexpr int P_STAGES = 2;
-constexpr int R_MAX_STAGES = 4;                   // raw FP32 tile ring (runtime depth)
-constexpr int D_SPLIT_BYTES = TC_MD * TC_KP * 2;  // 16 KB
-constexpr int D_BLOCK_BYTES = 2 * D_SPLIT_BYTES;  // 32 KB (= TC_DIR_BLOCK_BYTES)
+constexpr int R_MAX_STAGES = 4;                  // raw FP32 tile ring (runtime depth)
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t ACC_COLS = TC_NP;              // 128 per accumulator buffer
-constexpr uint32_t A_TMEM = 2 * ACC_COLS;         // 256: direction blocks (64 columns each)
-static_assert(A_TMEM + TC_GB * 64 <= TMEM_COLS, "TMEM budget");
-static_assert(D_BLOCK_BYTES == TC_DIR_BLOCK_BYTES, "direction operand block size");
+constexpr uint32_t ACC_COLS = TC_NP;             // 128 per accumulator buffer
+constexpr uint32_t A_TMEM = 2 * ACC_COLS;        // 256: direction blocks (8 ns columns each)
 constexpr int TC_SMEM_LIMIT = 227 * 1024;
 
+// Shared-memory layout (bytes from a 1024-aligned base), runtime in ns and d.
 struct TcSmem {
-    // offsets in bytes from a 1024-aligned base
-    static constexpr int P = 0;                                    // point operand stages
-    static constexpr int D = P + P_STAGES * P_STAGE_BYTES;         // direction staging, TC_DPH blocks
-    static constexpr int CNT = D + TC_DPH * D_BLOCK_BYTES;         // uint32 [TC_GB * 128]
-    static constexpr int ZS = CNT + TC_GB * TC_MD * 4;             // float [2][TC_KP] staged queries
-    static constexpr int SMX = ZS + 2 * TC_KP * 4;                 // float [2][2][128] partial |a| maxima
-    static constexpr int EXCL = SMX + 2 * 2 * TC_NP * 4;           // uint32 [8][4] excluded-point masks per tile
-    static constexpr int ZROWS = EXCL + 8 * 4 * 4;                 // uint32 [4] coinciding rows per unit slot
-    static constexpr int BARS = ZROWS + 16;                        // mbarriers
+    int P, D, CNT, ZS, SMX, EXCL, ZROWS, BARS, TADDR, RAW, total;
+    int stage_bytes, raw_stages;
     static constexpr int NBARS = 2 * P_STAGES + 2 + 2 + 3 + 2 * R_MAX_STAGES;
-    static constexpr int TADDR = BARS + NBARS * 8;
-    static constexpr int RAW = (TADDR + 16 + 1023) & ~1023;        // raw tiles, runtime d*512 bytes each
+    __host__ __device__ TcSmem(int ns, int d) {
+        stage_bytes = ns * 4096;                   // one packed tile / direction block
+        P = 0;                                     // P_STAGES point operands
+        D = P + P_STAGES * stage_bytes;            // direction staging (one block)
+        CNT = D + stage_bytes;                     // uint32 [TC_GB_MAX * 128]
+        ZS = CNT + TC_GB_MAX * TC_MD * 4;          // float [2][TC_MAXD] staged queries
+        SMX = ZS + 2 * TC_MAXD * 4;                // float [2][2][128] partial |a| maxima
+        EXCL = SMX + 2 * 2 * TC_NP * 4;            // uint32 [8][4] excluded-point masks per tile
+        ZROWS = EXCL + 8 * 4 * 4;                  // uint32 [4] coinciding rows per unit slot
+        BARS = ZROWS + 16;                         // mbarriers
+        TADDR = BARS + NBARS * 8;
+        RAW = (TADDR + 16 + 1023) & ~1023;         // raw FP32 tiles: 64 rows of 128 (rows >= d stay 0)
+        const int room = TC_SMEM_LIMIT - 1024 - RAW;
+        raw_stages = room / (TC_MAXD * TC_NP * 4);
+        if (raw_stages > R_MAX_STAGES) raw_stages = R_MAX_STAGES;
+        total = RAW + raw_stages * TC_MAXD * TC_NP * 4 + 1024;
+        (void)d;
+    }
 };
-
-int contract_tc_raw_stages(int d) {
-    const int room = TC_SMEM_LIMIT - 1024 - TcSmem::RAW;
-    int st = room / (d * TC_NP * 4);
-    return st > R_MAX_STAGES ? R_MAX_STAGES : st;
-}
-
-size_t contract_tc_smem_bytes(int d) {
-    return (size_t)TcSmem::RAW + (size_t)contract_tc_raw_stages(d) * d * TC_NP * 4 + 1024;
-}
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     // tcgen05 shared-memory descriptor: start>>4 [0,14), LBO>>4 [16,30),
@@ -107,71 +104,252 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
            ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
 
-// One (point tile, direction block) product: per K step of 16,
-//   D (+)= Ah*Bl, D += Al*Bh, D += Ah*Bh      (small terms first)
-// then the commit to the accumulator-full barrier, all under one elect with
-// immediate operand offsets (ptxas keeps it on the uniform datapath).
-//   acc: accumulator columns; aT: block's hi columns (lo at +32, K step at +8)
-//   bd : descriptor of the tile's hi split, K step 0 (K step +256, lo +1024)
-#define RRS_MMA3(KS, BH, BL, FIRSTP)                                                             \
-    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+" KS "], " BL ", %3, " FIRSTP ";\n"         \
-    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32+" KS "], " BH ", %3, 1;\n"                \
-    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+" KS "], " BH ", %3, 1;\n"
+// One (point tile, direction block) product: NS MMAs of K = 16 along the packed
+// split-product K axis, then the commit to the accumulator-full barrier, all
+// under one elect with immediate operand offsets (ptxas keeps the sequence on
+// the uniform datapath).
+//   acc: accumulator columns; aT: the block's A columns (K step i at +8 i)
+//   bd : descriptor of the tile's K step 0 (K step i at +4096 i bytes = +256 i)
+template <int NS>
+__device__ __forceinline__ void mma_tile_block(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar);
 
-template <int NKS>
-__device__ __forceinline__ void mma_tile_block(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc,
-                                               uint32_t bar) {
-    static_assert(NKS >= 1 && NKS <= 4, "K steps");
-    if constexpr (NKS == 1) {
-        asm volatile("{\n.reg .pred e;\n.reg .b64 l0;\nelect.sync _|e, 0xffffffff;\n"
-                     "add.s64 l0, %2, 1024;\n"
-                     RRS_MMA3("0", "%2", "l0", "0")
-                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                     ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-    } else if constexpr (NKS == 2) {
-        asm volatile("{\n.reg .pred e;\n.reg .b64 l0, h1, l1;\nelect.sync _|e, 0xffffffff;\n"
-                     "add.s64 l0, %2, 1024;\nadd.s64 h1, %2, 256;\nadd.s64 l1, %2, 1280;\n"
-                     RRS_MMA3("0", "%2", "l0", "0") RRS_MMA3("8", "h1", "l1", "1")
-                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                     ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-    } else if constexpr (NKS == 3) {
-        asm volatile("{\n.reg .pred e;\n.reg .b64 l0, h1, l1, h2, l2;\nelect.sync _|e, 0xffffffff;\n"
-                     "add.s64 l0, %2, 1024;\nadd.s64 h1, %2, 256;\nadd.s64 l1, %2, 1280;\n"
-                     "add.s64 h2, %2, 512;\nadd.s64 l2, %2, 1536;\n"
-                     RRS_MMA3("0", "%2", "l0", "0") RRS_MMA3("8", "h1", "l1", "1") RRS_MMA3("16", "h2", "l2", "1")
-                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                     ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-    } else {
-        asm volatile("{\n.reg .pred e;\n.reg .b64 l0, h1, l1, h2, l2, h3, l3;\nelect.sync _|e, 0xffffffff;\n"
-                     "add.s64 l0, %2, 1024;\nadd.s64 h1, %2, 256;\nadd.s64 l1, %2, 1280;\n"
-                     "add.s64 h2, %2, 512;\nadd.s64 l2, %2, 1536;\nadd.s64 h3, %2, 768;\nadd.s64 l3, %2, 1792;\n"
-                     RRS_MMA3("0", "%2", "l0", "0") RRS_MMA3("8", "h1", "l1", "1") RRS_MMA3("16", "h2", "l2", "1")
-                     RRS_MMA3("24", "h3", "l3", "1")
-                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                     ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-    }
+template <>
+__device__ __forceinline__ void mma_tile_block<1>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
 }
-#undef RRS_MMA3
 
-// Direction block b of the staging area (canonical K-major: [split][k chunk 8]
-// [direction 128][16 B]) -> TMEM columns [aT, aT + 64): eight 128x256b copies.
-__device__ __forceinline__ void tmem_cp_dirblock(uint32_t aT, uint64_t sd) {
-    // sd: descriptor of split 0, chunk 0; chunk pair +4096 B (256), split +16384 B (1024)
-    asm volatile(
-        "{\n.reg .pred e;\n.reg .b64 s1, s2, s3, s4, s5, s6, s7;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "add.s64 s1, %1, 256;\nadd.s64 s2, %1, 512;\nadd.s64 s3, %1, 768;\n"
-        "add.s64 s4, %1, 1024;\nadd.s64 s5, %1, 1280;\nadd.s64 s6, %1, 1536;\nadd.s64 s7, %1, 1792;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0+8], s1;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0+16], s2;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0+24], s3;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0+32], s4;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0+40], s5;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0+48], s6;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0+56], s7;\n"
-        "}\n" ::"r"(aT),
-        "l"(sd));
+template <>
+__device__ __forceinline__ void mma_tile_block<2>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    asm volatile("{\n.reg .pred e;\n.reg .b64 b1;\nelect.sync _|e, 0xffffffff;\n"
+                 "add.s64 b1, %2, 256;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+}
+
+template <>
+__device__ __forceinline__ void mma_tile_block<3>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2;\nelect.sync _|e, 0xffffffff;\n"
+                 "add.s64 b1, %2, 256;\n"
+                 "add.s64 b2, %2, 512;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+}
+
+template <>
+__device__ __forceinline__ void mma_tile_block<4>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3;\nelect.sync _|e, 0xffffffff;\n"
+                 "add.s64 b1, %2, 256;\n"
+                 "add.s64 b2, %2, 512;\n"
+                 "add.s64 b3, %2, 768;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+}
+
+template <>
+__device__ __forceinline__ void mma_tile_block<5>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4;\nelect.sync _|e, 0xffffffff;\n"
+                 "add.s64 b1, %2, 256;\n"
+                 "add.s64 b2, %2, 512;\n"
+                 "add.s64 b3, %2, 768;\n"
+                 "add.s64 b4, %2, 1024;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+}
+
+template <>
+__device__ __forceinline__ void mma_tile_block<6>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5;\nelect.sync _|e, 0xffffffff;\n"
+                 "add.s64 b1, %2, 256;\n"
+                 "add.s64 b2, %2, 512;\n"
+                 "add.s64 b3, %2, 768;\n"
+                 "add.s64 b4, %2, 1024;\n"
+                 "add.s64 b5, %2, 1280;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+}
+
+template <>
+__device__ __forceinline__ void mma_tile_block<7>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6;\nelect.sync _|e, 0xffffffff;\n"
+                 "add.s64 b1, %2, 256;\n"
+                 "add.s64 b2, %2, 512;\n"
+                 "add.s64 b3, %2, 768;\n"
+                 "add.s64 b4, %2, 1024;\n"
+                 "add.s64 b5, %2, 1280;\n"
+                 "add.s64 b6, %2, 1536;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+}
+
+template <>
+__device__ __forceinline__ void mma_tile_block<8>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7;\nelect.sync _|e, 0xffffffff;\n"
+                 "add.s64 b1, %2, 256;\n"
+                 "add.s64 b2, %2, 512;\n"
+                 "add.s64 b3, %2, 768;\n"
+                 "add.s64 b4, %2, 1024;\n"
+                 "add.s64 b5, %2, 1280;\n"
+                 "add.s64 b6, %2, 1536;\n"
+                 "add.s64 b7, %2, 1792;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+}
+
+template <>
+__device__ __forceinline__ void mma_tile_block<9>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7, b8;\nelect.sync _|e, 0xffffffff;\n"
+                 "add.s64 b1, %2, 256;\n"
+                 "add.s64 b2, %2, 512;\n"
+                 "add.s64 b3, %2, 768;\n"
+                 "add.s64 b4, %2, 1024;\n"
+                 "add.s64 b5, %2, 1280;\n"
+                 "add.s64 b6, %2, 1536;\n"
+                 "add.s64 b7, %2, 1792;\n"
+                 "add.s64 b8, %2, 2048;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], b8, %3, 1;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+}
+
+template <>
+__device__ __forceinline__ void mma_tile_block<10>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7, b8, b9;\nelect.sync _|e, 0xffffffff;\n"
+                 "add.s64 b1, %2, 256;\n"
+                 "add.s64 b2, %2, 512;\n"
+                 "add.s64 b3, %2, 768;\n"
+                 "add.s64 b4, %2, 1024;\n"
+                 "add.s64 b5, %2, 1280;\n"
+                 "add.s64 b6, %2, 1536;\n"
+                 "add.s64 b7, %2, 1792;\n"
+                 "add.s64 b8, %2, 2048;\n"
+                 "add.s64 b9, %2, 2304;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], b8, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], b9, %3, 1;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+}
+
+template <>
+__device__ __forceinline__ void mma_tile_block<11>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7, b8, b9, b10;\nelect.sync _|e, 0xffffffff;\n"
+                 "add.s64 b1, %2, 256;\n"
+                 "add.s64 b2, %2, 512;\n"
+                 "add.s64 b3, %2, 768;\n"
+                 "add.s64 b4, %2, 1024;\n"
+                 "add.s64 b5, %2, 1280;\n"
+                 "add.s64 b6, %2, 1536;\n"
+                 "add.s64 b7, %2, 1792;\n"
+                 "add.s64 b8, %2, 2048;\n"
+                 "add.s64 b9, %2, 2304;\n"
+                 "add.s64 b10, %2, 2560;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], b8, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], b9, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+80], b10, %3, 1;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+}
+
+template <>
+__device__ __forceinline__ void mma_tile_block<12>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7, b8, b9, b10, b11;\nelect.sync _|e, 0xffffffff;\n"
+                 "add.s64 b1, %2, 256;\n"
+                 "add.s64 b2, %2, 512;\n"
+                 "add.s64 b3, %2, 768;\n"
+                 "add.s64 b4, %2, 1024;\n"
+                 "add.s64 b5, %2, 1280;\n"
+                 "add.s64 b6, %2, 1536;\n"
+                 "add.s64 b7, %2, 1792;\n"
+                 "add.s64 b8, %2, 2048;\n"
+                 "add.s64 b9, %2, 2304;\n"
+                 "add.s64 b10, %2, 2560;\n"
+                 "add.s64 b11, %2, 2816;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], b8, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], b9, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+80], b10, %3, 1;\n"
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+88], b11, %3, 1;\n"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
+                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+}
+
+// A direction block in the staging area (canonical K-major [kk/8][128][16 B]) ->
+// TMEM columns [aT, aT + 8 ns): one 128x256b copy (two 16-byte chunks) per K
+// step (once per unit, so a plain loop of elected copies).
+__device__ __forceinline__ void tmem_cp_dirblock(uint32_t aT, uint64_t sd, int ns) {
+    for (int i = 0; i < ns; ++i)
+        asm volatile(
+            "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+            "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"(aT + 8u * (uint32_t)i),
+            "l"(sd + 256ull * (uint64_t)i));
 }
 
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
@@ -251,42 +429,41 @@ __device__ __forceinline__ TcUnit tc_unit(const TcArgs& a, int64_t u) {
     const int64_t rem = u - (int64_t)r.q * per_q;
     r.grp = (int)(rem / a.chunks);
     const int64_t c = rem - (int64_t)r.grp * a.chunks;
-    r.nbg = a.NB - r.grp * TC_GB < TC_GB ? a.NB - r.grp * TC_GB : TC_GB;
+    r.nbg = a.NB - r.grp * a.gb < a.gb ? a.NB - r.grp * a.gb : a.gb;
     r.t0 = c * a.tiles_per_chunk;
     r.t1 = r.t0 + a.tiles_per_chunk < a.tiles ? r.t0 + a.tiles_per_chunk : a.tiles;
     return r;
 }
 
-template <int NKS>
+template <int NS>
 __device__ __forceinline__ void mma_issue(const TcArgs& a, int64_t units, unsigned char* sP, unsigned char* sD,
                                           uint64_t* pfull, uint64_t* pempty, uint64_t* dfull, uint64_t* dempty,
                                           uint64_t* tfull, uint64_t* tempty, uint64_t* udone) {
     constexpr uint32_t tmem = 0u;
+    constexpr uint32_t stage_bytes = NS * 4096;
     // F32 accumulate, FP16 A and B, K-major both, N = 128, M = 128
     const uint32_t idesc = (1u << 4) | ((uint32_t)(TC_NP >> 3) << 17) | ((uint32_t)(TC_MD >> 4) << 24);
     uint32_t it = 0, gtile = 0, gacc = 0, gph = 0;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
         const TcUnit w = tc_unit(a, u);
-        const uint32_t dbase = smem_u32(sD);
-        for (int b0 = 0; b0 < w.nbg; b0 += TC_DPH, ++gph) {
+        for (int b = 0; b < w.nbg; ++b, ++gph) {
             mbar_wait_sleep(dfull, gph & 1u);
-            if (b0 == 0 && it > 0) mbar_wait(udone, (it - 1) & 1u);  // previous unit no longer reads TMEM A
+            if (b == 0 && it > 0) mbar_wait(udone, (it - 1) & 1u);  // previous unit no longer reads TMEM A
             tc_fence_after();
-            for (int b = b0; b < w.nbg && b < b0 + TC_DPH; ++b)
-                tmem_cp_dirblock(tmem + A_TMEM + 64u * b, umma_desc(dbase + (b - b0) * D_BLOCK_BYTES, 2048, 128));
+            tmem_cp_dirblock(tmem + A_TMEM + 8u * NS * b, umma_desc(smem_u32(sD), 2048, 128), NS);
             mma_commit_elect(dempty);  // staging free once the copies are done
         }
         for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
             const uint32_t s = gtile % P_STAGES;
             mbar_wait(&pfull[s], (gtile / P_STAGES) & 1u);
             tc_fence_after();
-            const uint64_t bd = umma_desc(smem_u32(sP) + s * P_STAGE_BYTES, 2048, 128);
+            const uint64_t bd = umma_desc(smem_u32(sP) + s * stage_bytes, 2048, 128);
             for (int b = 0; b < w.nbg; ++b, ++gacc) {
                 const uint32_t buf = gacc & 1u;
                 if (gacc >= 2) mbar_wait(&tempty[buf], ((gacc >> 1) - 1) & 1u);
                 tc_fence_after();
-                mma_tile_block<NKS>(tmem + buf * ACC_COLS, tmem + A_TMEM + 64u * b, bd, idesc,
-                                    smem_u32(&tfull[buf]));
+                mma_tile_block<NS>(tmem + buf * ACC_COLS, tmem + A_TMEM + 8u * NS * b, bd, idesc,
+                                   smem_u32(&tfull[buf]));
             }
             mma_commit_elect(&pempty[s]);  // point stage free once this tile's MMAs are done
         }
@@ -298,33 +475,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     extern __shared__ __align__(1024) unsigned char tc_raw[];
     // 1024-align by pointer arithmetic on the __shared__ array (keeps the address space)
     unsigned char* sm = tc_raw + ((1024u - (smem_u32(tc_raw) & 1023u)) & 1023u);
-    unsigned char* sP = sm + TcSmem::P;
-    unsigned char* sD = sm + TcSmem::D;
-    uint32_t* sCnt = reinterpret_cast<uint32_t*>(sm + TcSmem::CNT);
-    float* sZ = reinterpret_cast<float*>(sm + TcSmem::ZS);
-    uint32_t* sZrows = reinterpret_cast<uint32_t*>(sm + TcSmem::ZROWS);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + TcSmem::BARS);
+    const int d = a.d;
+    const TcLayout L = tc_layout(d);
+    const TcSmem lay(L.ns, d);
+    const int stage_bytes = lay.stage_bytes;
+    unsigned char* sP = sm + lay.P;
+    unsigned char* sD = sm + lay.D;
+    uint32_t* sCnt = reinterpret_cast<uint32_t*>(sm + lay.CNT);
+    float* sZ = reinterpret_cast<float*>(sm + lay.ZS);
+    float* sMx = reinterpret_cast<float*>(sm + lay.SMX);
+    uint32_t* sExcl = reinterpret_cast<uint32_t*>(sm + lay.EXCL);
+    uint32_t* sZrows = reinterpret_cast<uint32_t*>(sm + lay.ZROWS);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + lay.BARS);
     uint64_t* pfull = &bars[0];                   // [P_STAGES] point tile converted (converter warps)
     uint64_t* pempty = &bars[P_STAGES];           // [P_STAGES] MMAs reading it completed
     uint64_t* tfull = &bars[2 * P_STAGES];        // [2] accumulator ready
     uint64_t* tempty = &bars[2 * P_STAGES + 2];   // [2] accumulator drained (epilogue warps)
-    uint64_t* dfull = &bars[2 * P_STAGES + 4];    // direction staging phase loaded
+    uint64_t* dfull = &bars[2 * P_STAGES + 4];    // direction staging loaded
     uint64_t* dempty = &bars[2 * P_STAGES + 5];   // direction staging copied to TMEM
     uint64_t* udone = &bars[2 * P_STAGES + 6];    // all MMAs of a unit completed
     uint64_t* rfull = &bars[2 * P_STAGES + 7];    // [R_MAX_STAGES] raw tile landed
     uint64_t* rempty = &bars[2 * P_STAGES + 7 + R_MAX_STAGES];  // [R_MAX_STAGES] raw tile read
-    float* sMx = reinterpret_cast<float*>(sm + TcSmem::SMX);
-    uint32_t* sExcl = reinterpret_cast<uint32_t*>(sm + TcSmem::EXCL);
-    float* sRaw = reinterpret_cast<float*>(sm + TcSmem::RAW);
-    const int RS = a.raw_stages;
-    const uint32_t raw_bytes = (uint32_t)(a.d * TC_NP * 4);
-    uint32_t* sTaddr = reinterpret_cast<uint32_t*>(sm + TcSmem::TADDR);
+    uint32_t* sTaddr = reinterpret_cast<uint32_t*>(sm + lay.TADDR);
+    float* sRaw = reinterpret_cast<float*>(sm + lay.RAW);
+    const int RS = lay.raw_stages;
+    const uint32_t raw_bytes = (uint32_t)(d * TC_NP * 4);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int d = a.d;
     const int64_t units = (int64_t)a.Qb * a.groups * a.chunks;
 
-    for (int c = tid; c < TC_GB * TC_MD; c += TC_THREADS) sCnt[c] = 0u;
+    // point operand stages start zeroed: K positions past the packed products
+    // are never written again, so they stay 0 (A is 0 there too)
+    for (int i = tid; i < P_STAGES * stage_bytes / 16; i += TC_THREADS)
+        reinterpret_cast<uint4*>(sP)[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = tid; i < RS * TC_MAXD * TC_NP; i += TC_THREADS) sRaw[i] = 0.0f;  // rows >= d stay 0
+    for (int c = tid; c < TC_GB_MAX * TC_MD; c += TC_THREADS) sCnt[c] = 0u;
     if (tid < 4) sZrows[tid] = 0u;
     if (tid == 0) {
         for (int s = 0; s < P_STAGES; ++s) {
@@ -349,6 +534,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                      "r"(TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    fence_proxy_async();  // zeroed operand stages -> tensor-core reads
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -359,84 +545,103 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     constexpr uint32_t tmem = 0u;
 
     if (warp == 0) {
-        // ----------------------------- producer: unit direction blocks, 2 per phase
+        // -------------------------------- producer: unit direction blocks, one at a time
         uint32_t gph = 0;
         for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
             const TcUnit w = tc_unit(a, u);
-            const unsigned char* src =
-                a.uop + ((size_t)w.q * a.NB + (size_t)w.grp * TC_GB) * D_BLOCK_BYTES;
-            for (int b0 = 0; b0 < w.nbg; b0 += TC_DPH, ++gph) {
-                const int nb = w.nbg - b0 < TC_DPH ? w.nbg - b0 : TC_DPH;
+            const unsigned char* src = a.uop + ((size_t)w.q * a.NB + (size_t)w.grp * a.gb) * stage_bytes;
+            for (int b = 0; b < w.nbg; ++b, ++gph) {
                 if (gph > 0) mbar_wait_sleep(dempty, (gph - 1) & 1u);
-                expect_tx_elect(dfull, (uint32_t)(nb * D_BLOCK_BYTES));
-                for (int b = 0; b < nb; ++b)
-                    tma_load_elect(sD + b * D_BLOCK_BYTES, src + (size_t)(b0 + b) * D_BLOCK_BYTES, D_BLOCK_BYTES,
-                                   dfull);
-                __syncwarp();
-            }
-        }
-    } else if (warp == 2) {
-        // -------------------------------------- producer: raw FP32 point tiles
-        uint32_t g = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-            const TcUnit w = tc_unit(a, u);
-            for (int64_t t = w.t0; t < w.t1; ++t, ++g) {
-                const uint32_t rs = g % RS;
-                if (g >= (uint32_t)RS) mbar_wait_sleep(&rempty[rs], ((g / RS) - 1) & 1u);
-                expect_tx_elect(&rfull[rs], raw_bytes);
-                tma_load_elect(sRaw + (size_t)rs * d * TC_NP, a.xb + (size_t)t * d * TC_NP, raw_bytes, &rfull[rs]);
+                expect_tx_elect(dfull, (uint32_t)stage_bytes);
+                tma_load_elect(sD, src + (size_t)b * stage_bytes, (uint32_t)stage_bytes, dfull);
                 __syncwarp();
             }
         }
     } else if (warp == 1) {
         // -------------------------------------------------------- MMA issuer
-        switch ((d + 15) >> 4) {
+        switch (L.ns) {
             case 1: mma_issue<1>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
             case 2: mma_issue<2>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
             case 3: mma_issue<3>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
-            default: mma_issue<4>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+            case 4: mma_issue<4>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+            case 5: mma_issue<5>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+            case 6: mma_issue<6>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+            case 7: mma_issue<7>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+            case 8: mma_issue<8>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+            case 9: mma_issue<9>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+            case 10: mma_issue<10>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+            case 11: mma_issue<11>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+            default: mma_issue<12>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+        }
+    } else if (warp == 2) {
+        // -------------------------------------- producer: raw FP32 point tiles
+        uint32_t g = 0, rs = 0, rph = 0;  // ring slot and its phase, advanced incrementally
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+            const TcUnit w = tc_unit(a, u);
+            for (int64_t t = w.t0; t < w.t1; ++t, ++g) {
+                if (g >= (uint32_t)RS) mbar_wait_sleep(&rempty[rs], rph ^ 1u);
+                expect_tx_elect(&rfull[rs], raw_bytes);
+                tma_load_elect(sRaw + (size_t)rs * TC_MAXD * TC_NP, a.xb + (size_t)t * d * TC_NP, raw_bytes, &rfull[rs]);
+                __syncwarp();
+                if (++rs == (uint32_t)RS) {
+                    rs = 0;
+                    rph ^= 1u;
+                }
+            }
         }
     } else if (warp < TC_EPI_WARP0) {
         // ----------------------- converters: x - z -> scale -> FP16 hi/lo split
         const int ct = tid - TC_CONV_WARP0 * 32;  // 0..255
         const int r = ct & (TC_NP - 1);           // point of the tile
-        const int h = ct >> 7;                    // K half: coordinates [32 h, 32 h + 32)
-        uint32_t it = 0, gtile = 0;
+        const int h = ct >> 7;                    // coordinates [32 h, 32 h + 32)
+        const int main_chunks = 2 * L.q16;        // 8-coordinate chunks in the aligned part
+        uint32_t it = 0, gtile = 0, rs = 0, rph = 0;
         for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
             const TcUnit w = tc_unit(a, u);
-            float* zs = sZ + (it & 1u) * TC_KP;
-            if (ct < TC_KP) zs[ct] = ct < d ? __ldg(a.zq + (size_t)w.q * d + ct) : 0.0f;
+            float* zs = sZ + (it & 1u) * TC_MAXD;
+            if (ct < TC_MAXD) zs[ct] = ct < d ? __ldg(a.zq + (size_t)w.q * d + ct) : 0.0f;
             named_bar(2, TC_CONV_THREADS);  // zs ready; keeps the converter warps in step per unit
             uint32_t zcount = 0;
             for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
                 const uint32_t s = gtile % P_STAGES;
-                const uint32_t rs = gtile % RS;
                 const bool ok = t * TC_NP + r < a.n;
-                mbar_wait(&rfull[rs], (gtile / RS) & 1u);
-                // staged tile [d][128]: lane-consecutive points, conflict-free
-                const float* X = sRaw + (size_t)rs * d * TC_NP + r;
+                mbar_wait(&rfull[rs], rph);
+                // staged tile [64][128] (rows >= d are 0, zs too): lane-consecutive points,
+                // conflict-free, immediate offsets; chunks past d are skipped (warp-uniform)
+                const float* X = sRaw + (size_t)rs * TC_MAXD * TC_NP + 32 * h * TC_NP + r;
+                const float* zh = zs + 32 * h;
                 float av[32];
                 float mx = 0.0f;
 #pragma unroll
-                for (int k = 0; k < 32; k += 4) {
-                    const float4 z4 = *reinterpret_cast<const float4*>(zs + 32 * h + k);
-                    const float zz[4] = {z4.x, z4.y, z4.z, z4.w};
+                for (int c = 0; c < 4; ++c) {
+                    if (8 * (4 * h + c) < d) {
+                        const float4 z0 = *reinterpret_cast<const float4*>(zh + 8 * c);
+                        const float4 z1 = *reinterpret_cast<const float4*>(zh + 8 * c + 4);
+                        const float zz[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int kk = 32 * h + k + e;
-                        av[k + e] = (ok && kk < d) ? (X[kk * TC_NP] - zz[e]) : 0.0f;
-                        mx = fmaxf(mx, fabsf(av[k + e]));
+                        for (int e = 0; e < 8; ++e) {
+                            av[8 * c + e] = X[(8 * c + e) * TC_NP] - zz[e];
+                            mx = fmaxf(mx, fabsf(av[8 * c + e]));
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) av[8 * c + e] = 0.0f;
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&rempty[rs]);  // raw tile consumed (loads ordered by release)
+                if (++rs == (uint32_t)RS) {
+                    rs = 0;
+                    rph ^= 1u;
+                }
                 float* mxs = sMx + (gtile & 1u) * 2 * TC_NP;
                 mxs[h * TC_NP + r] = mx;
-                named_bar(2, TC_CONV_THREADS);  // both K halves' maxima visible
+                named_bar(2, TC_CONV_THREADS);  // both halves' maxima visible
                 mx = fmaxf(mxs[r], mxs[TC_NP + r]);
                 if (h == 0) {
                     // points the epilogue must not count: coinciding rows (every product a
-                    // signed zero, ties on both sides) and rows beyond n
+                    // signed zero, ties on both sides) and rows beyond n (their operand is
+                    // finite garbage, x = 0 padding minus z)
                     zcount += (ok && mx == 0.0f) ? 1u : 0u;
                     const uint32_t ex = __ballot_sync(0xffffffffu, !ok || mx == 0.0f);
                     if (lane == 0) sExcl[(gtile & 7u) * 4 + (r >> 5)] = ex;
@@ -448,10 +653,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                     scale = __uint_as_float((uint32_t)(127 + 14 - E) << 23);  // 2^(14-E)
                 }
                 if (gtile >= P_STAGES) mbar_wait(&pempty[s], ((gtile / P_STAGES) - 1) & 1u);
-                // canonical K-major, no swizzle: [split][k chunk c (8 values)][point r][16 bytes]
-                unsigned char* P = sP + s * P_STAGE_BYTES + r * 16;
+                // packed K layout (kernels.h tc_layout), canonical K-major:
+                // [kk / 8][point r][16 bytes]
+                unsigned char* P = sP + s * stage_bytes + r * 16;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
+                    const int cc = 4 * h + c;  // coordinate chunk
+                    if (8 * cc >= d) continue;
                     uint32_t hw[4], lw[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -461,10 +669,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                         hw[e] = *reinterpret_cast<const uint32_t*>(&hh);
                         lw[e] = pack_half2(v0 - hf.x, v1 - hf.y);
                     }
-                    const int cc = 4 * h + c;
-                    *reinterpret_cast<uint4*>(P + cc * (TC_NP * 16)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-                    *reinterpret_cast<uint4*>(P + P_SPLIT_BYTES + cc * (TC_NP * 16)) =
-                        make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                    if (cc < main_chunks) {
+                        // aligned part: products 0 (hi), 1 (lo), 2 (hi) of coordinates 8 cc .. 8 cc + 7
+                        const uint4 hv = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                        *reinterpret_cast<uint4*>(P + cc * (TC_NP * 16)) = hv;
+                        *reinterpret_cast<uint4*>(P + (main_chunks + cc) * (TC_NP * 16)) =
+                            make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                        *reinterpret_cast<uint4*>(P + (2 * main_chunks + cc) * (TC_NP * 16)) = hv;
+                    } else {
+                        // remainder coordinates 16 Q + i: scattered into the tail K steps
+                        // (a rolled loop: at most two such chunks, d % 16 values)
+#pragma unroll 1
+                        for (int e = 0; e < 8; ++e) {
+                            const int cd = 8 * cc + e;
+                            if (cd >= d) break;
+                            const int wi = e >> 1;
+                            const uint32_t hv = wi == 0 ? hw[0] : wi == 1 ? hw[1] : wi == 2 ? hw[2] : hw[3];
+                            const uint32_t lv = wi == 0 ? lw[0] : wi == 1 ? lw[1] : wi == 2 ? lw[2] : lw[3];
+                            const uint16_t hb = (uint16_t)((e & 1) ? (hv >> 16) : (hv & 0xFFFFu));
+                            const uint16_t lb = (uint16_t)((e & 1) ? (lv >> 16) : (lv & 0xFFFFu));
+                            int kk = 32 * L.q16 + cd;  // 48 Q + (cd - 16 Q): product 0
+#pragma unroll
+                            for (int pr = 0; pr < 3; ++pr, kk += L.rem)
+                                *reinterpret_cast<uint16_t*>(P + (kk >> 3) * (TC_NP * 16) + (kk & 7) * 2) =
+                                    pr == 1 ? lb : hb;
+                        }
+                    }
                 }
                 fence_proxy_async();  // generic-proxy smem writes -> tensor-core reads
                 __syncwarp();
@@ -483,11 +713,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
         uint32_t it = 0, gacc = 0, gtile = 0;
         for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
             const TcUnit w = tc_unit(a, u);
-            uint32_t cnt[TC_GB] = {0u, 0u, 0u, 0u};  // #(y<0) per resident block
+            uint32_t cnt[TC_GB_MAX];  // #(y<0) per resident block
+#pragma unroll
+            for (int b = 0; b < TC_GB_MAX; ++b) cnt[b] = 0u;
             for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
                 uint32_t keep0 = 0u, keep1 = 0u;
 #pragma unroll
-                for (int b = 0; b < TC_GB; ++b) {
+                for (int b = 0; b < TC_GB_MAX; ++b) {
                     if (b < w.nbg) {
                         const uint32_t buf = gacc & 1u;
                         mbar_wait(&tfull[buf], (gacc >> 1) & 1u);
@@ -521,7 +753,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                 }
             }
 #pragma unroll
-            for (int b = 0; b < TC_GB; ++b)
+            for (int b = 0; b < TC_GB_MAX; ++b)
                 if (b < w.nbg) atomicAdd(sCnt + b * TC_MD + 32 * quarter + lane, cnt[b]);
             named_bar(1, TC_EPI_THREADS);  // all direction counts of this unit are in
             // #(y>0) = real rows - coinciding rows - #(y<0); an exact zero from a
@@ -531,7 +763,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
             const int valid = (int)(r1 - w.t0 * TC_NP);
             const int zrows = (int)sZrows[it & 3u];
             int* dst = a.counts + (size_t)w.q * a.mpad * 2;
-            const int j0 = w.grp * TC_GB * TC_MD;
+            const int j0 = w.grp * a.gb * TC_MD;
             for (int c = ct; c < w.nbg * TC_MD; c += TC_EPI_THREADS) {
                 const int lt = (int)sCnt[c];
                 sCnt[c] = 0u;
@@ -551,7 +783,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
 }
 
 void plan_contract_tc(TcArgs& a, int sms) {
-    a.groups = (a.NB + TC_GB - 1) / TC_GB;
+    const TcLayout L = tc_layout(a.d);
+    int gb = (int)(256 / (8 * L.ns));  // direction blocks that fit the 256 A columns of TMEM
+    if (gb > TC_GB_MAX) gb = TC_GB_MAX;
+    a.gb = gb;
+    a.groups = (a.NB + gb - 1) / gb;
     // split the point tiles into chunks so that every SM gets >= ~16 units
     const int64_t base = (int64_t)a.Qb * a.groups;
     int64_t chunks = (16LL * sms + base - 1) / base;
@@ -562,11 +798,12 @@ void plan_contract_tc(TcArgs& a, int sms) {
 }
 
 cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st) {
-    if (a.d > TC_KP || a.d < 1) return cudaErrorInvalidValue;
+    if (a.d > TC_MAXD || a.d < 1 || tc_layout(a.d).ns > TC_MAXNS) return cudaErrorInvalidValue;
     plan_contract_tc(a, sms);
-    a.raw_stages = contract_tc_raw_stages(a.d);
+    const TcSmem lay(tc_layout(a.d).ns, a.d);
+    a.raw_stages = lay.raw_stages;
     if (a.raw_stages < 2) return cudaErrorInvalidValue;
-    const size_t smem = contract_tc_smem_bytes(a.d);
+    const size_t smem = (size_t)lay.total;
     cudaError_t e =
         cudaFuncSetAttribute(contract_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -154,7 +154,7 @@ int validate_cfg(const rrs_config* c) {
 struct Plan {
     int m, mpad, MB, Qb;
     bool tc;     // tensor-core FP16-split contraction (halfspace, d <= 64)
-    int nb8;     // 128-direction blocks per query (tensor path operand, TC_DIR_BLOCK_BYTES each)
+    int nb8;     // 128-direction blocks per query (tensor path operand, tc_block_bytes(d) each)
     int jchunk;  // direction blocks per store launch (projection notions)
     int tpu, chunks;
 };
@@ -169,7 +169,7 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     p.tc = tc_ok && (e->contract_path == 2 || (e->contract_path == 0 && e->n >= 4096));
     const int64_t d = e->d, n = e->n;
     int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * d * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 8 +
-                    d * 40 + 64 + (int64_t)p.nb8 * TC_DIR_BLOCK_BYTES;
+                    d * 40 + 64 + (int64_t)p.nb8 * tc_block_bytes(e->d);
     int64_t budget = e->ws_limit;
     int64_t qb = 4096;
     if (notion != RRS_HALFSPACE) {
@@ -216,7 +216,7 @@ int ensure_ws(rrs_engine* e, const Plan& p, int notion) {
     CK(e->reflmode.ensure(Qb * 4));
     CK(e->dmin.ensure(Qb * 8));
     CK(e->bestcnt.ensure(Qb * 8));
-    CK(e->uop.ensure(p.tc ? Qb * (size_t)p.nb8 * TC_DIR_BLOCK_BYTES : 16));
+    CK(e->uop.ensure(p.tc ? Qb * (size_t)p.nb8 * tc_block_bytes(e->d) : 16));
     if (notion == RRS_HALFSPACE) {
         CK(e->counts.ensure(Qb * p.mpad * 2 * 4));
         CK(e->depths.ensure(8));
@@ -263,6 +263,7 @@ int contract_halfspace(rrs_engine* e, const Plan& p, int Qb) {
         t.m = p.m;
         t.mpad = p.mpad;
         CK(launch_contract_tc(t, e->sms, e->stream));
+        e->stats.tensor_contract_launches++;
     } else {
         ContractArgs c = contract_args(e, p, Qb, 0, p.MB);
         CK(launch_contract_count(c, e->stream));

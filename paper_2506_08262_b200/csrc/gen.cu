@@ -147,17 +147,23 @@ __device__ double pw_rec(const double* a, int n) {
 __device__ __forceinline__ double pw_sum(const double* a, int n) { return 0.0 + pw_rec(a, n); }
 
 // Tensor-path direction operand (contract_tc.cu): u * 2^15 = hi + lo, both
-// FP16 (hi = fp16(u 2^15), lo = fp16(u 2^15 - hi), |u| <= 1), stored in the
-// canonical K-major no-swizzle layout of a 128-direction block (MMA A operand):
-//   [split 2][k chunk 8][direction 128][8 fp16]   (32 KB per block)
+// FP16 (hi = fp16(u 2^15), lo = fp16(u 2^15 - hi), |u| <= 1), placed at the
+// three K positions of the packed split-product layout (kernels.h, tc_layout):
+// hi for products 0 and 1, lo for product 2.
 // oprow points at (block, direction) = block base + (j & 127) * 16.
-__device__ __forceinline__ void put_tc_operand(unsigned char* oprow, int c, double u) {
+__device__ __forceinline__ void tc_split(double u, __half& h, __half& l) {
     const double v = u * 32768.0;
-    const __half h = __double2half(v);
-    const __half l = __double2half(v - (double)__half2float(h));
-    unsigned char* p = oprow + (c >> 3) * 2048 + (c & 7) * 2;
-    *reinterpret_cast<__half*>(p) = h;
-    *reinterpret_cast<__half*>(p + 16384) = l;
+    h = __double2half(v);
+    l = __double2half(v - (double)__half2float(h));
+}
+__device__ __forceinline__ void put_tc_operand(unsigned char* oprow, const TcLayout& L, int c, double u) {
+    __half h, l;
+    tc_split(u, h, l);
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+        const int kk = tc_pos(L, p, c);
+        *reinterpret_cast<__half*>(oprow + (kk >> 3) * 2048 + (kk & 7) * 2) = (p == 2) ? l : h;
+    }
 }
 
 // ------------------------------------------------------- cap generation K1 --
@@ -177,12 +183,13 @@ __device__ void gen_direction_warp(const GenArgs& a, int64_t gdir, double* g, do
     float* u32 = a.u32 ? a.u32 + (size_t)q * a.mpad * d + (size_t)(j / BN) * d * BN + (j % BN) : nullptr;
     unsigned char* op = nullptr;
     if (a.uop && j < a.NB * 128)
-        op = a.uop + ((size_t)q * a.NB + (j >> 7)) * TC_DIR_BLOCK_BYTES + (size_t)(j & 127) * 16;
+        op = a.uop + ((size_t)q * a.NB + (j >> 7)) * tc_block_bytes(d) + (size_t)(j & 127) * 16;
     if (j >= a.m) {
         if (u32)
             for (int c = lane; c < d; c += 32) u32[(size_t)c * BN] = 0.0f;
         if (op)
-            for (int c = lane; c < 64; c += 32) put_tc_operand(op, c, 0.0);
+            for (int kk = lane; kk < 16 * tc_layout(d).ns; kk += 32)
+                *reinterpret_cast<__half*>(op + (kk >> 3) * 2048 + (kk & 7) * 2) = __double2half(0.0);
         return;
     }
     const uint32_t qg = (uint32_t)((uint64_t)(a.q0 + q) & 0xFFFFFFFFu);
@@ -194,8 +201,15 @@ __device__ void gen_direction_warp(const GenArgs& a, int64_t gdir, double* g, do
             u64[0] = pole[0];
             if (u32) u32[0] = (float)pole[0];
         }
-        if (op)
-            for (int c = lane; c < 64; c += 32) put_tc_operand(op, c, c == 0 ? pole[0] : 0.0);
+        if (op) {
+            const TcLayout L = tc_layout(d);
+            for (int kk = lane; kk < 16 * L.ns; kk += 32) {
+                int p, c;
+                tc_elem(L, kk, p, c);
+                if (c < 0) *reinterpret_cast<__half*>(op + (kk >> 3) * 2048 + (kk & 7) * 2) = __double2half(0.0);
+            }
+            if (lane == 0) put_tc_operand(op, L, 0, pole[0]);
+        }
         return;
     }
     const int dm = d - 1;
@@ -244,8 +258,15 @@ __device__ void gen_direction_warp(const GenArgs& a, int64_t gdir, double* g, do
         u64[c] = val;
         if (u32) u32[(size_t)c * BN] = (float)val;
     }
-    if (op)
-        for (int c = lane; c < 64; c += 32) put_tc_operand(op, c, c < d ? sc[c] : 0.0);
+    if (op) {
+        const TcLayout L = tc_layout(d);
+        for (int kk = lane; kk < 16 * L.ns; kk += 32) {  // zero padding positions
+            int p, c;
+            tc_elem(L, kk, p, c);
+            if (c < 0) *reinterpret_cast<__half*>(op + (kk >> 3) * 2048 + (kk & 7) * 2) = __double2half(0.0);
+        }
+        for (int c = lane; c < d; c += 32) put_tc_operand(op, L, c, sc[c]);
+    }
 }
 
 __global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
@@ -414,25 +435,42 @@ __global__ void __launch_bounds__(GV_THREADS) cap_generate_v2_kernel(GenArgs a) 
         }
     }
     if (a.uop) {
-        const int jj = tid & (GV_DIRS - 1), cc = tid >> 5;  // 32 directions x 8 k chunks
-        unsigned char* base = a.uop + ((size_t)q * a.NB + (j0 >> 7)) * TC_DIR_BLOCK_BYTES + cc * 2048 +
-                              (size_t)((j0 & 127) + jj) * 16;
-        uint32_t hw[4], lw[4];
+        // packed split-product layout, one 16-byte chunk (8 K positions) per task
+        const TcLayout L = tc_layout(d);
+        const int nchunk = 2 * L.ns;
+        unsigned char* base = a.uop + ((size_t)q * a.NB + (j0 >> 7)) * tc_block_bytes(d) + (size_t)(j0 & 127) * 16;
+        for (int t = tid; t < GV_DIRS * nchunk; t += GV_THREADS) {
+            const int jj = t & (GV_DIRS - 1), cc = t >> 5;
+            uint32_t w[4] = {0u, 0u, 0u, 0u};
+            if (jj < nval) {
+                const double* row = val + jj * d;
+                if (8 * cc < 48 * L.q16) {
+                    // aligned part: one product p of 8 consecutive coordinates c0 .. c0 + 7
+                    const int st = cc >> 1, p = st / L.q16;
+                    const int c0 = 16 * (st - p * L.q16) + 8 * (cc & 1);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            __half h2[2], l2[2];
+                    for (int e = 0; e < 4; ++e) {
+                        __half h0, l0, h1, l1;
+                        tc_split(row[c0 + 2 * e], h0, l0);
+                        tc_split(row[c0 + 2 * e + 1], h1, l1);
+                        w[e] = (uint32_t)__half_as_ushort(p == 2 ? l0 : h0) |
+                               ((uint32_t)__half_as_ushort(p == 2 ? l1 : h1) << 16);
+                    }
+                } else {
 #pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const int c = cc * 8 + 2 * e + t;
-                const double w = (jj < nval && c < d) ? val[jj * d + c] * 32768.0 : 0.0;
-                h2[t] = __double2half(w);
-                l2[t] = __double2half(w - (double)__half2float(h2[t]));
+                    for (int e = 0; e < 8; ++e) {
+                        int p, c;
+                        tc_elem(L, cc * 8 + e, p, c);
+                        if (c >= 0) {
+                            __half h, l;
+                            tc_split(row[c], h, l);
+                            w[e >> 1] |= (uint32_t)__half_as_ushort(p == 2 ? l : h) << (16 * (e & 1));
+                        }
+                    }
+                }
             }
-            hw[e] = (uint32_t)__half_as_ushort(h2[0]) | ((uint32_t)__half_as_ushort(h2[1]) << 16);
-            lw[e] = (uint32_t)__half_as_ushort(l2[0]) | ((uint32_t)__half_as_ushort(l2[1]) << 16);
+            *reinterpret_cast<uint4*>(base + (size_t)cc * 2048 + jj * 16) = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        *reinterpret_cast<uint4*>(base) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(base + 16384) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
     if (s_zero) {
         // unreachable for 53-bit uniforms: regenerate zero-norm directions on the warp
@@ -460,20 +498,27 @@ __global__ void pack_directions_kernel(const double* __restrict__ u64, float* __
 
 __global__ void pack_tc_operand_kernel(const double* __restrict__ u64, unsigned char* __restrict__ uop, int Qb,
                                        int m, int NB, int d) {
+    // one K position of one direction per thread
+    const TcLayout L = tc_layout(d);
+    const int K = 16 * L.ns;
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t total = (int64_t)Qb * NB * 128 * 64;
+    int64_t total = (int64_t)Qb * NB * 128 * K;
     if (idx >= total) return;
-    int c = (int)(idx & 63);
-    int64_t r = idx >> 6;
+    int kk = (int)(idx % K);
+    int64_t r = idx / K;
     int j = (int)(r % (NB * 128));
     int q = (int)(r / (NB * 128));
-    double u = (j < m && c < d) ? u64[((size_t)q * m + j) * d + c] : 0.0;
-    put_tc_operand(uop + ((size_t)q * NB + (j >> 7)) * TC_DIR_BLOCK_BYTES + (size_t)(j & 127) * 16, c, u);
+    int p, c;
+    tc_elem(L, kk, p, c);
+    __half h = __double2half(0.0), l = h;
+    if (c >= 0 && j < m) tc_split(u64[((size_t)q * m + j) * d + c], h, l);
+    *reinterpret_cast<__half*>(uop + ((size_t)q * NB + (j >> 7)) * tc_block_bytes(d) + (size_t)(kk >> 3) * 2048 +
+                               (size_t)(j & 127) * 16 + (kk & 7) * 2) = (p == 2) ? l : h;
 }
 
 cudaError_t launch_pack_tc_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,
                                    cudaStream_t st) {
-    int64_t total = (int64_t)Qb * NB * 128 * 64;
+    int64_t total = (int64_t)Qb * NB * 128 * 16 * tc_layout(d).ns;
     pack_tc_operand_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(u64, uop, Qb, m, NB, d);
     return cudaGetLastError();
 }

@@ -12,7 +12,7 @@ struct GenArgs {
     const double* refl_v;    // [Qb][d]
     double* u64;             // [Qb][m][d]
     float* u32;              // [Qb][mpad/BN][d][BN]
-    unsigned char* uop;      // nullable: [Qb][NB][TC_DIR_BLOCK_BYTES] FP16 hi/lo operand (tensor path)
+    unsigned char* uop;      // nullable: [Qb][NB][tc_block_bytes(d)] packed FP16 split operand (tensor path)
     int NB;                  // 128-direction blocks per query in uop
     uint64_t seed;
     int64_t q0;              // global query index of batch row 0
@@ -75,17 +75,60 @@ struct ContractArgs {
 };
 
 // Tensor-core (FP16 hi/lo split) halfspace contraction, contract_tc.cu.
-constexpr int TC_DIR_BLOCK_BYTES = 32768;  // [2 splits][8 k chunks][128 directions][8 fp16]
+// Packed K layout of the split products, shared by the direction operand (A,
+// written by gen.cu) and the point operand (B, written by the kernel):
+//   d = 16 Q + r.  K steps s < 3Q (16 elements each): product p = s / Q of the
+//   coordinates 16 (s % Q) .. +15;  K steps 3Q .. 3Q + R - 1, R = ceil(3r/16):
+//   element e = kk - 48 Q < 3 r is product e / r of coordinate 16 Q + e % r,
+//   the rest zero.  Products: p = 0 hi*hi, 1 hi*lo, 2 lo*hi (A value: lo for
+//   p = 2 else hi; B value: lo for p = 1 else hi), so
+//   sum_kk A[kk] B[kk] = sum_c (uh bh + uh bl + ul bh)  over ns = 3Q + R steps
+//   (d = 50: 10 MMAs instead of 3 x ceil(50/16) = 12).
+// Storage: canonical K-major, no swizzle: [kk / 8][row 128][8 fp16] per
+// 128-row block, i.e. ns * 4096 bytes per block.
+struct TcLayout {
+    int q16, rem, ns;
+};
+__host__ __device__ inline TcLayout tc_layout(int d) {
+    TcLayout L;
+    L.q16 = d / 16;
+    L.rem = d % 16;
+    L.ns = 3 * L.q16 + (3 * L.rem + 15) / 16;
+    return L;
+}
+__host__ __device__ inline int tc_block_bytes(int d) { return tc_layout(d).ns * 4096; }
+// K position of product p of coordinate c
+__host__ __device__ inline int tc_pos(const TcLayout& L, int p, int c) {
+    return c < 16 * L.q16 ? 16 * (p * L.q16 + c / 16) + c % 16 : 48 * L.q16 + p * L.rem + (c - 16 * L.q16);
+}
+// inverse: product p and coordinate c of K position kk (c = -1: zero padding)
+__host__ __device__ inline void tc_elem(const TcLayout& L, int kk, int& p, int& c) {
+    if (kk < 48 * L.q16) {
+        const int s = kk / 16;
+        p = s / L.q16;
+        c = 16 * (s % L.q16) + kk % 16;
+    } else {
+        const int e = kk - 48 * L.q16;
+        if (L.rem == 0 || e >= 3 * L.rem) {
+            p = 0;
+            c = -1;
+        } else {
+            p = e / L.rem;
+            c = 16 * L.q16 + e % L.rem;
+        }
+    }
+}
+
 struct TcArgs {
     const float* xb;            // [T][d][128]
     const float* zq;            // [Qb][d]
-    const unsigned char* uop;   // [Qb][NB][TC_DIR_BLOCK_BYTES] direction operand
+    const unsigned char* uop;   // [Qb][NB][tc_block_bytes(d)] direction operand
     int* counts;                // [Qb][mpad][2]
     int64_t n;
     int64_t tiles;
     int d, Qb, NB, m, mpad;
     // filled by launch_contract_tc
-    int groups, chunks, raw_stages;
+    int groups, chunks, raw_stages, gb;
     int64_t tiles_per_chunk;
 };
 
