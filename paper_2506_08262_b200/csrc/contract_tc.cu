@@ -610,22 +610,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                 // conflict-free, immediate offsets; chunks past d are skipped (warp-uniform)
                 const float* X = sRaw + (size_t)rs * TC_MAXD * TC_NP + 32 * h * TC_NP + r;
                 const float* zh = zs + 32 * h;
-                float av[32];
+                float2 av[16];  // coordinate pairs, packed FP32x2 arithmetic (FADD2 / FMUL2)
                 float mx = 0.0f;
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     if (8 * (4 * h + c) < d) {
                         const float4 z0 = *reinterpret_cast<const float4*>(zh + 8 * c);
                         const float4 z1 = *reinterpret_cast<const float4*>(zh + 8 * c + 4);
-                        const float zz[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
+                        const float2 nz[4] = {make_float2(-z0.x, -z0.y), make_float2(-z0.z, -z0.w),
+                                              make_float2(-z1.x, -z1.y), make_float2(-z1.z, -z1.w)};
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            av[8 * c + e] = X[(8 * c + e) * TC_NP] - zz[e];
-                            mx = fmaxf(mx, fabsf(av[8 * c + e]));
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 xv = make_float2(X[(8 * c + 2 * e) * TC_NP], X[(8 * c + 2 * e + 1) * TC_NP]);
+                            const float2 v = __fadd2_rn(xv, nz[e]);
+                            av[4 * c + e] = v;
+                            mx = fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y)));
                         }
                     } else {
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) av[8 * c + e] = 0.0f;
+                        for (int e = 0; e < 4; ++e) av[4 * c + e] = make_float2(0.0f, 0.0f);
                     }
                 }
                 __syncwarp();
@@ -661,13 +664,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                     const int cc = 4 * h + c;  // coordinate chunk
                     if (8 * cc >= d) continue;
                     uint32_t hw[4], lw[4];
+                    const float2 sc2 = make_float2(scale, scale);
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const float v0 = av[c * 8 + 2 * e] * scale, v1 = av[c * 8 + 2 * e + 1] * scale;
-                        const __half2 hh = __floats2half2_rn(v0, v1);
+                        const float2 v = __fmul2_rn(av[4 * c + e], sc2);
+                        const __half2 hh = __floats2half2_rn(v.x, v.y);
                         const float2 hf = __half22float2(hh);
+                        const float2 res = __fadd2_rn(v, make_float2(-hf.x, -hf.y));
                         hw[e] = *reinterpret_cast<const uint32_t*>(&hh);
-                        lw[e] = pack_half2(v0 - hf.x, v1 - hf.y);
+                        lw[e] = pack_half2(res.x, res.y);
                     }
                     if (cc < main_chunks) {
                         // aligned part: products 0 (hi), 1 (lo), 2 (hi) of coordinates 8 cc .. 8 cc + 7

@@ -326,7 +326,7 @@ __device__ __forceinline__ double pw_sum8(int n, int k, F f) {
     return 0.0 + res;
 }
 
-__global__ void __launch_bounds__(GV_THREADS) cap_generate_v2_kernel(GenArgs a) {
+__global__ void __launch_bounds__(GV_THREADS, 3) cap_generate_v2_kernel(GenArgs a) {
     extern __shared__ double vsm[];
     const int d = a.d, dm = d - 1;
     double* val = vsm;                          // [GV_DIRS][d] uniforms -> normals -> row
