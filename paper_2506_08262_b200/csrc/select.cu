@@ -227,8 +227,249 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SelectArgs a)
     if (threadIdx.x == 0) a.depths[(size_t)q * a.m + j] = depth;
 }
 
+// ---------------------------------------------------------------- K3 v2 --
+// Rows up to SEL2_MAX_N (config 3: n = 50k) live in shared memory as
+// order-preserving uint32 keys; one CTA (256 threads) per direction.
+//   * k-th smallest key: radix select on 8-bit digits starting below the
+//     common prefix of the row's min and max keys (digits every key shares are
+//     skipped), per-warp privatised 256-bin histograms, one 256-bin scan per
+//     pass (one bin per thread);
+//   * even counts take the midpoint with the next larger key (one min pass);
+//   * the MAD / positive-deviation keys are rewritten in place once (FP64
+//     deviation, FP32 key) instead of being recomputed every pass.
+// Same arithmetic as select_kernel: FP32 order statistics, FP64 midpoints and
+// deviations (_kernels.pyx:202-351).
+constexpr int SEL2_THREADS = 256;
+constexpr int SEL2_WARPS = SEL2_THREADS / 32;
+constexpr int64_t SEL2_MAX_N = 53248;  // 208 KB of keys
+
+struct Sel2Shared {
+    uint32_t hist[SEL2_WARPS][256];
+    uint32_t wsum[SEL2_WARPS];
+    uint32_t s_kmin, s_kmax;
+    int s_bin;
+    uint32_t s_below;
+    uint32_t s_cnt;
+};
+
+__device__ __forceinline__ uint32_t block_reduce_min(uint32_t v, Sel2Shared& sh) {
+    v = __reduce_min_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0) sh.wsum[threadIdx.x >> 5] = v;
+    __syncthreads();
+    uint32_t r = 0xFFFFFFFFu;
+    for (int w = 0; w < SEL2_WARPS; ++w) r = min(r, sh.wsum[w]);
+    __syncthreads();
+    return r;
+}
+__device__ __forceinline__ uint32_t block_reduce_add(uint32_t v, Sel2Shared& sh) {
+    v = __reduce_add_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0) sh.wsum[threadIdx.x >> 5] = v;
+    __syncthreads();
+    uint32_t r = 0;
+    for (int w = 0; w < SEL2_WARPS; ++w) r += sh.wsum[w];
+    __syncthreads();
+    return r;
+}
+
+// k-th smallest (0-based) of keys[0, n) whose values lie in [kmin, kmax];
+// c_le = number of keys <= the result.  (Compacting the surviving candidates
+// after a pass was measured slower: the scratch costs occupancy.)
+__device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t k, uint32_t kmin, uint32_t kmax,
+                             Sel2Shared& sh, uint32_t& c_le) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t* src = keys;
+    const uint32_t diff = kmin ^ kmax;
+    if (diff == 0u) {
+        c_le = (uint32_t)n;
+        return kmin;
+    }
+    const int top = 31 - __clz(diff);            // highest differing bit
+    int shift = (top >= 24) ? 24 : (top >= 16) ? 16 : (top >= 8) ? 8 : 0;
+    uint32_t pmask = shift + 8 >= 32 ? 0u : ~((1u << (shift + 8)) - 1u);
+    uint32_t prefix = kmin & pmask;                // digits above `shift` are common
+    uint32_t below_total = 0, last = 0;
+    for (;;) {
+        uint32_t* h = sh.hist[warp];
+        for (int b = lane; b < 256; b += 32) h[b] = 0u;
+        __syncthreads();
+        // 4 keys per 16-byte load; the row is 16-byte aligned, the tail is scalar
+        const int n4 = n >> 2;
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        for (int i = tid; i < n4; i += SEL2_THREADS) {
+            const uint4 k4 = s4[i];
+            if ((k4.x & pmask) == prefix) atomicAdd(&h[(k4.x >> shift) & 255u], 1u);
+            if ((k4.y & pmask) == prefix) atomicAdd(&h[(k4.y >> shift) & 255u], 1u);
+            if ((k4.z & pmask) == prefix) atomicAdd(&h[(k4.z >> shift) & 255u], 1u);
+            if ((k4.w & pmask) == prefix) atomicAdd(&h[(k4.w >> shift) & 255u], 1u);
+        }
+        for (int i = 4 * n4 + tid; i < n; i += SEL2_THREADS) {
+            const uint32_t key = src[i];
+            if ((key & pmask) == prefix) atomicAdd(&h[(key >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        // bin totals (thread b owns bin b), exclusive scan over the 256 bins
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < SEL2_WARPS; ++w) tot += sh.hist[w][tid];
+        uint32_t incl = tot;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += o;
+        }
+        if (lane == 31) sh.wsum[warp] = incl;
+        __syncthreads();
+        uint32_t woff = 0;
+        for (int w = 0; w < warp; ++w) woff += sh.wsum[w];
+        const uint32_t excl = woff + incl - tot;
+        if (excl <= k && k < excl + tot) {
+            sh.s_bin = tid;
+            sh.s_below = excl;
+            sh.s_cnt = tot;
+        }
+        __syncthreads();
+        const uint32_t bin = (uint32_t)sh.s_bin;
+        k -= sh.s_below;
+        below_total += sh.s_below;
+        last = sh.s_cnt;
+        prefix |= bin << shift;
+        pmask |= 255u << shift;
+        __syncthreads();
+        if (shift == 0) break;
+        shift -= 8;
+    }
+    c_le = below_total + last;
+    return prefix;
+}
+
+__device__ uint32_t sel2_min_greater(const uint32_t* __restrict__ keys, int n, uint32_t key, Sel2Shared& sh) {
+    // min over keys > key: map keys <= key to 0xFFFFFFFF (key + 1 .. wraps only for key = max)
+    uint32_t best = 0xFFFFFFFFu;
+    const int n4 = n >> 2;
+    const uint4* s4 = reinterpret_cast<const uint4*>(keys);
+    for (int i = threadIdx.x; i < n4; i += SEL2_THREADS) {
+        const uint4 k4 = s4[i];
+        best = min(best, k4.x > key ? k4.x : 0xFFFFFFFFu);
+        best = min(best, k4.y > key ? k4.y : 0xFFFFFFFFu);
+        best = min(best, k4.z > key ? k4.z : 0xFFFFFFFFu);
+        best = min(best, k4.w > key ? k4.w : 0xFFFFFFFFu);
+    }
+    for (int i = 4 * n4 + threadIdx.x; i < n; i += SEL2_THREADS) {
+        const uint32_t k2 = keys[i];
+        if (k2 > key && k2 < best) best = k2;
+    }
+    return block_reduce_min(best, sh);
+}
+
+// median of the first `cnt` order statistics' centre: keys outside the
+// participating set must be larger than every participant (0xFFFFFFFF)
+__device__ double sel2_median(const uint32_t* __restrict__ keys, int n, uint32_t cnt, uint32_t kmin, uint32_t kmax,
+                              Sel2Shared& sh) {
+    const uint32_t k = (cnt - 1) >> 1;
+    uint32_t c_le;
+    const uint32_t lo = sel2_kth(keys, n, k, kmin, kmax, sh, c_le);
+    const double lov = (double)kfloat(lo);
+    if (cnt & 1) return lov;
+    uint32_t hi = lo;
+    if (c_le < k + 2) hi = sel2_min_greater(keys, n, lo, sh);
+    return (lov + (double)kfloat(hi)) / 2.0;
+}
+
+__global__ void __launch_bounds__(SEL2_THREADS) select_v2_kernel(const SelectArgs a) {
+    extern __shared__ __align__(16) unsigned char sel2_raw[];
+    Sel2Shared& sh = *reinterpret_cast<Sel2Shared*>(sel2_raw);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(sel2_raw + ((sizeof(Sel2Shared) + 15) & ~size_t(15)));
+    const int jj = blockIdx.x;
+    const int q = blockIdx.y;
+    const int j = a.j0 + jj;
+    if (j >= a.m) return;
+    const int n = (int)a.n;
+    const float* yrow = a.y + ((size_t)q * a.jcount + jj) * a.n;
+    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+    if ((n & 3) == 0) {
+        const float4* s4 = reinterpret_cast<const float4*>(yrow);
+        uint4* k4 = reinterpret_cast<uint4*>(keys);
+        for (int i = threadIdx.x; i < n / 4; i += SEL2_THREADS) {
+            const float4 v = __ldg(s4 + i);
+            const uint4 k = make_uint4(fkey(v.x), fkey(v.y), fkey(v.z), fkey(v.w));
+            k4[i] = k;
+            kmin = min(kmin, min(min(k.x, k.y), min(k.z, k.w)));
+            kmax = max(kmax, max(max(k.x, k.y), max(k.z, k.w)));
+        }
+    } else {
+        for (int i = threadIdx.x; i < n; i += SEL2_THREADS) {
+            const uint32_t k = fkey(__ldg(yrow + i));
+            keys[i] = k;
+            kmin = min(kmin, k);
+            kmax = max(kmax, k);
+        }
+    }
+    __syncthreads();
+    kmin = block_reduce_min(kmin, sh);
+    kmax = ~block_reduce_min(~kmax, sh);
+    const double med = sel2_median(keys, n, (uint32_t)n, kmin, kmax, sh);
+    double depth;
+    if (a.notion == 1) {
+        // MAD: keys of |y - med| (FP64 deviation, FP32 key), in place
+        uint32_t dmin = 0xFFFFFFFFu, dmax = 0u;
+        for (int i = threadIdx.x; i < n; i += SEL2_THREADS) {
+            const uint32_t k = fkey((float)fabs((double)kfloat(keys[i]) - med));
+            keys[i] = k;
+            dmin = min(dmin, k);
+            dmax = max(dmax, k);
+        }
+        __syncthreads();
+        dmin = block_reduce_min(dmin, sh);
+        dmax = ~block_reduce_min(~dmax, sh);
+        const double mad = sel2_median(keys, n, (uint32_t)n, dmin, dmax, sh);
+        const double dev = fabs(med);
+        if (mad == 0.0) depth = (dev == 0.0) ? 1.0 : 0.0;
+        else depth = 1.0 / (1.0 + dev / mad);
+    } else {
+        const double dev = -med;
+        if (dev <= 0.0) {
+            depth = 1.0;
+        } else {
+            // positive deviations y - med > 0 keep their key, the rest sort last
+            uint32_t dmin = 0xFFFFFFFFu, dmax = 0u, npos = 0;
+            for (int i = threadIdx.x; i < n; i += SEL2_THREADS) {
+                const double t = (double)kfloat(keys[i]) - med;
+                uint32_t k = 0xFFFFFFFFu;
+                if (t > 0.0) {
+                    k = fkey((float)t);
+                    ++npos;
+                    dmin = min(dmin, k);
+                    dmax = max(dmax, k);
+                }
+                keys[i] = k;
+            }
+            __syncthreads();
+            npos = block_reduce_add(npos, sh);
+            dmin = block_reduce_min(dmin, sh);
+            dmax = ~block_reduce_min(~dmax, sh);
+            if (npos == 0) depth = 0.0;
+            else {
+                // participants are the npos smallest keys; select within [dmin, dmax]
+                // (the 0xFFFFFFFF markers never match the prefix of a participant)
+                const double madp = sel2_median(keys, n, npos, dmin, dmax, sh);
+                depth = 1.0 / (1.0 + dev / madp);
+            }
+        }
+    }
+    if (threadIdx.x == 0) a.depths[(size_t)q * a.m + j] = depth;
+}
+
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
     if (a.Qb == 0 || a.jcount == 0) return cudaSuccess;
+    if (a.n <= SEL2_MAX_N) {
+        const size_t smem = ((sizeof(Sel2Shared) + 15) & ~size_t(15)) + (size_t)a.n * 4;
+        cudaError_t e = cudaFuncSetAttribute(select_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        dim3 grid((unsigned)a.jcount, (unsigned)a.Qb);
+        select_v2_kernel<<<grid, SEL2_THREADS, smem, st>>>(a);
+        return cudaGetLastError();
+    }
     size_t smem = (sizeof(SelShared) + 15) & ~size_t(15);
     if (a.n <= SEL_CACHE_MAX) smem += (size_t)a.n * sizeof(float);
     cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
