@@ -299,3 +299,24 @@ def test_tier1_config4_scale_counts(b200, path, dist):
         slack += int(np.count_nonzero((cle != rle) | (cge != rge)))
         zone_total += int(T.sum())
     print(f"config-4 shape {dist}/{path}: tie-zone elements {zone_total}, directions using slack {slack} / 4000")
+
+
+@pytest.mark.parametrize("d", [1, 3, 16, 22, 27, 44, 50, 64])
+def test_tensor_layout_dims(b200, d):
+    """The packed split-product K layout (kernels.h tc_layout) for every shape of
+    remainder: d % 16 = 0 (no tail step), 3 (one), 6 (two), 11/12 (three tail
+    steps), d < 16 (tail only) -- tensor-path counts against FP64 within the
+    tie zone, n not a multiple of the 128-point tile, m not a multiple of 128."""
+    rng = np.random.default_rng(100 + d)
+    X = rng.standard_normal((4096 + 203, d)) * rng.uniform(0.1, 10.0, size=d)
+    U = rng.standard_normal((333, d))
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    data = b200.Dataset(X)
+    xn = np.linalg.norm(X, axis=1)
+    for z in (X[17], 0.5 * X[3] + 0.5 * X[4], np.full(d, 0.1)):
+        with contract_path(b200, "tensor"):
+            _, cle, cge = b200.evaluate_directions_counts(z, data, U)
+        y = X @ U.T - (U @ z)[None, :]
+        T = (np.abs(y) < TIE_REL * np.maximum(xn, np.linalg.norm(z))[:, None]).sum(axis=0)
+        rle, rge = (y <= 0).sum(axis=0), (y >= 0).sum(axis=0)
+        assert np.all(np.abs(cle - rle) <= T) and np.all(np.abs(cge - rge) <= T), d
