@@ -204,6 +204,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="queries per GPU per step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "tensor2"],
+                    help="halfspace contraction kernel (auto: the library's choice)")
     args = ap.parse_args()
     wl = args.workload
     if args.impl == "reference":
@@ -228,6 +230,7 @@ def main():
     cfg = rrs.RrsConfig(total_directions=k, refinements=r, shrink=alpha, notion=notion, seed=1)
     X = make_data(distn, n, d)
     eng = rrs.engine(local)
+    eng.set_contract_path(args.contract_path)
     stream = torch.cuda.Stream()  # one non-default stream shared by torch and the engine
     torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)

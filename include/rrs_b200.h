@@ -108,7 +108,8 @@ int rrs_philox4x32_host(rrs_engine* e, const uint32_t* ctr, int64_t N, uint32_t 
 
 /* Halfspace contraction kernel: 0 = auto (tensor cores when d <= 64 and
  * n >= 4096), 1 = FP32 FFMA (contract.cu), 2 = tcgen05 FP16 hi/lo split with
- * FP32 accumulation (contract_tc.cu; halfspace, d <= 64). */
+ * FP32 accumulation (contract_tc.cu; halfspace, d <= 64), 3 = the same on SM
+ * pairs with cta_group::2 MMAs (contract_tc2.cu). */
 int rrs_engine_set_contract_path(rrs_engine* e, int32_t path);
 
 /* Diagnostics for the last batch: device time (ms) of each stage summed over

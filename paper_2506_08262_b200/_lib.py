@@ -173,8 +173,9 @@ class Engine:
         _raise(load_library().rrs_engine_set_workspace_limit(self._h, int(nbytes)))
 
     def set_contract_path(self, path: str):
-        """'auto' | 'ffma' | 'tensor' (halfspace contraction kernel)."""
-        code = {"auto": 0, "ffma": 1, "tensor": 2}[path]
+        """'auto' | 'ffma' | 'tensor' | 'tensor2' (halfspace contraction kernel;
+        tensor2 = the 2-SM cta_group::2 variant)."""
+        code = {"auto": 0, "ffma": 1, "tensor": 2, "tensor2": 3}[path]
         _raise(load_library().rrs_engine_set_contract_path(self._h, code))
 
     def enable_timing(self, on: bool = True):

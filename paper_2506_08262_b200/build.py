@@ -24,6 +24,7 @@ SOURCES = {  # file -> extra flags
     "gen.cu": ["-fmad=false"],
     "contract.cu": [],
     "contract_tc.cu": [],
+    "contract_tc2.cu": [],
     "select.cu": [],
     "engine.cu": [],
 }

@@ -485,7 +485,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     float* sZ = reinterpret_cast<float*>(sm + lay.ZS);
     float* sMx = reinterpret_cast<float*>(sm + lay.SMX);
     uint32_t* sExcl = reinterpret_cast<uint32_t*>(sm + lay.EXCL);
-    uint32_t* sZrows = reinterpret_cast<uint32_t*>(sm + lay.ZROWS);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + lay.BARS);
     uint64_t* pfull = &bars[0];                   // [P_STAGES] point tile converted (converter warps)
     uint64_t* pempty = &bars[P_STAGES];           // [P_STAGES] MMAs reading it completed
@@ -510,7 +509,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
         reinterpret_cast<uint4*>(sP)[i] = make_uint4(0u, 0u, 0u, 0u);
     for (int i = tid; i < RS * TC_MAXD * TC_NP; i += TC_THREADS) sRaw[i] = 0.0f;  // rows >= d stay 0
     for (int c = tid; c < TC_GB_MAX * TC_MD; c += TC_THREADS) sCnt[c] = 0u;
-    if (tid < 4) sZrows[tid] = 0u;
     if (tid == 0) {
         for (int s = 0; s < P_STAGES; ++s) {
             mbar_init(&pfull[s], TC_CONV_WARPS);
@@ -601,7 +599,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
             float* zs = sZ + (it & 1u) * TC_MAXD;
             if (ct < TC_MAXD) zs[ct] = ct < d ? __ldg(a.zq + (size_t)w.q * d + ct) : 0.0f;
             named_bar(2, TC_CONV_THREADS);  // zs ready; keeps the converter warps in step per unit
-            uint32_t zcount = 0;
             for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
                 const uint32_t s = gtile % P_STAGES;
                 const bool ok = t * TC_NP + r < a.n;
@@ -645,7 +642,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                     // points the epilogue must not count: coinciding rows (every product a
                     // signed zero, ties on both sides) and rows beyond n (their operand is
                     // finite garbage, x = 0 padding minus z)
-                    zcount += (ok && mx == 0.0f) ? 1u : 0u;
                     const uint32_t ex = __ballot_sync(0xffffffffu, !ok || mx == 0.0f);
                     if (lane == 0) sExcl[(gtile & 7u) * 4 + (r >> 5)] = ex;
                 }
@@ -705,9 +701,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&pfull[s]);
             }
-            // coinciding rows (x - z == 0) of this unit: ties on both sides
-            zcount = __reduce_add_sync(0xffffffffu, zcount);
-            if (lane == 0 && zcount) atomicAdd(&sZrows[it & 3u], zcount);
         }
     } else {
         // ------------------------------------------------------------ epilogue
@@ -721,6 +714,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
             uint32_t cnt[TC_GB_MAX];  // #(y<0) per resident block
 #pragma unroll
             for (int b = 0; b < TC_GB_MAX; ++b) cnt[b] = 0u;
+            uint32_t zsum = 0;  // coinciding rows (x - z == 0) of the unit's tiles
             for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
                 uint32_t keep0 = 0u, keep1 = 0u;
 #pragma unroll
@@ -734,8 +728,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                             // excluded points of this tile (written by the converters before the
                             // tile's pfull; ordered through pfull -> MMA -> tfull), bit j = point
                             // half*64 + 32 i + j
-                            keep0 = ~sExcl[(gtile & 7u) * 4 + 2 * half];
-                            keep1 = ~sExcl[(gtile & 7u) * 4 + 2 * half + 1];
+                            const uint32_t* ex = sExcl + (gtile & 7u) * 4;
+                            keep0 = ~ex[2 * half];
+                            keep1 = ~ex[2 * half + 1];
+                            // excluded = coinciding or past n: coinciding = excluded - padding
+                            const int64_t pad = (t + 1) * TC_NP - a.n;
+                            zsum += (uint32_t)(__popc(ex[0]) + __popc(ex[1]) + __popc(ex[2]) + __popc(ex[3])) -
+                                    (uint32_t)(pad > 0 ? pad : 0);
                         }
                         const uint32_t tb = tmem + lane_base + buf * ACC_COLS + (uint32_t)(half * 64);
                         uint32_t y0[32], y1[32];
@@ -766,7 +765,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
             // zone) lands on the positive side
             const int64_t r1 = w.t1 * TC_NP < a.n ? w.t1 * TC_NP : a.n;
             const int valid = (int)(r1 - w.t0 * TC_NP);
-            const int zrows = (int)sZrows[it & 3u];
+            const int zrows = (int)zsum;
             int* dst = a.counts + (size_t)w.q * a.mpad * 2;
             const int j0 = w.grp * a.gb * TC_MD;
             for (int c = ct; c < w.nbg * TC_MD; c += TC_EPI_THREADS) {
@@ -778,7 +777,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                 if (gtv) atomicAdd(dst + 2 * (j0 + c) + 1, gtv);
             }
             named_bar(1, TC_EPI_THREADS);
-            if (ct == 0) sZrows[it & 3u] = 0u;
         }
     }
 

@@ -88,7 +88,7 @@ struct rrs_engine {
     int64_t tiles = 0;
     // workspace
     DevBuf zq, u64, u32, uop, counts, depths, y, pole, reflv, reflmode, dmin, bestcnt;
-    int contract_path = 0;  // 0 auto, 1 FFMA (contract.cu), 2 tensor cores (contract_tc.cu)
+    int contract_path = 0;  // 0 auto, 1 FFMA (contract.cu), 2 tensor cores (contract_tc.cu), 3 2-SM (contract_tc2.cu)
     DevBuf tmp_in, tmp_out0, tmp_out1, tmp_out2, tmp_out3;
     // timing
     bool timing = false;
@@ -166,7 +166,7 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     p.mpad = p.MB * BN;
     p.nb8 = p.MB;
     const bool tc_ok = notion == RRS_HALFSPACE && e->d <= 64;
-    p.tc = tc_ok && (e->contract_path == 2 || (e->contract_path == 0 && e->n >= 4096));
+    p.tc = tc_ok && (e->contract_path >= 2 || (e->contract_path == 0 && e->n >= 4096));
     const int64_t d = e->d, n = e->n;
     int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * d * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 8 +
                     d * 40 + 64 + (int64_t)p.nb8 * tc_block_bytes(e->d);
@@ -262,7 +262,10 @@ int contract_halfspace(rrs_engine* e, const Plan& p, int Qb) {
         t.NB = p.nb8;
         t.m = p.m;
         t.mpad = p.mpad;
-        CK(launch_contract_tc(t, e->sms, e->stream));
+        if (e->contract_path == 3)
+            CK(launch_contract_tc2(t, e->sms, e->stream));
+        else
+            CK(launch_contract_tc(t, e->sms, e->stream));
         e->stats.tensor_contract_launches++;
     } else {
         ContractArgs c = contract_args(e, p, Qb, 0, p.MB);
@@ -500,7 +503,8 @@ int rrs_engine_set_workspace_limit(rrs_engine* e, int64_t bytes) {
 
 int rrs_engine_set_contract_path(rrs_engine* e, int32_t path) {
     if (!e) return fail(RRS_ERR_INVALID, "engine is null");
-    if (path < 0 || path > 2) return fail(RRS_ERR_INVALID, "contract path must be 0 (auto), 1 (FFMA) or 2 (tensor)");
+    if (path < 0 || path > 3)
+        return fail(RRS_ERR_INVALID, "contract path must be 0 (auto), 1 (FFMA), 2 (tensor) or 3 (tensor, 2-SM)");
     e->contract_path = path;
     return RRS_OK;
 }

@@ -159,6 +159,7 @@ cudaError_t launch_contract_count(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_contract_store(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
 cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st);
+cudaError_t launch_contract_tc2(TcArgs a, int sms, cudaStream_t st);  // 2-SM (cta_group::2) variant
 cudaError_t launch_pack_tc_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,
                                    cudaStream_t st);
 size_t contract_tc_smem_bytes();
