@@ -51,6 +51,10 @@
 
 #include <cuda_fp16.h>
 
+#ifndef RRS_TC_UNITS_PER_SM
+#define RRS_TC_UNITS_PER_SM 16  // load balance of the persistent grid (units per SM, at least)
+#endif
+
 namespace rrs {
 
 constexpr int TC_CONV_WARP0 = 3;                 // first converter warp
@@ -791,9 +795,9 @@ void plan_contract_tc(TcArgs& a, int sms) {
     if (gb > TC_GB_MAX) gb = TC_GB_MAX;
     a.gb = gb;
     a.groups = (a.NB + gb - 1) / gb;
-    // split the point tiles into chunks so that every SM gets >= ~16 units
+    // split the point tiles into chunks so that every SM gets >= RRS_TC_UNITS_PER_SM units
     const int64_t base = (int64_t)a.Qb * a.groups;
-    int64_t chunks = (16LL * sms + base - 1) / base;
+    int64_t chunks = ((int64_t)RRS_TC_UNITS_PER_SM * sms + base - 1) / base;
     if (chunks < 1) chunks = 1;
     if (chunks > a.tiles) chunks = a.tiles;
     a.tiles_per_chunk = (a.tiles + chunks - 1) / chunks;

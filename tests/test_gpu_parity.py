@@ -320,3 +320,23 @@ def test_tensor_layout_dims(b200, d):
         T = (np.abs(y) < TIE_REL * np.maximum(xn, np.linalg.norm(z))[:, None]).sum(axis=0)
         rle, rge = (y <= 0).sum(axis=0), (y >= 0).sum(axis=0)
         assert np.all(np.abs(cle - rle) <= T) and np.all(np.abs(cge - rge) <= T), d
+
+
+@pytest.mark.parametrize("notion", ["projection", "asym_projection"])
+@pytest.mark.parametrize("n", [53248, 60001])
+def test_tier2_large_rows(b200, notion, n):
+    """Rows at the shared-memory limit of the select kernel and past it (the
+    global-memory select path), Cauchy data, against the FP64 oracle."""
+    from oracle import oracle
+    from paper_2506_08262_b200.synthetic import student_t
+
+    X = student_t(7, n, 1.0, seed=3)
+    rng = np.random.default_rng(4)
+    U = rng.standard_normal((16, 7))
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    data = b200.Dataset(X)
+    cfg = b200.ParallelConfig(workers=1)
+    for z in (X[5], np.median(X, axis=0) + 0.1):
+        got = b200.evaluate_directions(z, data, U, notion, cfg)
+        ref = oracle.evaluate_directions(z, X, U, notion)
+        np.testing.assert_allclose(got, ref, rtol=DEPTH_RTOL, atol=0)
