@@ -239,34 +239,49 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SelectArgs a)
 //     deviation, FP32 key) instead of being recomputed every pass.
 // Same arithmetic as select_kernel: FP32 order statistics, FP64 midpoints and
 // deviations (_kernels.pyx:202-351).
-constexpr int SEL2_THREADS = 256;
-constexpr int SEL2_WARPS = SEL2_THREADS / 32;
 constexpr int64_t SEL2_MAX_N = 53248;  // 208 KB of keys
+// 256 threads for rows up to SEL2_WIDE_N, 512 above (one CTA per SM at n = 50k:
+// more warps in flight for the latency-bound passes)
+constexpr int64_t SEL2_WIDE_N = 16384;
 
+// hist[(key >> shift) & 255] += 1 when (key & pmask) == prefix: a predicated
+// red.shared (no branch / reconvergence per element)
+__device__ __forceinline__ void hist_add_if(uint32_t* h, uint32_t key, uint32_t pmask, uint32_t prefix, int shift) {
+    const uint32_t addr = smem_u32(h + ((key >> shift) & 255u));
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.eq.u32 p, %0, %1;\n@p red.shared.add.u32 [%2], 1;\n}\n" ::"r"(key & pmask),
+        "r"(prefix), "r"(addr)
+        : "memory");
+}
+
+template <int NT>
 struct Sel2Shared {
-    uint32_t hist[SEL2_WARPS][256];
-    uint32_t wsum[SEL2_WARPS];
+    static constexpr int W = NT / 32;
+    uint32_t hist[W][256];
+    uint32_t wsum[W];
     uint32_t s_kmin, s_kmax;
     int s_bin;
     uint32_t s_below;
     uint32_t s_cnt;
 };
 
-__device__ __forceinline__ uint32_t block_reduce_min(uint32_t v, Sel2Shared& sh) {
+template <int NT>
+__device__ __forceinline__ uint32_t block_reduce_min(uint32_t v, Sel2Shared<NT>& sh) {
     v = __reduce_min_sync(0xffffffffu, v);
     if ((threadIdx.x & 31) == 0) sh.wsum[threadIdx.x >> 5] = v;
     __syncthreads();
     uint32_t r = 0xFFFFFFFFu;
-    for (int w = 0; w < SEL2_WARPS; ++w) r = min(r, sh.wsum[w]);
+    for (int w = 0; w < NT / 32; ++w) r = min(r, sh.wsum[w]);
     __syncthreads();
     return r;
 }
-__device__ __forceinline__ uint32_t block_reduce_add(uint32_t v, Sel2Shared& sh) {
+template <int NT>
+__device__ __forceinline__ uint32_t block_reduce_add(uint32_t v, Sel2Shared<NT>& sh) {
     v = __reduce_add_sync(0xffffffffu, v);
     if ((threadIdx.x & 31) == 0) sh.wsum[threadIdx.x >> 5] = v;
     __syncthreads();
     uint32_t r = 0;
-    for (int w = 0; w < SEL2_WARPS; ++w) r += sh.wsum[w];
+    for (int w = 0; w < NT / 32; ++w) r += sh.wsum[w];
     __syncthreads();
     return r;
 }
@@ -274,8 +289,9 @@ __device__ __forceinline__ uint32_t block_reduce_add(uint32_t v, Sel2Shared& sh)
 // k-th smallest (0-based) of keys[0, n) whose values lie in [kmin, kmax];
 // c_le = number of keys <= the result.  (Compacting the surviving candidates
 // after a pass was measured slower: the scratch costs occupancy.)
+template <int NT>
 __device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t k, uint32_t kmin, uint32_t kmax,
-                             Sel2Shared& sh, uint32_t& c_le) {
+                             Sel2Shared<NT>& sh, uint32_t& c_le) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t* src = keys;
     const uint32_t diff = kmin ^ kmax;
@@ -295,37 +311,37 @@ __device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t 
         // 4 keys per 16-byte load; the row is 16-byte aligned, the tail is scalar
         const int n4 = n >> 2;
         const uint4* s4 = reinterpret_cast<const uint4*>(src);
-        for (int i = tid; i < n4; i += SEL2_THREADS) {
+        for (int i = tid; i < n4; i += NT) {
             const uint4 k4 = s4[i];
-            if ((k4.x & pmask) == prefix) atomicAdd(&h[(k4.x >> shift) & 255u], 1u);
-            if ((k4.y & pmask) == prefix) atomicAdd(&h[(k4.y >> shift) & 255u], 1u);
-            if ((k4.z & pmask) == prefix) atomicAdd(&h[(k4.z >> shift) & 255u], 1u);
-            if ((k4.w & pmask) == prefix) atomicAdd(&h[(k4.w >> shift) & 255u], 1u);
+            hist_add_if(h, k4.x, pmask, prefix, shift);
+            hist_add_if(h, k4.y, pmask, prefix, shift);
+            hist_add_if(h, k4.z, pmask, prefix, shift);
+            hist_add_if(h, k4.w, pmask, prefix, shift);
         }
-        for (int i = 4 * n4 + tid; i < n; i += SEL2_THREADS) {
-            const uint32_t key = src[i];
-            if ((key & pmask) == prefix) atomicAdd(&h[(key >> shift) & 255u], 1u);
-        }
+        for (int i = 4 * n4 + tid; i < n; i += NT) hist_add_if(h, src[i], pmask, prefix, shift);
         __syncthreads();
-        // bin totals (thread b owns bin b), exclusive scan over the 256 bins
+        // bin totals (thread b < 256 owns bin b), exclusive scan over the 256 bins
         uint32_t tot = 0;
+        if (tid < 256)
 #pragma unroll
-        for (int w = 0; w < SEL2_WARPS; ++w) tot += sh.hist[w][tid];
+            for (int w = 0; w < NT / 32; ++w) tot += sh.hist[w][tid];
         uint32_t incl = tot;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
             if (lane >= off) incl += o;
         }
-        if (lane == 31) sh.wsum[warp] = incl;
+        if (lane == 31 && warp < 8) sh.wsum[warp] = incl;
         __syncthreads();
-        uint32_t woff = 0;
-        for (int w = 0; w < warp; ++w) woff += sh.wsum[w];
-        const uint32_t excl = woff + incl - tot;
-        if (excl <= k && k < excl + tot) {
-            sh.s_bin = tid;
-            sh.s_below = excl;
-            sh.s_cnt = tot;
+        if (tid < 256) {
+            uint32_t woff = 0;
+            for (int w = 0; w < warp; ++w) woff += sh.wsum[w];
+            const uint32_t excl = woff + incl - tot;
+            if (excl <= k && k < excl + tot) {
+                sh.s_bin = tid;
+                sh.s_below = excl;
+                sh.s_cnt = tot;
+            }
         }
         __syncthreads();
         const uint32_t bin = (uint32_t)sh.s_bin;
@@ -342,19 +358,20 @@ __device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t 
     return prefix;
 }
 
-__device__ uint32_t sel2_min_greater(const uint32_t* __restrict__ keys, int n, uint32_t key, Sel2Shared& sh) {
+template <int NT>
+__device__ uint32_t sel2_min_greater(const uint32_t* __restrict__ keys, int n, uint32_t key, Sel2Shared<NT>& sh) {
     // min over keys > key: map keys <= key to 0xFFFFFFFF (key + 1 .. wraps only for key = max)
     uint32_t best = 0xFFFFFFFFu;
     const int n4 = n >> 2;
     const uint4* s4 = reinterpret_cast<const uint4*>(keys);
-    for (int i = threadIdx.x; i < n4; i += SEL2_THREADS) {
+    for (int i = threadIdx.x; i < n4; i += NT) {
         const uint4 k4 = s4[i];
         best = min(best, k4.x > key ? k4.x : 0xFFFFFFFFu);
         best = min(best, k4.y > key ? k4.y : 0xFFFFFFFFu);
         best = min(best, k4.z > key ? k4.z : 0xFFFFFFFFu);
         best = min(best, k4.w > key ? k4.w : 0xFFFFFFFFu);
     }
-    for (int i = 4 * n4 + threadIdx.x; i < n; i += SEL2_THREADS) {
+    for (int i = 4 * n4 + threadIdx.x; i < n; i += NT) {
         const uint32_t k2 = keys[i];
         if (k2 > key && k2 < best) best = k2;
     }
@@ -363,8 +380,9 @@ __device__ uint32_t sel2_min_greater(const uint32_t* __restrict__ keys, int n, u
 
 // median of the first `cnt` order statistics' centre: keys outside the
 // participating set must be larger than every participant (0xFFFFFFFF)
+template <int NT>
 __device__ double sel2_median(const uint32_t* __restrict__ keys, int n, uint32_t cnt, uint32_t kmin, uint32_t kmax,
-                              Sel2Shared& sh) {
+                              Sel2Shared<NT>& sh) {
     const uint32_t k = (cnt - 1) >> 1;
     uint32_t c_le;
     const uint32_t lo = sel2_kth(keys, n, k, kmin, kmax, sh, c_le);
@@ -375,10 +393,11 @@ __device__ double sel2_median(const uint32_t* __restrict__ keys, int n, uint32_t
     return (lov + (double)kfloat(hi)) / 2.0;
 }
 
-__global__ void __launch_bounds__(SEL2_THREADS) select_v2_kernel(const SelectArgs a) {
+template <int NT>
+__global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
     extern __shared__ __align__(16) unsigned char sel2_raw[];
-    Sel2Shared& sh = *reinterpret_cast<Sel2Shared*>(sel2_raw);
-    uint32_t* keys = reinterpret_cast<uint32_t*>(sel2_raw + ((sizeof(Sel2Shared) + 15) & ~size_t(15)));
+    Sel2Shared<NT>& sh = *reinterpret_cast<Sel2Shared<NT>*>(sel2_raw);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(sel2_raw + ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)));
     const int jj = blockIdx.x;
     const int q = blockIdx.y;
     const int j = a.j0 + jj;
@@ -389,7 +408,7 @@ __global__ void __launch_bounds__(SEL2_THREADS) select_v2_kernel(const SelectArg
     if ((n & 3) == 0) {
         const float4* s4 = reinterpret_cast<const float4*>(yrow);
         uint4* k4 = reinterpret_cast<uint4*>(keys);
-        for (int i = threadIdx.x; i < n / 4; i += SEL2_THREADS) {
+        for (int i = threadIdx.x; i < n / 4; i += NT) {
             const float4 v = __ldg(s4 + i);
             const uint4 k = make_uint4(fkey(v.x), fkey(v.y), fkey(v.z), fkey(v.w));
             k4[i] = k;
@@ -397,7 +416,7 @@ __global__ void __launch_bounds__(SEL2_THREADS) select_v2_kernel(const SelectArg
             kmax = max(kmax, max(max(k.x, k.y), max(k.z, k.w)));
         }
     } else {
-        for (int i = threadIdx.x; i < n; i += SEL2_THREADS) {
+        for (int i = threadIdx.x; i < n; i += NT) {
             const uint32_t k = fkey(__ldg(yrow + i));
             keys[i] = k;
             kmin = min(kmin, k);
@@ -412,7 +431,7 @@ __global__ void __launch_bounds__(SEL2_THREADS) select_v2_kernel(const SelectArg
     if (a.notion == 1) {
         // MAD: keys of |y - med| (FP64 deviation, FP32 key), in place
         uint32_t dmin = 0xFFFFFFFFu, dmax = 0u;
-        for (int i = threadIdx.x; i < n; i += SEL2_THREADS) {
+        for (int i = threadIdx.x; i < n; i += NT) {
             const uint32_t k = fkey((float)fabs((double)kfloat(keys[i]) - med));
             keys[i] = k;
             dmin = min(dmin, k);
@@ -432,7 +451,7 @@ __global__ void __launch_bounds__(SEL2_THREADS) select_v2_kernel(const SelectArg
         } else {
             // positive deviations y - med > 0 keep their key, the rest sort last
             uint32_t dmin = 0xFFFFFFFFu, dmax = 0u, npos = 0;
-            for (int i = threadIdx.x; i < n; i += SEL2_THREADS) {
+            for (int i = threadIdx.x; i < n; i += NT) {
                 const double t = (double)kfloat(keys[i]) - med;
                 uint32_t k = 0xFFFFFFFFu;
                 if (t > 0.0) {
@@ -462,12 +481,20 @@ __global__ void __launch_bounds__(SEL2_THREADS) select_v2_kernel(const SelectArg
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
     if (a.Qb == 0 || a.jcount == 0) return cudaSuccess;
     if (a.n <= SEL2_MAX_N) {
-        const size_t smem = ((sizeof(Sel2Shared) + 15) & ~size_t(15)) + (size_t)a.n * 4;
-        cudaError_t e = cudaFuncSetAttribute(select_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
         dim3 grid((unsigned)a.jcount, (unsigned)a.Qb);
-        select_v2_kernel<<<grid, SEL2_THREADS, smem, st>>>(a);
+        if (a.n <= SEL2_WIDE_N) {
+            const size_t smem = ((sizeof(Sel2Shared<256>) + 15) & ~size_t(15)) + (size_t)a.n * 4;
+            cudaError_t e = cudaFuncSetAttribute(select_v2_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return e;
+            select_v2_kernel<256><<<grid, 256, smem, st>>>(a);
+        } else {
+            const size_t smem = ((sizeof(Sel2Shared<512>) + 15) & ~size_t(15)) + (size_t)a.n * 4;
+            cudaError_t e = cudaFuncSetAttribute(select_v2_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return e;
+            select_v2_kernel<512><<<grid, 512, smem, st>>>(a);
+        }
         return cudaGetLastError();
     }
     size_t smem = (sizeof(SelShared) + 15) & ~size_t(15);
