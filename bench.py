@@ -38,12 +38,17 @@ WORKLOADS = {
     "config2": ("projection", 10_000, 20, 20_000, 20, 0.9, "gaussian", 512),
     "config3": ("asym_projection", 50_000, 50, 20_000, 20, 0.9, "cauchy", 32),
     "config4": ("halfspace", 100_000, 50, 20_000, 20, 0.9, "gaussian", 1024),
+    # config 5 cells (n = 1M, d = 200) on a fixed query subset per step
+    "config5": ("halfspace", 1_000_000, 200, 20_000, 20, 0.9, "gaussian", 16),
+    "config5p": ("projection", 1_000_000, 200, 20_000, 20, 0.9, "gaussian", 4),
 }
 WORKLOAD_TEXT = {
     "config1": "halfspace depth RRS, n=1000 Gaussian, d=5, NRandom=1000, n_refinements=10, all points as queries",
     "config2": "projection depth RRS (median/MAD), n=10k, d=20, Gaussian, k=20000 x r=20",
     "config3": "asymmetric projection depth RRS, n=50k, d=50, Cauchy (t, nu=1), k=20000 x r=20",
     "config4": "halfspace depth RRS, n=100k, d=50, K=1000x20 refinements (k=20000), all n points as queries",
+    "config5": "halfspace depth RRS, n=1M, d=200, Gaussian, k=20000 x r=20, alpha 0.9 (one cell of the sweep)",
+    "config5p": "projection depth RRS, n=1M, d=200, Gaussian, k=20000 x r=20, alpha 0.9 (one cell of the sweep)",
 }
 FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: 148 SMs x 128 FP32 lanes x FMA x 1965 MHz
 
