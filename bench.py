@@ -267,6 +267,7 @@ def main():
     contract_ms = 0.0
     contract_launches = 0
     tensor_launches = 0
+    select_ms = 0.0
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -280,6 +281,7 @@ def main():
         contract_ms += st["ms_contract_total"]
         contract_launches += st["contract_launches"]
         tensor_launches += st["tensor_contract_launches"]
+        select_ms += st["ms_univariate"]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -328,6 +330,18 @@ def main():
     roofline.update({"flops_per_launch": flops_per_launch, "avg_launch_ms": avg_launch_ms,
                      "kernel_share_of_step": contract_ms / ms if ms else None,
                      "hbm_peak_measured_gbs": peaks.get("hbm_gbs")})
+    if notion != "halfspace" and select_ms > contract_ms:
+        # the univariate stage dominates: report its roofline, HBM-bound on reading every stored
+        # projection once (4 n bytes per direction and refinement); the contraction stays alongside
+        hbm = peaks.get("hbm_gbs") or 8000.0
+        sel_bytes = 4.0 * n * m * r * B * args.steps
+        sel_gbs = sel_bytes / (select_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": sel_gbs, "peak": hbm, "unit": "GB/s", "frac": sel_gbs / hbm,
+                    "traffic": None, "kernel": "select_v2_kernel" if n <= 53248 else "select_kernel",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "nominal 8 TB/s",
+                    "achieved_is": "algorithmic bytes (the stored projections, 4 n per direction) / select time",
+                    "kernel_share_of_step": select_ms / ms if ms else None,
+                    "contraction": roofline}
 
     # e2e through the public API with host buffers (H2D of data + queries, D2H of results)
     e2e = None
