@@ -6,6 +6,12 @@ depthforge-compatible names (optimizer.py / projection.py / directions.py):
     RefinementRecord, PhaseTimer, depth_batch, refined_random_search,
     evaluate_directions, simple_random_search, pole_update_rule,
     generate_batch, Pole, CapSpec, DirectionBatch
+    perfmodel (perfmodel.py): CostConstants, Workload, TimingProfile, t_sequential,
+    t_parallel, speedup, speedup_plateau, fit_constants, FitReport
+    Mahalanobis baseline (univariate.py): LocationScatter, estimate_mle,
+    mahalanobis_depth, mahalanobis_depth_batch
+    study harness (study/): rank_study, convergence_study, convergence_frontier,
+    breakdown_bench, runtime_grid, spearman_rho, kendall_tau, synthetic specs
 data-depth-style wrappers:
     halfspace, projection, aprojection (NRandom, n_refinements, sphcap_shrink,
     solver="refinedrandom")
@@ -18,6 +24,9 @@ from ._lib import Engine, LibraryNotBuilt, device_count, engine, load_library
 from .config import (CapSpec, Dataset, DepthResult, DimensionMismatch, DirectionBatch, NOTIONS,
                      ParallelConfig, PhaseTimer, Pole, RefinementRecord, RrsConfig)
 from .datadepth import aprojection, halfspace, projection
+from .mahalanobis import LocationScatter, estimate_mle, mahalanobis_depth, mahalanobis_depth_batch
+from .perfmodel import (CostConstants, FitReport, RankDeficientDesign, TimingProfile, Workload, fit_constants,
+                        speedup, speedup_plateau, t_parallel, t_sequential)
 from .solver import (depth_batch, depth_batch_arrays, evaluate_directions, evaluate_directions_counts,
                      generate_batch, pole_update_rule, refined_random_search, simple_random_search)
 
@@ -30,6 +39,9 @@ def backend_name() -> str:
 __version__ = "0.1.0"
 
 __all__ = [
+    "CostConstants", "FitReport", "LocationScatter", "RankDeficientDesign", "TimingProfile", "Workload",
+    "estimate_mle", "fit_constants", "mahalanobis_depth", "mahalanobis_depth_batch", "speedup",
+    "speedup_plateau", "t_parallel", "t_sequential",
     "CapSpec", "Dataset", "DepthResult", "DimensionMismatch", "DirectionBatch", "Engine",
     "LibraryNotBuilt", "NOTIONS", "ParallelConfig", "PhaseTimer", "Pole", "RefinementRecord",
     "RrsConfig", "aprojection", "backend_name", "depth_batch", "depth_batch_arrays", "device_count",

@@ -1,0 +1,109 @@
+"""Study drivers on one B200:
+
+1. phase breakdown (CUDA-event phases) over a workload set + the paper's T_G
+   fit with measured lam = f_CPU / f_GPU (host "cpu MHz" / SM clock sampled
+   by nvidia-smi during the runs), g = 148 SMs;
+2. rank study (pdf ordering vs RRS depths, Spearman / Kendall);
+3. convergence frontier (minimal r per (d, k)).
+
+    python scripts/study_b200.py --out gpurun_out/study.json
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import paper_2506_08262_b200 as rrs  # noqa: E402
+from paper_2506_08262_b200 import perfmodel as pm  # noqa: E402
+from paper_2506_08262_b200 import study  # noqa: E402
+
+
+def cpu_mhz() -> float:
+    vals = [float(l.split(":")[1]) for l in open("/proc/cpuinfo") if l.startswith("cpu MHz")]
+    return float(np.median(vals)) if vals else float("nan")
+
+
+def sm_mhz() -> float:
+    try:
+        out = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=10).stdout
+        return float(out.split()[0])
+    except Exception:
+        return float("nan")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="gpurun_out/study.json")
+    ap.add_argument("--quick", action="store_true")
+    a = ap.parse_args()
+    res = {}
+
+    # 1. breakdown + fit ---------------------------------------------------
+    shapes = [(20_000, 10, 2_000, 2), (50_000, 20, 4_000, 4), (100_000, 50, 10_000, 10), (100_000, 50, 20_000, 20),
+              (30_000, 50, 6_000, 3), (200_000, 8, 3_000, 3), (60_000, 100, 2_000, 2), (10_000, 20, 20_000, 20)]
+    if a.quick:
+        shapes = shapes[:4]
+    clocks = []
+    for notion in ("halfspace", "projection"):
+        prof_f = []
+        f_cpu = cpu_mhz()
+        t0 = time.time()
+        ws0 = [pm.Workload(n=n, d=d, k=k, r=r, g=148, lam=1.0, d_chunk=1) for n, d, k, r in shapes]
+        study.breakdown_bench(ws0[:1], notion, "parallel", repeats=1)          # warm the library + dataset path
+        clocks.append(sm_mhz())
+        profs = study.breakdown_bench(ws0, notion, "parallel", repeats=5)
+        clocks.append(sm_mhz())
+        f_gpu = float(np.nanmax(clocks)) if np.isfinite(clocks).any() else float("nan")
+        lam = f_cpu / f_gpu if np.isfinite(f_cpu) and np.isfinite(f_gpu) and f_gpu > 0 else 1.0
+        # re-label the workloads with the measured lam (phase times unchanged)
+        for p in profs:
+            w = p.workload
+            prof_f.append(pm.TimingProfile(workload=pm.Workload(n=w.n, d=w.d, k=w.k, r=w.r, g=148, lam=lam,
+                                                                d_chunk=1),
+                                           generation=p.generation, projection=p.projection,
+                                           univariate=p.univariate, total=p.total, path="parallel"))
+        rep = pm.fit_constants(prof_f)
+        pred = [pm.t_parallel(rep.constants, p.workload) for p in prof_f]
+        res[f"breakdown_{notion}"] = {
+            "f_cpu_mhz": f_cpu, "f_gpu_mhz": f_gpu, "lam": lam, "g": 148, "d_chunk": 1,
+            "rows": study.profile_rows(prof_f),
+            "fit": json.loads(rep.to_json()),
+            "predicted_total_s": pred, "measured_total_s": [p.total for p in prof_f],
+            "seconds": time.time() - t0,
+        }
+        print(notion, "fit", rep.to_json().replace("\n", " ")[:400], flush=True)
+
+    # 2. rank study --------------------------------------------------------
+    t0 = time.time()
+    spec = study.ToeplitzGaussianSpec(dim=5, n=10_000, seed=0)
+    cfg = rrs.RrsConfig(total_directions=10_000, refinements=20, shrink=0.9, seed=1)
+    rs = study.rank_study(spec, ["halfspace", "projection", "asym_projection"], 500 if a.quick else 2000, cfg)
+    res["rank_study"] = {"spec": "ToeplitzGaussian d=5 n=10000 seed 0", "k": 10_000, "r": 20,
+                         "queries": len(next(iter(rs.depths.values()))), "rows": list(rs.rows),
+                         "seconds": time.time() - t0}
+    print("rank", rs.rows, flush=True)
+
+    # 3. convergence frontier ---------------------------------------------
+    t0 = time.time()
+    grid = study.StudyGrid(alphas=(0.9,), refinement_counts=(5, 10, 20, 40), direction_counts=(1_000, 5_000, 20_000),
+                           dims=(5, 10, 20), query_count=64 if a.quick else 256,
+                           reference=study.ReferenceSpec(k=100_000, r=40, alpha=0.9, repeats=3))
+    fr = study.convergence_frontier(grid, "halfspace", study.ToeplitzGaussianSpec(dim=5, n=10_000, seed=0),
+                                    tol=1e-4, seed=0)
+    res["frontier_halfspace"] = {"rows": list(fr.rows), "seconds": time.time() - t0}
+    print("frontier", fr.rows, flush=True)
+
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+    with open(a.out, "w") as fh:
+        json.dump(res, fh, indent=1, default=float)
+
+
+if __name__ == "__main__":
+    main()

@@ -340,3 +340,31 @@ def test_tier2_large_rows(b200, notion, n):
         got = b200.evaluate_directions(z, data, U, notion, cfg)
         ref = oracle.evaluate_directions(z, X, U, notion)
         np.testing.assert_allclose(got, ref, rtol=DEPTH_RTOL, atol=0)
+
+
+@pytest.mark.parametrize("notion", ["halfspace", "projection"])
+def test_config5_shape(b200, notion):
+    """The config-5 shape (d = 200, past the tensor path's d <= 64: FFMA
+    contraction; n past the shared-memory select: global-memory select) at
+    n = 400k, Cauchy data, against FP64: halfspace counts within the tie zone,
+    projection depths to DEPTH_RTOL."""
+    from oracle import oracle
+    from paper_2506_08262_b200.synthetic import student_t
+
+    X = student_t(200, 400_000, 1.0, seed=5)
+    rng = np.random.default_rng(6)
+    U = rng.standard_normal((48, 200))
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    data = b200.Dataset(X)
+    z = X[9] + 0.01 * rng.standard_normal(200)
+    if notion == "halfspace":
+        _, cle, cge = b200.evaluate_directions_counts(z, data, U)
+        y = X @ U.T - (U @ z)[None, :]
+        xn = np.linalg.norm(X, axis=1)
+        T = (np.abs(y) < TIE_REL * np.maximum(xn, np.linalg.norm(z))[:, None]).sum(axis=0)
+        rle, rge = (y <= 0).sum(axis=0), (y >= 0).sum(axis=0)
+        assert np.all(np.abs(cle - rle) <= T) and np.all(np.abs(cge - rge) <= T)
+    else:
+        got = b200.evaluate_directions(z, data, U[:8], notion, b200.ParallelConfig(workers=1))
+        ref = oracle.evaluate_directions(z, X, U[:8], notion)
+        np.testing.assert_allclose(got, ref, rtol=DEPTH_RTOL, atol=0)
