@@ -56,7 +56,6 @@ def test_cli_exit_codes(tmp_path, capsys):
     assert "does not match data dimension 3" in capsys.readouterr().err
     assert cli.main(["depth", "--data", str(bad), "--query-inline", "1", "--notion", "halfspace"]) == cli.EXIT_BAD_DATA
     assert cli.main(["depth", "--data", str(x), "--query-inline", "1,a,2", "--notion", "projection"]) == cli.EXIT_BAD_DATA
-    assert cli.main(["depth", "--data", str(x), "--query-inline", "1,2,3", "--notion", "mahalanobis"]) == cli.EXIT_BAD_FLAGS
     assert cli.main(["depth", "--data", str(x), "--query-inline", "1,2,3", "--notion", "halfspace",
                      "--k", "5", "--r", "10"]) == cli.EXIT_BAD_FLAGS  # RrsConfig: k < r
     assert cli.main(["depth", "--data", str(x)]) == 2  # argparse usage error
@@ -68,6 +67,67 @@ def test_cli_gen(tmp_path):
     from paper_2506_08262_b200.synthetic import student_t
 
     assert np.array_equal(io.read_matrix(out), student_t(4, 50, 1.0, seed=3))
+    assert cli.main(["gen", "--dist", "student", "--d", "4", "--n", "5", "--out", str(out)]) == cli.EXIT_BAD_FLAGS
+    assert cli.main(["gen", "--dist", "exponential", "--d", "2", "--n", "6", "--seed", "9", "--out", str(out)]) == 0
+    from paper_2506_08262_b200.study import ExponentialSpec, generate
+
+    assert np.array_equal(io.read_matrix(out), generate(ExponentialSpec(dim=2, n=6, seed=9)))
+
+
+def test_cli_mahalanobis_depth(tmp_path, capsys):
+    """Host algebra, no device: (1 + quadratic form)^-1 with the MLE estimate."""
+    from paper_2506_08262_b200 import estimate_mle, mahalanobis_depth_batch
+
+    X = np.random.default_rng(3).standard_normal((40, 3))
+    io.write_matrix(tmp_path / "x.dfmx", X)
+    capsys.readouterr()
+    assert cli.main(["depth", "--data", str(tmp_path / "x.dfmx"), "--query-inline", "0.1,0.2,0.3",
+                     "--notion", "mahalanobis"]) == 0
+    out = json.loads(capsys.readouterr().out)
+    want = mahalanobis_depth_batch(np.array([[0.1, 0.2, 0.3]]), estimate_mle(X))[0]
+    assert out["backend"] == "b200" and out["query_count"] == 1 and out["results"] == [{"depth": float(want)}]
+
+
+def test_rows_csv_and_config(tmp_path):
+    rows = [{"a": 1, "b": 1.0 / 3.0, "c": "x"}, {"a": 2, "b": 2.5, "c": "y"}]
+    io.write_rows_csv(tmp_path / "r.csv", rows)
+    back = io.read_rows_csv(tmp_path / "r.csv")
+    assert back[0] == {"a": "1", "b": "0.33333333333333331", "c": "x"} and float(back[0]["b"]) == 1.0 / 3.0
+    (tmp_path / "c.cfg").write_text("# comment\nalphas = 0.6, 0.9  # trailing\n\nqueries=5\n")
+    assert io.parse_config(tmp_path / "c.cfg") == {"alphas": "0.6, 0.9", "queries": "5"}
+    assert io.parse_list("1, 2,,3", int) == [1, 2, 3]
+    (tmp_path / "bad.cfg").write_text("novalue\n")
+    with pytest.raises(ValueError, match="key = value"):
+        io.parse_config(tmp_path / "bad.cfg")
+
+
+def test_cli_fit_model(tmp_path, capsys):
+    """fit-model on breakdown-style rows: constants recovered, --predict plateau,
+    exit 3 for missing columns, exit 6 for a rank-deficient design."""
+    from paper_2506_08262_b200 import perfmodel as pm
+    from paper_2506_08262_b200.study import profile_rows
+
+    C = pm.CostConstants(c_const=1e-3, c_rv=1e-9, c_proj=1e-12, c_depth=2e-11)
+    profs = []
+    for n, d, k, r in ((1000, 5, 400, 2), (5000, 10, 900, 3), (20000, 3, 2000, 4), (8000, 40, 600, 1), (3000, 7, 5000, 5)):
+        w = pm.Workload(n=n, d=d, k=k, r=r, g=148, lam=1.5, d_chunk=1)
+        g, p, u = pm._terms(w, "parallel")
+        profs.append(pm.TimingProfile(workload=w, generation=C.c_rv * g, projection=C.c_proj * p,
+                                      univariate=C.c_depth * u, total=C.c_const + C.c_rv * g + C.c_proj * p
+                                      + C.c_depth * u, path="parallel"))
+    io.write_rows_csv(tmp_path / "b.csv", profile_rows(profs))
+    capsys.readouterr()
+    assert cli.main(["fit-model", "--profiles", str(tmp_path / "b.csv"), "--predict", "--g", "148",
+                     "--lambda", "1.5", "--d", "50", "--d-chunk", "1"]) == 0
+    out = json.loads(capsys.readouterr().out)
+    assert out["constants"]["c_proj"] == pytest.approx(1e-12, rel=1e-9)
+    assert out["predict"]["plateau"] == pytest.approx(pm.speedup_plateau(C, 50, 1, 148, 1.5), rel=1e-6)
+    io.write_rows_csv(tmp_path / "short.csv", [{"n": 1, "d": 2}])
+    assert cli.main(["fit-model", "--profiles", str(tmp_path / "short.csv")]) == cli.EXIT_BAD_DATA
+    io.write_rows_csv(tmp_path / "same.csv", profile_rows([profs[0]] * 4))
+    assert cli.main(["fit-model", "--profiles", str(tmp_path / "same.csv")]) == cli.EXIT_RANK_DEFICIENT
+    assert cli.main(["study", "rank", "--out", str(tmp_path / "f" / "x"), "--dist", "student", "--d", "3"]) \
+        == cli.EXIT_BAD_FLAGS   # --nu required, checked before any device work
 
 
 @pytest.mark.gpu

@@ -124,3 +124,34 @@ def test_runtime_grid(b200):
 
     res = study.runtime_grid((3, 5), (200, 400), n=1000, r=2, notion="halfspace", repeats=2)
     assert len(res.rows) == 4 and all(r["seconds"] > 0 for r in res.rows)
+
+
+def test_cli_bench_and_study_commands(b200, tmp_path, capsys):
+    """The reference's bench / study / fit-model commands end to end on the
+    device at desk-test sizes (config files override the desk defaults)."""
+    from paper_2506_08262_b200 import cli, io
+
+    cfg = tmp_path / "tiny.cfg"
+    cfg.write_text("alphas = 0.9\nrefinements = 2,4\ndirections = 100,200\nd = 3\ndims = 2,3\nn = 300\n"
+                   "queries = 4\nref_k = 1000\nref_r = 5\nref_repeats = 1\nk = 500\nr = 5\n"
+                   "notions = halfspace,projection\n")
+    for cmd, files in ((["study", "converge"], ["converge.csv", "converge_means.csv", "converge_summary.json"]),
+                       (["study", "frontier"], ["frontier.csv", "frontier_summary.json"]),
+                       (["study", "rank"], ["rank.csv", "rank_summary.json"])):
+        out = tmp_path / cmd[1]
+        assert cli.main(cmd + ["--config", str(cfg), "--out", str(out), "--seed", "1"]) == 0, cmd
+        assert all((out / f).exists() for f in files), cmd
+    assert len(io.read_rows_csv(tmp_path / "converge" / "converge.csv")) == 4 * 4
+    assert [r["pair"] for r in io.read_rows_csv(tmp_path / "rank" / "rank.csv")] == \
+        ["pdf_x_halfspace", "pdf_x_projection", "pdf_x_mahalanobis"]
+    bd = tmp_path / "bd"
+    assert cli.main(["bench", "breakdown", "--path", "parallel", "--dims", "3,6", "--directions", "200,400",
+                     "--n", "2000", "--r", "2", "--repeats", "2", "--workers", "148", "--d-chunk", "1",
+                     "--out", str(bd)]) == 0
+    assert len(io.read_rows_csv(bd / "breakdown.csv")) == 4 * 3
+    capsys.readouterr()
+    assert cli.main(["fit-model", "--profiles", str(bd / "breakdown.csv")]) == 0
+    assert json.loads(capsys.readouterr().out)["profile_count"] == 4
+    assert cli.main(["bench", "grid", "--dims", "3", "--directions", "100,200", "--n", "500", "--repeats", "2",
+                     "--notion", "halfspace", "--out", str(tmp_path / "grid")]) == 0
+    assert cli.main(["bench", "grid", "--notion", "mahalanobis", "--out", str(tmp_path / "g2")]) == 2
