@@ -240,9 +240,13 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SelectArgs a)
 // Same arithmetic as select_kernel: FP32 order statistics, FP64 midpoints and
 // deviations (_kernels.pyx:202-351).
 constexpr int64_t SEL2_MAX_N = 53248;  // 208 KB of keys
-// 256 threads for rows up to SEL2_WIDE_N, 512 above (one CTA per SM at n = 50k:
-// more warps in flight for the latency-bound passes)
+// 256 threads for rows up to SEL2_WIDE_N, 512 up to SEL2_WIDER_N, 1024 above
+// (one CTA per SM at n = 50k: more warps in flight for the latency-bound passes)
 constexpr int64_t SEL2_WIDE_N = 16384;
+#ifndef RRS_SEL2_WIDER_N
+#define RRS_SEL2_WIDER_N 24576
+#endif
+constexpr int64_t SEL2_WIDER_N = RRS_SEL2_WIDER_N;
 
 // hist[(key >> shift) & 255] += 1 when (key & pmask) == prefix: a predicated
 // red.shared (no branch / reconvergence per element)
@@ -257,7 +261,8 @@ __device__ __forceinline__ void hist_add_if(uint32_t* h, uint32_t key, uint32_t 
 template <int NT>
 struct Sel2Shared {
     static constexpr int W = NT / 32;
-    uint32_t hist[W][256];
+    static constexpr int H = W < 16 ? W : 16;  // histograms (warps w and w + 16 share one at NT = 1024)
+    uint32_t hist[H][256];
     uint32_t wsum[W];
     uint32_t s_kmin, s_kmax;
     int s_bin;
@@ -305,7 +310,7 @@ __device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t 
     uint32_t prefix = kmin & pmask;                // digits above `shift` are common
     uint32_t below_total = 0, last = 0;
     for (;;) {
-        uint32_t* h = sh.hist[warp];
+        uint32_t* h = sh.hist[warp % Sel2Shared<NT>::H];
         for (int b = lane; b < 256; b += 32) h[b] = 0u;
         __syncthreads();
         // 4 keys per 16-byte load; the row is 16-byte aligned, the tail is scalar
@@ -324,7 +329,7 @@ __device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t 
         uint32_t tot = 0;
         if (tid < 256)
 #pragma unroll
-            for (int w = 0; w < NT / 32; ++w) tot += sh.hist[w][tid];
+            for (int w = 0; w < Sel2Shared<NT>::H; ++w) tot += sh.hist[w][tid];
         uint32_t incl = tot;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -478,24 +483,22 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
     if (threadIdx.x == 0) a.depths[(size_t)q * a.m + j] = depth;
 }
 
+template <int NT>
+static cudaError_t launch_sel2(const SelectArgs& a, dim3 grid, cudaStream_t st) {
+    const size_t smem = ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)) + (size_t)a.n * 4;
+    cudaError_t e = cudaFuncSetAttribute(select_v2_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    select_v2_kernel<NT><<<grid, NT, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
     if (a.Qb == 0 || a.jcount == 0) return cudaSuccess;
     if (a.n <= SEL2_MAX_N) {
         dim3 grid((unsigned)a.jcount, (unsigned)a.Qb);
-        if (a.n <= SEL2_WIDE_N) {
-            const size_t smem = ((sizeof(Sel2Shared<256>) + 15) & ~size_t(15)) + (size_t)a.n * 4;
-            cudaError_t e = cudaFuncSetAttribute(select_v2_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem);
-            if (e != cudaSuccess) return e;
-            select_v2_kernel<256><<<grid, 256, smem, st>>>(a);
-        } else {
-            const size_t smem = ((sizeof(Sel2Shared<512>) + 15) & ~size_t(15)) + (size_t)a.n * 4;
-            cudaError_t e = cudaFuncSetAttribute(select_v2_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem);
-            if (e != cudaSuccess) return e;
-            select_v2_kernel<512><<<grid, 512, smem, st>>>(a);
-        }
-        return cudaGetLastError();
+        if (a.n <= SEL2_WIDE_N) return launch_sel2<256>(a, grid, st);
+        if (a.n <= SEL2_WIDER_N) return launch_sel2<512>(a, grid, st);
+        return launch_sel2<1024>(a, grid, st);
     }
     size_t smem = (sizeof(SelShared) + 15) & ~size_t(15);
     if (a.n <= SEL_CACHE_MAX) smem += (size_t)a.n * sizeof(float);
