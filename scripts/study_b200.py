@@ -3,8 +3,10 @@
 1. phase breakdown (CUDA-event phases) over a workload set + the paper's T_G
    fit with measured lam = f_CPU / f_GPU (host "cpu MHz" / SM clock sampled
    by nvidia-smi during the runs), g = 148 SMs;
-2. rank study (pdf ordering vs RRS depths, Spearman / Kendall);
-3. convergence frontier (minimal r per (d, k)).
+2. rank study (pdf ordering vs RRS depths, Spearman / Kendall) at the
+   reference CLI's --full settings (500 of the 5000 queries);
+3. convergence frontier (minimal r per (d, k)) at the reference CLI's --full
+   settings (the paper's Table 4 grid).
 
     python scripts/study_b200.py --out gpurun_out/study.json
 """
@@ -80,25 +82,36 @@ def main():
         }
         print(notion, "fit", rep.to_json().replace("\n", " ")[:400], flush=True)
 
-    # 2. rank study --------------------------------------------------------
-    t0 = time.time()
-    spec = study.ToeplitzGaussianSpec(dim=5, n=10_000, seed=0)
-    cfg = rrs.RrsConfig(total_directions=10_000, refinements=20, shrink=0.9, seed=1)
-    rs = study.rank_study(spec, ["halfspace", "projection", "asym_projection"], 500 if a.quick else 2000, cfg)
-    res["rank_study"] = {"spec": "ToeplitzGaussian d=5 n=10000 seed 0", "k": 10_000, "r": 20,
-                         "queries": len(next(iter(rs.depths.values()))), "rows": list(rs.rows),
-                         "seconds": time.time() - t0}
-    print("rank", rs.rows, flush=True)
+    # 2. rank study: the reference CLI's --full settings (d = 50, n = 100k, k = 100k,
+    #    r = 40, projection + asym_projection) on a bounded number of queries
+    from paper_2506_08262_b200.cli import STUDY_SETTINGS
 
-    # 3. convergence frontier ---------------------------------------------
+    full = STUDY_SETTINGS["rank"][1]
     t0 = time.time()
-    grid = study.StudyGrid(alphas=(0.9,), refinement_counts=(5, 10, 20, 40), direction_counts=(1_000, 5_000, 20_000),
-                           dims=(5, 10, 20), query_count=64 if a.quick else 256,
-                           reference=study.ReferenceSpec(k=100_000, r=40, alpha=0.9, repeats=3))
-    fr = study.convergence_frontier(grid, "halfspace", study.ToeplitzGaussianSpec(dim=5, n=10_000, seed=0),
-                                    tol=1e-4, seed=0)
-    res["frontier_halfspace"] = {"rows": list(fr.rows), "seconds": time.time() - t0}
-    print("frontier", fr.rows, flush=True)
+    spec = study.ToeplitzGaussianSpec(dim=int(full["d"]), n=int(full["n"]), seed=0)
+    cfg = rrs.RrsConfig(total_directions=int(full["k"]), refinements=int(full["r"]), shrink=float(full["alpha"]),
+                        seed=0)
+    nq = 100 if a.quick else 500
+    rs = study.rank_study(spec, full["notions"].split(","), nq, cfg)
+    res["rank_study_full_settings"] = {"settings": dict(full, queries=str(nq)), "rows": list(rs.rows),
+                                       "seconds": time.time() - t0}
+    print("rank", rs.rows, time.time() - t0, flush=True)
+
+    # 3. convergence frontier: the reference CLI's --full settings (Table 4 grid:
+    #    d in 5..175, k up to 1e5, r up to 175, reference k = 3e5 x 3 repeats)
+    fs = STUDY_SETTINGS["frontier"][1]
+    t0 = time.time()
+    dims = [int(v) for v in fs["dims"].split(",")]
+    grid = study.StudyGrid(alphas=(float(fs["alphas"]),),
+                           refinement_counts=tuple(int(v) for v in fs["refinements"].split(",")),
+                           direction_counts=tuple(int(v) for v in fs["directions"].split(",")),
+                           dims=tuple(dims[:2] if a.quick else dims), query_count=int(fs["queries"]),
+                           reference=study.ReferenceSpec(k=int(fs["ref_k"]), r=int(fs["ref_r"]),
+                                                        alpha=float(fs["ref_alpha"]), repeats=int(fs["ref_repeats"])))
+    fr = study.convergence_frontier(grid, fs["notion"], study.ToeplitzGaussianSpec(dim=dims[0], n=int(fs["n"]), seed=0),
+                                    tol=float(fs["tol"]), seed=0)
+    res["frontier_full_settings"] = {"settings": fs, "rows": list(fr.rows), "seconds": time.time() - t0}
+    print("frontier", fr.rows, time.time() - t0, flush=True)
 
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as fh:
