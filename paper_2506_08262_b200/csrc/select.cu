@@ -24,6 +24,10 @@ constexpr int SEL_THREADS = 512;
 constexpr int SEL_WARPS = SEL_THREADS / 32;
 constexpr int HIST_BINS = 2048;
 constexpr int64_t SEL_CACHE_MAX = 40960;  // floats of y cached per CTA (160 KB)
+#ifndef RRS_SEL_UNROLL
+#define RRS_SEL_UNROLL 2
+#endif
+constexpr int SEL_UNROLL = RRS_SEL_UNROLL;  // float4 loads in flight per thread per pass
 
 __device__ __forceinline__ uint32_t fkey(float f) {
     uint32_t b = __float_as_uint(f);
@@ -86,7 +90,7 @@ __device__ __forceinline__ int block_sum(int v, SelShared& sh) {
 // number of participating keys <= that key.
 template <typename KF>
 __device__ uint32_t block_select(const float* __restrict__ src, int64_t n, int64_t k, KF kf,
-                                 SelShared& sh, int64_t& c_le) {
+                                 SelShared& sh, int64_t& c_le, bool aligned4) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t prefix = 0, pmask = 0;
     int64_t kk = k, below_total = 0;
@@ -99,15 +103,36 @@ __device__ uint32_t block_select(const float* __restrict__ src, int64_t n, int64
         const uint32_t bmask = (uint32_t)(nb - 1);
         for (int b = tid; b < nb; b += SEL_THREADS) sh.hist[b] = 0;
         __syncthreads();
-        for (int64_t base = (int64_t)warp * 32; base < n; base += (int64_t)SEL_WARPS * 32) {
-            const int64_t i = base + lane;
+        // 16-byte loads, SEL_UNROLL in flight per thread (the row streams from
+        // HBM/L2 when it exceeds shared memory: bytes in flight set the rate)
+        const auto add = [&](float y, bool valid) {
             int bin = -1;
-            if (i < n) {
-                uint32_t key;
-                if (kf(src[i], key) && (key & pmask) == prefix) bin = (int)((key >> shift) & bmask);
-            }
+            uint32_t key;
+            if (valid && kf(y, key) && (key & pmask) == prefix) bin = (int)((key >> shift) & bmask);
             const unsigned grp = __match_any_sync(0xffffffffu, bin);
             if (bin >= 0 && lane == __ffs(grp) - 1) atomicAdd(&sh.hist[bin], __popc(grp));
+        };
+        const int64_t n4 = aligned4 ? (n >> 2) : 0;
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        for (int64_t base = (int64_t)warp * 32 * SEL_UNROLL; base < n4; base += (int64_t)SEL_WARPS * 32 * SEL_UNROLL) {
+            float4 v[SEL_UNROLL];
+#pragma unroll
+            for (int u = 0; u < SEL_UNROLL; ++u) {
+                const int64_t i = base + u * 32 + lane;
+                v[u] = i < n4 ? s4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < SEL_UNROLL; ++u) {
+                const bool ok = base + u * 32 + lane < n4;
+                add(v[u].x, ok);
+                add(v[u].y, ok);
+                add(v[u].z, ok);
+                add(v[u].w, ok);
+            }
+        }
+        for (int64_t b0 = 4 * n4 + (int64_t)warp * 32; b0 < n; b0 += (int64_t)SEL_WARPS * 32) {
+            const int64_t i = b0 + lane;
+            add(i < n ? src[i] : 0.f, i < n);
         }
         __syncthreads();
         // exclusive scan over nb bins: each thread owns nb/SEL_THREADS consecutive bins
@@ -149,12 +174,31 @@ __device__ uint32_t block_select(const float* __restrict__ src, int64_t n, int64
 // smallest participating key strictly greater than `key`
 template <typename KF>
 __device__ uint32_t block_min_greater(const float* __restrict__ src, int64_t n, uint32_t key, KF kf,
-                                      SelShared& sh) {
+                                      SelShared& sh, bool aligned4) {
     uint32_t best = 0xFFFFFFFFu;
-    for (int64_t i = threadIdx.x; i < n; i += SEL_THREADS) {
+    const auto take = [&](float y) {
         uint32_t k2;
-        if (kf(src[i], k2) && k2 > key && k2 < best) best = k2;
+        if (kf(y, k2) && k2 > key && k2 < best) best = k2;
+    };
+    const int64_t n4 = aligned4 ? (n >> 2) : 0;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    for (int64_t base = threadIdx.x; base < n4; base += (int64_t)SEL_THREADS * SEL_UNROLL) {
+        float4 v[SEL_UNROLL];
+#pragma unroll
+        for (int u = 0; u < SEL_UNROLL; ++u) {
+            const int64_t i = base + (int64_t)u * SEL_THREADS;
+            v[u] = i < n4 ? s4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < SEL_UNROLL; ++u)
+            if (base + (int64_t)u * SEL_THREADS < n4) {
+                take(v[u].x);
+                take(v[u].y);
+                take(v[u].z);
+                take(v[u].w);
+            }
     }
+    for (int64_t i = 4 * n4 + threadIdx.x; i < n; i += SEL_THREADS) take(src[i]);
     best = __reduce_min_sync(0xffffffffu, best);
     if (threadIdx.x == 0) sh.s_min = 0xFFFFFFFFull;
     __syncthreads();
@@ -169,14 +213,14 @@ __device__ uint32_t block_min_greater(const float* __restrict__ src, int64_t n, 
 // univariate.py:71-77 / _kernels.pyx:255-267
 template <typename KF>
 __device__ double block_median(const float* __restrict__ src, int64_t n, int64_t cnt, KF kf,
-                               SelShared& sh) {
+                               SelShared& sh, bool aligned4) {
     const int64_t k = (cnt - 1) >> 1;
     int64_t c_le;
-    const uint32_t lo = block_select(src, n, k, kf, sh, c_le);
+    const uint32_t lo = block_select(src, n, k, kf, sh, c_le, aligned4);
     const double lov = (double)kfloat(lo);
     if (cnt & 1) return lov;
     uint32_t hi = lo;
-    if (c_le < k + 2) hi = block_min_greater(src, n, lo, kf, sh);
+    if (c_le < k + 2) hi = block_min_greater(src, n, lo, kf, sh, aligned4);
     return (lov + (double)kfloat(hi)) / 2.0;
 }
 
@@ -202,10 +246,12 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SelectArgs a)
         __syncthreads();
         src = cache;
     }
-    const double med = block_median(src, n, n, KeyMed{}, sh);
+    // rows start 16-byte aligned when n % 4 == 0 (y is [Qb][jcount][n] floats)
+    const bool al = (n & 3) == 0;
+    const double med = block_median(src, n, n, KeyMed{}, sh, al);
     double depth;
     if (a.notion == 1) {
-        const double mad = block_median(src, n, n, KeyAbsDev{med}, sh);
+        const double mad = block_median(src, n, n, KeyAbsDev{med}, sh, al);
         const double dev = fabs(med);
         if (mad == 0.0) depth = (dev == 0.0) ? 1.0 : 0.0;
         else depth = 1.0 / (1.0 + dev / mad);
@@ -215,11 +261,18 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SelectArgs a)
             depth = 1.0;
         } else {
             int local = 0;
-            for (int64_t i = threadIdx.x; i < n; i += SEL_THREADS) local += ((double)src[i] - med > 0.0);
+            const int64_t n4 = al ? (n >> 2) : 0;
+            const float4* s4 = reinterpret_cast<const float4*>(src);
+            for (int64_t i = threadIdx.x; i < n4; i += SEL_THREADS) {
+                const float4 v = s4[i];
+                local += ((double)v.x - med > 0.0) + ((double)v.y - med > 0.0) + ((double)v.z - med > 0.0) +
+                         ((double)v.w - med > 0.0);
+            }
+            for (int64_t i = 4 * n4 + threadIdx.x; i < n; i += SEL_THREADS) local += ((double)src[i] - med > 0.0);
             const int npos = block_sum(local, sh);
             if (npos == 0) depth = 0.0;
             else {
-                const double madp = block_median(src, n, npos, KeyPosDev{med}, sh);
+                const double madp = block_median(src, n, npos, KeyPosDev{med}, sh, al);
                 depth = 1.0 / (1.0 + dev / madp);
             }
         }
@@ -316,7 +369,21 @@ __device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t 
         // 4 keys per 16-byte load; the row is 16-byte aligned, the tail is scalar
         const int n4 = n >> 2;
         const uint4* s4 = reinterpret_cast<const uint4*>(src);
-        for (int i = tid; i < n4; i += NT) {
+        // two 16-byte loads issued before the (memory-clobbering) histogram
+        // updates: bytes in flight matter when the row streams from HBM / L2
+        int i = tid;
+        for (; i + NT < n4; i += 2 * NT) {
+            const uint4 ka = s4[i], kb = s4[i + NT];
+            hist_add_if(h, ka.x, pmask, prefix, shift);
+            hist_add_if(h, ka.y, pmask, prefix, shift);
+            hist_add_if(h, ka.z, pmask, prefix, shift);
+            hist_add_if(h, ka.w, pmask, prefix, shift);
+            hist_add_if(h, kb.x, pmask, prefix, shift);
+            hist_add_if(h, kb.y, pmask, prefix, shift);
+            hist_add_if(h, kb.z, pmask, prefix, shift);
+            hist_add_if(h, kb.w, pmask, prefix, shift);
+        }
+        if (i < n4) {
             const uint4 k4 = s4[i];
             hist_add_if(h, k4.x, pmask, prefix, shift);
             hist_add_if(h, k4.y, pmask, prefix, shift);
@@ -398,23 +465,28 @@ __device__ double sel2_median(const uint32_t* __restrict__ keys, int n, uint32_t
     return (lov + (double)kfloat(hi)) / 2.0;
 }
 
-template <int NT>
+// GLB = false: the row's keys live in shared memory (n <= SEL2_MAX_N).
+// GLB = true: rows too long for shared memory; the keys are written over the
+// row's own projections in global memory (the row belongs to this CTA and is
+// dead after the select) and every pass streams them from L2 / HBM.
+template <int NT, bool GLB>
 __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
     extern __shared__ __align__(16) unsigned char sel2_raw[];
     Sel2Shared<NT>& sh = *reinterpret_cast<Sel2Shared<NT>*>(sel2_raw);
-    uint32_t* keys = reinterpret_cast<uint32_t*>(sel2_raw + ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)));
     const int jj = blockIdx.x;
     const int q = blockIdx.y;
     const int j = a.j0 + jj;
     if (j >= a.m) return;
     const int n = (int)a.n;
     const float* yrow = a.y + ((size_t)q * a.jcount + jj) * a.n;
+    uint32_t* keys = GLB ? const_cast<uint32_t*>(reinterpret_cast<const uint32_t*>(yrow))
+                         : reinterpret_cast<uint32_t*>(sel2_raw + ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)));
     uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
     if ((n & 3) == 0) {
         const float4* s4 = reinterpret_cast<const float4*>(yrow);
         uint4* k4 = reinterpret_cast<uint4*>(keys);
         for (int i = threadIdx.x; i < n / 4; i += NT) {
-            const float4 v = __ldg(s4 + i);
+            const float4 v = s4[i];
             const uint4 k = make_uint4(fkey(v.x), fkey(v.y), fkey(v.z), fkey(v.w));
             k4[i] = k;
             kmin = min(kmin, min(min(k.x, k.y), min(k.z, k.w)));
@@ -422,7 +494,7 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
         }
     } else {
         for (int i = threadIdx.x; i < n; i += NT) {
-            const uint32_t k = fkey(__ldg(yrow + i));
+            const uint32_t k = fkey(yrow[i]);
             keys[i] = k;
             kmin = min(kmin, k);
             kmax = max(kmax, k);
@@ -483,29 +555,33 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
     if (threadIdx.x == 0) a.depths[(size_t)q * a.m + j] = depth;
 }
 
-template <int NT>
+template <int NT, bool GLB>
 static cudaError_t launch_sel2(const SelectArgs& a, dim3 grid, cudaStream_t st) {
-    const size_t smem = ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)) + (size_t)a.n * 4;
-    cudaError_t e = cudaFuncSetAttribute(select_v2_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)) + (GLB ? 0 : (size_t)a.n * 4);
+    cudaError_t e = cudaFuncSetAttribute(select_v2_kernel<NT, GLB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return e;
-    select_v2_kernel<NT><<<grid, NT, smem, st>>>(a);
+    select_v2_kernel<NT, GLB><<<grid, NT, smem, st>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
     if (a.Qb == 0 || a.jcount == 0) return cudaSuccess;
+    dim3 grid((unsigned)a.jcount, (unsigned)a.Qb);
     if (a.n <= SEL2_MAX_N) {
-        dim3 grid((unsigned)a.jcount, (unsigned)a.Qb);
-        if (a.n <= SEL2_WIDE_N) return launch_sel2<256>(a, grid, st);
-        if (a.n <= SEL2_WIDER_N) return launch_sel2<512>(a, grid, st);
-        return launch_sel2<1024>(a, grid, st);
+        if (a.n <= SEL2_WIDE_N) return launch_sel2<256, false>(a, grid, st);
+        if (a.n <= SEL2_WIDER_N) return launch_sel2<512, false>(a, grid, st);
+        return launch_sel2<1024, false>(a, grid, st);
     }
+#ifndef RRS_SEL_LEGACY_GLOBAL
+    // (16-byte key loads: rows must start aligned, i.e. n % 4 == 0)
+    if ((a.n & 3) == 0 && a.n < ((int64_t)1 << 31)) return launch_sel2<1024, true>(a, grid, st);
+#endif
     size_t smem = (sizeof(SelShared) + 15) & ~size_t(15);
     if (a.n <= SEL_CACHE_MAX) smem += (size_t)a.n * sizeof(float);
     cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)a.jcount, (unsigned)a.Qb);
     select_kernel<<<grid, SEL_THREADS, smem, st>>>(a);
     return cudaGetLastError();
 }

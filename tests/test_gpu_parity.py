@@ -323,10 +323,11 @@ def test_tensor_layout_dims(b200, d):
 
 
 @pytest.mark.parametrize("notion", ["projection", "asym_projection"])
-@pytest.mark.parametrize("n", [53248, 60001])
+@pytest.mark.parametrize("n", [53248, 60000, 60001])
 def test_tier2_large_rows(b200, notion, n):
     """Rows at the shared-memory limit of the select kernel and past it (the
-    global-memory select path), Cauchy data, against the FP64 oracle."""
+    global-memory select paths: keys streamed in place for n % 4 == 0, the
+    11-bit legacy kernel otherwise), Cauchy data, against the FP64 oracle."""
     from oracle import oracle
     from paper_2506_08262_b200.synthetic import student_t
 
