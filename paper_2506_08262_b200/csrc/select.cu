@@ -311,6 +311,16 @@ __device__ __forceinline__ void hist_add_if(uint32_t* h, uint32_t key, uint32_t 
         : "memory");
 }
 
+// hist[key >> 24] += 1 (the first radix digit, counted while the keys are written)
+#ifdef RRS_SEL_NO_PREHIST
+constexpr bool SEL2_PRE = false;
+#else
+constexpr bool SEL2_PRE = true;
+#endif
+__device__ __forceinline__ void hist_top_add(uint32_t* h, uint32_t key) {
+    if (SEL2_PRE) asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(smem_u32(h + (key >> 24))) : "memory");
+}
+
 template <int NT>
 struct Sel2Shared {
     static constexpr int W = NT / 32;
@@ -349,7 +359,7 @@ __device__ __forceinline__ uint32_t block_reduce_add(uint32_t v, Sel2Shared<NT>&
 // after a pass was measured slower: the scratch costs occupancy.)
 template <int NT>
 __device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t k, uint32_t kmin, uint32_t kmax,
-                             Sel2Shared<NT>& sh, uint32_t& c_le) {
+                             Sel2Shared<NT>& sh, uint32_t& c_le, bool pre) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t* src = keys;
     const uint32_t diff = kmin ^ kmax;
@@ -362,8 +372,12 @@ __device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t 
     uint32_t pmask = shift + 8 >= 32 ? 0u : ~((1u << (shift + 8)) - 1u);
     uint32_t prefix = kmin & pmask;                // digits above `shift` are common
     uint32_t below_total = 0, last = 0;
+    // pre: the pass that wrote the keys already histogrammed their top digit
+    // (bits 24..31) into sh.hist; use it when the first pass starts there
+    bool skip_count = pre && shift == 24;
     for (;;) {
         uint32_t* h = sh.hist[warp % Sel2Shared<NT>::H];
+        if (!skip_count) {
         for (int b = lane; b < 256; b += 32) h[b] = 0u;
         __syncthreads();
         // 4 keys per 16-byte load; the row is 16-byte aligned, the tail is scalar
@@ -391,6 +405,8 @@ __device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t 
             hist_add_if(h, k4.w, pmask, prefix, shift);
         }
         for (int i = 4 * n4 + tid; i < n; i += NT) hist_add_if(h, src[i], pmask, prefix, shift);
+        }
+        skip_count = false;
         __syncthreads();
         // bin totals (thread b < 256 owns bin b), exclusive scan over the 256 bins
         uint32_t tot = 0;
@@ -454,10 +470,10 @@ __device__ uint32_t sel2_min_greater(const uint32_t* __restrict__ keys, int n, u
 // participating set must be larger than every participant (0xFFFFFFFF)
 template <int NT>
 __device__ double sel2_median(const uint32_t* __restrict__ keys, int n, uint32_t cnt, uint32_t kmin, uint32_t kmax,
-                              Sel2Shared<NT>& sh) {
+                              Sel2Shared<NT>& sh, bool pre) {
     const uint32_t k = (cnt - 1) >> 1;
     uint32_t c_le;
-    const uint32_t lo = sel2_kth(keys, n, k, kmin, kmax, sh, c_le);
+    const uint32_t lo = sel2_kth(keys, n, k, kmin, kmax, sh, c_le, pre);
     const double lov = (double)kfloat(lo);
     if (cnt & 1) return lov;
     uint32_t hi = lo;
@@ -481,6 +497,12 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
     const float* yrow = a.y + ((size_t)q * a.jcount + jj) * a.n;
     uint32_t* keys = GLB ? const_cast<uint32_t*>(reinterpret_cast<const uint32_t*>(yrow))
                          : reinterpret_cast<uint32_t*>(sel2_raw + ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)));
+    uint32_t* htop = sh.hist[(threadIdx.x >> 5) % Sel2Shared<NT>::H];
+    const auto clear_top = [&]() {
+        for (int b = threadIdx.x & 31; b < 256; b += 32) htop[b] = 0u;
+        __syncthreads();
+    };
+    clear_top();
     uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
     if ((n & 3) == 0) {
         const float4* s4 = reinterpret_cast<const float4*>(yrow);
@@ -489,6 +511,10 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
             const float4 v = s4[i];
             const uint4 k = make_uint4(fkey(v.x), fkey(v.y), fkey(v.z), fkey(v.w));
             k4[i] = k;
+            hist_top_add(htop, k.x);
+            hist_top_add(htop, k.y);
+            hist_top_add(htop, k.z);
+            hist_top_add(htop, k.w);
             kmin = min(kmin, min(min(k.x, k.y), min(k.z, k.w)));
             kmax = max(kmax, max(max(k.x, k.y), max(k.z, k.w)));
         }
@@ -496,6 +522,7 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
         for (int i = threadIdx.x; i < n; i += NT) {
             const uint32_t k = fkey(yrow[i]);
             keys[i] = k;
+            hist_top_add(htop, k);
             kmin = min(kmin, k);
             kmax = max(kmax, k);
         }
@@ -503,21 +530,23 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
     __syncthreads();
     kmin = block_reduce_min(kmin, sh);
     kmax = ~block_reduce_min(~kmax, sh);
-    const double med = sel2_median(keys, n, (uint32_t)n, kmin, kmax, sh);
+    const double med = sel2_median(keys, n, (uint32_t)n, kmin, kmax, sh, SEL2_PRE);
     double depth;
     if (a.notion == 1) {
         // MAD: keys of |y - med| (FP64 deviation, FP32 key), in place
+        clear_top();
         uint32_t dmin = 0xFFFFFFFFu, dmax = 0u;
         for (int i = threadIdx.x; i < n; i += NT) {
             const uint32_t k = fkey((float)fabs((double)kfloat(keys[i]) - med));
             keys[i] = k;
+            hist_top_add(htop, k);
             dmin = min(dmin, k);
             dmax = max(dmax, k);
         }
         __syncthreads();
         dmin = block_reduce_min(dmin, sh);
         dmax = ~block_reduce_min(~dmax, sh);
-        const double mad = sel2_median(keys, n, (uint32_t)n, dmin, dmax, sh);
+        const double mad = sel2_median(keys, n, (uint32_t)n, dmin, dmax, sh, SEL2_PRE);
         const double dev = fabs(med);
         if (mad == 0.0) depth = (dev == 0.0) ? 1.0 : 0.0;
         else depth = 1.0 / (1.0 + dev / mad);
@@ -527,6 +556,8 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
             depth = 1.0;
         } else {
             // positive deviations y - med > 0 keep their key, the rest sort last
+            // (the markers land in top bin 255 exactly as in a counting pass)
+            clear_top();
             uint32_t dmin = 0xFFFFFFFFu, dmax = 0u, npos = 0;
             for (int i = threadIdx.x; i < n; i += NT) {
                 const double t = (double)kfloat(keys[i]) - med;
@@ -538,6 +569,7 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
                     dmax = max(dmax, k);
                 }
                 keys[i] = k;
+                hist_top_add(htop, k);
             }
             __syncthreads();
             npos = block_reduce_add(npos, sh);
@@ -547,7 +579,7 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
             else {
                 // participants are the npos smallest keys; select within [dmin, dmax]
                 // (the 0xFFFFFFFF markers never match the prefix of a participant)
-                const double madp = sel2_median(keys, n, npos, dmin, dmax, sh);
+                const double madp = sel2_median(keys, n, npos, dmin, dmax, sh, SEL2_PRE);
                 depth = 1.0 / (1.0 + dev / madp);
             }
         }
