@@ -25,6 +25,7 @@ SOURCES = {  # file -> extra flags
     "contract.cu": [],
     "contract_tc.cu": [],
     "contract_tc2.cu": [],
+    "contract_tcw.cu": [],
     "select.cu": [],
     "engine.cu": [],
 }

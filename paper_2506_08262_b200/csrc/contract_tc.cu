@@ -48,6 +48,7 @@
 // Replaces _kernels.pyx:120-199 (projection) + 270-289 (halfspace_span).
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_common.cuh"
 
 #include <cuda_fp16.h>
 
@@ -100,326 +101,6 @@ struct TcSmem {
         (void)d;
     }
 };
-
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    // tcgen05 shared-memory descriptor: start>>4 [0,14), LBO>>4 [16,30),
-    // SBO>>4 [32,46), version 1 [46,48), base offset 0, layout SWIZZLE_NONE
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
-}
-
-// One (point tile, direction block) product: NS MMAs of K = 16 along the packed
-// split-product K axis, then the commit to the accumulator-full barrier, all
-// under one elect with immediate operand offsets (ptxas keeps the sequence on
-// the uniform datapath).
-//   acc: accumulator columns; aT: the block's A columns (K step i at +8 i)
-//   bd : descriptor of the tile's K step 0 (K step i at +4096 i bytes = +256 i)
-template <int NS>
-__device__ __forceinline__ void mma_tile_block(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar);
-
-template <>
-__device__ __forceinline__ void mma_tile_block<1>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<2>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<3>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<4>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<5>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<6>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<7>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "add.s64 b6, %2, 1536;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<8>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "add.s64 b6, %2, 1536;\n"
-                 "add.s64 b7, %2, 1792;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<9>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7, b8;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "add.s64 b6, %2, 1536;\n"
-                 "add.s64 b7, %2, 1792;\n"
-                 "add.s64 b8, %2, 2048;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], b8, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<10>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7, b8, b9;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "add.s64 b6, %2, 1536;\n"
-                 "add.s64 b7, %2, 1792;\n"
-                 "add.s64 b8, %2, 2048;\n"
-                 "add.s64 b9, %2, 2304;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], b8, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], b9, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<11>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7, b8, b9, b10;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "add.s64 b6, %2, 1536;\n"
-                 "add.s64 b7, %2, 1792;\n"
-                 "add.s64 b8, %2, 2048;\n"
-                 "add.s64 b9, %2, 2304;\n"
-                 "add.s64 b10, %2, 2560;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], b8, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], b9, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+80], b10, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<12>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7, b8, b9, b10, b11;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "add.s64 b6, %2, 1536;\n"
-                 "add.s64 b7, %2, 1792;\n"
-                 "add.s64 b8, %2, 2048;\n"
-                 "add.s64 b9, %2, 2304;\n"
-                 "add.s64 b10, %2, 2560;\n"
-                 "add.s64 b11, %2, 2816;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], b8, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], b9, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+80], b10, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+88], b11, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-// A direction block in the staging area (canonical K-major [kk/8][128][16 B]) ->
-// TMEM columns [aT, aT + 8 ns): one 128x256b copy (two 16-byte chunks) per K
-// step (once per unit, so a plain loop of elected copies).
-__device__ __forceinline__ void tmem_cp_dirblock(uint32_t aT, uint64_t sd, int ns) {
-    for (int i = 0; i < ns; ++i)
-        asm volatile(
-            "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-            "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"(aT + 8u * (uint32_t)i),
-            "l"(sd + 256ull * (uint64_t)i));
-}
-
-__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
-    asm volatile(
-        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load_elect(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void expect_tx_elect(uint64_t* bar, uint32_t bytes) {
-    asm volatile(
-        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(bytes)
-        : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// Wait with a suspend-time hint (for warps that run ahead of their consumer).
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAITS_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-        "@!p bra WAITS_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(1000000u)
-        : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ void named_bar(int id, int count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ uint32_t pack_half2(float lo_elem, float hi_elem) {
-    const __half2 h = __floats2half2_rn(lo_elem, hi_elem);
-    return *reinterpret_cast<const uint32_t*>(&h);
-}
 
 struct TcUnit {
     int q, grp, nbg;     // query, direction group, blocks in the group

@@ -1,0 +1,469 @@
+// contract_tcw.cu -- K2 on the tensor cores for 64 < d <= 256 ("wide"): the
+// FP16 hi/lo split contraction of contract_tc.cu with the coordinates taken in
+// slices of 64 (kernels.h tc_layout: full slices of 12 K steps + a last slice).
+//
+// Same arithmetic and result contract as contract_tc.cu (see there): a_il =
+// x_il - z_l in FP32, a power-of-two scale per point, a*s = ah + al (FP16),
+// u 2^15 = uh + ul, y s 2^15 ~= sum (uh al + ul ah + uh ah) accumulated in FP32
+// in TMEM; counts of y < 0 per direction in the epilogue.  The per-point scale
+// comes from the bound max_l |x_il| + max_l |z_l| >= max_l |a_il| (a dataset
+// property, precomputed) instead of the exact maximum, so a point's slices can
+// be converted one at a time; the split keeps 22 bits relative to each value
+// (FP16 lo has its own exponent), so the bound only moves the subnormal floor
+// (2^-25 of the scaled unit, i.e. ~2^-39 of the bound).
+//
+// Layout (M = 128 directions on TMEM lanes, N = 128 points, K = 16 per MMA):
+//   one direction block per unit (its A operand: 8 ns TMEM columns, 304 at
+//   d = 200, resident for the unit, loaded slice by slice through a 48 KB
+//   staging area); FP32 accumulator: two buffers of 128 columns when
+//   8 ns <= 256 (d <= 128), else one (the MMAs of the next tile wait for the
+//   epilogue to drain it);
+//   per (tile, slice): the raw FP32 rows [64 s, 64 s + 64) of the tile (TMA),
+//   converted into one 48 KB point-operand stage (2 stages), ns_s MMAs
+//   accumulating into the tile's accumulator.
+// Work units = (chunk of point tiles, query, direction block) with the chunk
+// slowest-varying: the CTAs running at the same time read the same tiles, so
+// the dataset (800 MB at config 5) streams from HBM about once per wave and
+// is re-read from L2 by the other units.
+// Warp roles as in contract_tc.cu: 0 direction-slice producer, 1 TMEM
+// allocator + MMA issuer, 2 raw-tile producer, 3-10 converters, 11-18 epilogue.
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+#include <cuda_fp16.h>
+
+namespace rrs {
+
+namespace {
+
+constexpr int W_CONV_WARP0 = 3;
+constexpr int W_CONV_WARPS = 8;
+constexpr int W_CONV_THREADS = W_CONV_WARPS * 32;
+constexpr int W_EPI_WARP0 = W_CONV_WARP0 + W_CONV_WARPS;
+constexpr int W_EPI_WARPS = 8;
+constexpr int W_EPI_THREADS = W_EPI_WARPS * 32;
+constexpr int W_THREADS = (W_EPI_WARP0 + W_EPI_WARPS) * 32;  // 608
+constexpr int W_MAXD = 256;
+constexpr int W_MD = 128;
+constexpr int W_NP = 128;
+constexpr int W_P_STAGES = 2;
+constexpr int W_R_MAX = 4;
+constexpr int W_STAGE = TC_SLICE_NS * 4096;  // one slice of a tile / of a direction block: 48 KB
+constexpr uint32_t W_TMEM_COLS = 512;
+constexpr uint32_t W_ACC = 128;
+constexpr int W_SMEM_LIMIT = 227 * 1024;
+
+struct WSmem {
+    int P, D, CNT, ZS, NZ, EXCL, BARS, TADDR, RAW, total, raw_stages;
+    static constexpr int NBARS = 2 * W_P_STAGES + 2 + 2 + 3 + 2 * W_R_MAX;
+    __host__ __device__ WSmem() {
+        P = 0;
+        D = P + W_P_STAGES * W_STAGE;
+        CNT = D + W_STAGE;                       // uint32 [128]
+        ZS = CNT + W_MD * 4;                     // float [2][256] (+ [2] max |z|)
+        NZ = ZS + 2 * W_MAXD * 4 + 16;           // uint32 [2][128] nonzero flags per point half
+        EXCL = NZ + 2 * W_NP * 4;                // uint32 [8][4]
+        BARS = EXCL + 8 * 4 * 4;
+        TADDR = BARS + NBARS * 8;
+        RAW = (TADDR + 16 + 1023) & ~1023;       // [64][128] floats per stage
+        const int room = W_SMEM_LIMIT - 1024 - RAW;
+        raw_stages = room / (TC_SLICE * W_NP * 4);
+        if (raw_stages > W_R_MAX) raw_stages = W_R_MAX;
+        total = RAW + raw_stages * TC_SLICE * W_NP * 4 + 1024;
+    }
+};
+
+struct WUnit {
+    int q, blk;
+    int64_t t0, t1;
+};
+
+__device__ __forceinline__ WUnit w_unit(const TcArgs& a, int64_t u) {
+    WUnit r;
+    const int64_t per_c = (int64_t)a.Qb * a.NB;
+    const int64_t c = u / per_c;
+    const int64_t rem = u - c * per_c;
+    r.q = (int)(rem / a.NB);
+    r.blk = (int)(rem - (int64_t)r.q * a.NB);
+    r.t0 = c * a.tiles_per_chunk;
+    r.t1 = r.t0 + a.tiles_per_chunk < a.tiles ? r.t0 + a.tiles_per_chunk : a.tiles;
+    return r;
+}
+
+__device__ __forceinline__ int slice_width(int d, int s) {
+    const int w = d - TC_SLICE * s;
+    return w < TC_SLICE ? w : TC_SLICE;
+}
+__device__ __forceinline__ int slice_ns(const TcLayout& L, int s) {
+    return s < L.full ? TC_SLICE_NS : L.ns - TC_SLICE_NS * L.full;
+}
+
+// ns MMAs (K = 16 each) of one slice into the accumulator; the first one
+// overwrites it when `first` (the tile's first slice), the rest accumulate.
+__device__ __forceinline__ void mma_slice(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, int ns, bool first) {
+    for (int i = 0; i < ns; ++i) {
+        const uint32_t en = (first && i == 0) ? 0u : 1u;
+        asm volatile(
+            "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(acc),
+            "r"(aT + 8u * (uint32_t)i), "l"(bd + 256ull * (uint64_t)i), "r"(idesc), "r"(en)
+            : "memory");
+    }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs a) {
+    extern __shared__ __align__(1024) unsigned char w_raw[];
+    unsigned char* sm = w_raw + ((1024u - (smem_u32(w_raw) & 1023u)) & 1023u);
+    const int d = a.d;
+    const TcLayout L = tc_layout(d);
+    const int S = L.full + 1;                 // slices
+    const bool dbl = 8 * L.ns <= 256;         // two accumulator buffers fit beside A
+    const uint32_t a_base = dbl ? 2 * W_ACC : W_ACC;
+    const WSmem lay;
+    unsigned char* sP = sm + lay.P;
+    unsigned char* sD = sm + lay.D;
+    uint32_t* sCnt = reinterpret_cast<uint32_t*>(sm + lay.CNT);
+    float* sZ = reinterpret_cast<float*>(sm + lay.ZS);
+    uint32_t* sNz = reinterpret_cast<uint32_t*>(sm + lay.NZ);
+    uint32_t* sExcl = reinterpret_cast<uint32_t*>(sm + lay.EXCL);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + lay.BARS);
+    uint64_t* pfull = &bars[0];
+    uint64_t* pempty = &bars[W_P_STAGES];
+    uint64_t* tfull = &bars[2 * W_P_STAGES];
+    uint64_t* tempty = &bars[2 * W_P_STAGES + 2];
+    uint64_t* dfull = &bars[2 * W_P_STAGES + 4];
+    uint64_t* dempty = &bars[2 * W_P_STAGES + 5];
+    uint64_t* udone = &bars[2 * W_P_STAGES + 6];
+    uint64_t* rfull = &bars[2 * W_P_STAGES + 7];
+    uint64_t* rempty = &bars[2 * W_P_STAGES + 7 + W_R_MAX];
+    uint32_t* sTaddr = reinterpret_cast<uint32_t*>(sm + lay.TADDR);
+    float* sRaw = reinterpret_cast<float*>(sm + lay.RAW);
+    const int RS = lay.raw_stages;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t units = (int64_t)a.Qb * a.NB * a.chunks;
+
+    for (int i = tid; i < W_P_STAGES * W_STAGE / 16; i += W_THREADS)
+        reinterpret_cast<uint4*>(sP)[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int c = tid; c < W_MD; c += W_THREADS) sCnt[c] = 0u;
+    if (tid < 2) sZ[2 * W_MAXD + tid] = 0.0f;
+    if (tid == 0) {
+        for (int s = 0; s < W_P_STAGES; ++s) {
+            mbar_init(&pfull[s], W_CONV_WARPS);
+            mbar_init(&pempty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], W_EPI_WARPS);
+        }
+        mbar_init(dfull, 1);
+        mbar_init(dempty, 1);
+        mbar_init(udone, 1);
+        for (int r = 0; r < W_R_MAX; ++r) {
+            mbar_init(&rfull[r], 1);
+            mbar_init(&rempty[r], W_CONV_WARPS);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(sTaddr)),
+                     "r"(W_TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (*sTaddr != 0u) __trap();
+    constexpr uint32_t tmem = 0u;
+
+    if (warp == 0) {
+        // ----------------------- producer: the unit's direction block, slice by slice
+        uint32_t g = 0;
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+            const WUnit w = w_unit(a, u);
+            const unsigned char* src = a.uop + ((size_t)w.q * a.NB + w.blk) * (size_t)L.ns * 4096;
+            for (int s = 0; s < S; ++s, ++g) {
+                const uint32_t bytes = (uint32_t)slice_ns(L, s) * 4096u;
+                if (g > 0) mbar_wait_sleep(dempty, (g - 1) & 1u);
+                expect_tx_elect(dfull, bytes);
+                tma_load_elect(sD, src + (size_t)s * W_STAGE, bytes, dfull);
+                __syncwarp();
+            }
+        }
+    } else if (warp == 1) {
+        // -------------------------------------------------------- MMA issuer
+        const uint32_t idesc = (1u << 4) | ((uint32_t)(W_NP >> 3) << 17) | ((uint32_t)(W_MD >> 4) << 24);
+        uint32_t it = 0, g = 0, gs = 0, gacc = 0;
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+            const WUnit w = w_unit(a, u);
+            for (int s = 0; s < S; ++s, ++g) {
+                mbar_wait_sleep(dfull, g & 1u);
+                if (s == 0 && it > 0) mbar_wait(udone, (it - 1) & 1u);  // previous unit's MMAs done with A
+                tc_fence_after();
+                tmem_cp_dirblock(tmem + a_base + 8u * TC_SLICE_NS * s, umma_desc(smem_u32(sD), 2048, 128),
+                                 slice_ns(L, s));
+                mma_commit_elect(dempty);
+            }
+            for (int64_t t = w.t0; t < w.t1; ++t, ++gacc) {
+                const uint32_t buf = dbl ? (gacc & 1u) : 0u;
+                if (dbl) {
+                    if (gacc >= 2) mbar_wait(&tempty[buf], ((gacc >> 1) - 1) & 1u);
+                } else if (gacc >= 1) {
+                    mbar_wait(&tempty[0], (gacc - 1) & 1u);
+                }
+                for (int s = 0; s < S; ++s, ++gs) {
+                    const uint32_t st = gs % W_P_STAGES;
+                    mbar_wait(&pfull[st], (gs / W_P_STAGES) & 1u);
+                    tc_fence_after();
+                    mma_slice(tmem + buf * W_ACC, tmem + a_base + 8u * TC_SLICE_NS * s,
+                              umma_desc(smem_u32(sP) + st * W_STAGE, 2048, 128), idesc, slice_ns(L, s), s == 0);
+                    mma_commit_elect(&pempty[st]);
+                }
+                mma_commit_elect(&tfull[buf]);
+            }
+            mma_commit_elect(udone);
+        }
+    } else if (warp == 2) {
+        // --------------------------------- producer: raw FP32 rows per (tile, slice)
+        uint32_t g = 0, rs = 0, rph = 0;
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+            const WUnit w = w_unit(a, u);
+            for (int64_t t = w.t0; t < w.t1; ++t) {
+                for (int s = 0; s < S; ++s, ++g) {
+                    const uint32_t bytes = (uint32_t)(slice_width(d, s) * W_NP * 4);
+                    if (g >= (uint32_t)RS) mbar_wait_sleep(&rempty[rs], rph ^ 1u);
+                    expect_tx_elect(&rfull[rs], bytes);
+                    tma_load_elect(sRaw + (size_t)rs * TC_SLICE * W_NP,
+                                   a.xb + ((size_t)t * d + (size_t)TC_SLICE * s) * W_NP, bytes, &rfull[rs]);
+                    __syncwarp();
+                    if (++rs == (uint32_t)RS) {
+                        rs = 0;
+                        rph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp < W_EPI_WARP0) {
+        // ---------------------------------- converters: (point r, 32-coordinate half h)
+        const int ct = tid - W_CONV_WARP0 * 32;
+        const int r = ct & (W_NP - 1);
+        const int h = ct >> 7;
+        uint32_t it = 0, gs = 0, rs = 0, rph = 0, gtile = 0;
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+            const WUnit w = w_unit(a, u);
+            float* zs = sZ + (it & 1u) * W_MAXD;
+            float zl = 0.0f;
+            for (int c = ct; c < W_MAXD; c += W_CONV_THREADS) {
+                const float z = c < d ? __ldg(a.zq + (size_t)w.q * d + c) : 0.0f;
+                zs[c] = z;
+                zl = fmaxf(zl, fabsf(z));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) zl = fmaxf(zl, __shfl_xor_sync(0xffffffffu, zl, o));
+            float* zmx = sZ + 2 * W_MAXD;  // [2] max |z| per unit parity (non-negative: int max order)
+            if (lane == 0) atomicMax(reinterpret_cast<int*>(zmx + (it & 1u)), __float_as_int(zl));
+            named_bar(2, W_CONV_THREADS);
+            const float zmax = zmx[it & 1u];
+            for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
+                const bool ok = t * W_NP + r < a.n;
+                // per-point scale 2^(14 - E), bound max|x_i| + max|z| < 2^E
+                const float bnd = (ok ? __ldg(a.xmax + t * W_NP + r) : 0.0f) + zmax;
+                float scale = 0.0f;
+                if (bnd > 0.0f) {
+                    int E = (int)((__float_as_uint(bnd) >> 23) & 0xFF) - 126;
+                    if (E < -100) E = -100;
+                    scale = __uint_as_float((uint32_t)(127 + 14 - E) << 23);
+                }
+                bool nz = false;
+                for (int s = 0; s < S; ++s, ++gs) {
+                    const int ds = slice_width(d, s);
+                    const int q16 = s < L.full ? 4 : L.q16;
+                    const int rem = s < L.full ? 0 : L.rem;
+                    const int main_chunks = 2 * q16;
+                    const uint32_t st = gs % W_P_STAGES;
+                    mbar_wait(&rfull[rs], rph);
+                    const float* X = sRaw + (size_t)rs * TC_SLICE * W_NP + 32 * h * W_NP + r;
+                    const float* zh = zs + TC_SLICE * s + 32 * h;
+                    float2 av[16];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        if (8 * (4 * h + c) < ds) {
+                            const float4 z0 = *reinterpret_cast<const float4*>(zh + 8 * c);
+                            const float4 z1 = *reinterpret_cast<const float4*>(zh + 8 * c + 4);
+                            const float2 nzv[4] = {make_float2(-z0.x, -z0.y), make_float2(-z0.z, -z0.w),
+                                                   make_float2(-z1.x, -z1.y), make_float2(-z1.z, -z1.w)};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                // rows past the slice width hold stale data: masked to x = 0
+                                // (z is 0 there too), never stored below
+                                const int c0 = 8 * (4 * h + c) + 2 * e;
+                                const float x0 = c0 < ds ? X[(8 * c + 2 * e) * W_NP] : 0.0f;
+                                const float x1 = c0 + 1 < ds ? X[(8 * c + 2 * e + 1) * W_NP] : 0.0f;
+                                const float2 v = __fadd2_rn(make_float2(x0, x1), nzv[e]);
+                                av[4 * c + e] = v;
+                                nz |= (v.x != 0.0f) | (v.y != 0.0f);
+                            }
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) av[4 * c + e] = make_float2(0.0f, 0.0f);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&rempty[rs]);
+                    if (++rs == (uint32_t)RS) {
+                        rs = 0;
+                        rph ^= 1u;
+                    }
+                    if (gs >= W_P_STAGES) mbar_wait(&pempty[st], ((gs / W_P_STAGES) - 1) & 1u);
+                    unsigned char* P = sP + st * W_STAGE + r * 16;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int cc = 4 * h + c;
+                        if (8 * cc >= ds) continue;
+                        uint32_t hw[4], lw[4];
+                        const float2 sc2 = make_float2(scale, scale);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 v = __fmul2_rn(av[4 * c + e], sc2);
+                            const __half2 hh = __floats2half2_rn(v.x, v.y);
+                            const float2 hf = __half22float2(hh);
+                            const float2 res = __fadd2_rn(v, make_float2(-hf.x, -hf.y));
+                            hw[e] = *reinterpret_cast<const uint32_t*>(&hh);
+                            lw[e] = pack_half2(res.x, res.y);
+                        }
+                        if (cc < main_chunks) {
+                            const uint4 hv = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                            *reinterpret_cast<uint4*>(P + cc * (W_NP * 16)) = hv;
+                            *reinterpret_cast<uint4*>(P + (main_chunks + cc) * (W_NP * 16)) =
+                                make_uint4(lw[0], lw[1], lw[2], lw[3]);
+                            *reinterpret_cast<uint4*>(P + (2 * main_chunks + cc) * (W_NP * 16)) = hv;
+                        } else {
+#pragma unroll 1
+                            for (int e = 0; e < 8; ++e) {
+                                const int cd = 8 * cc + e;
+                                if (cd >= ds) break;
+                                const int wi = e >> 1;
+                                const uint32_t hv = wi == 0 ? hw[0] : wi == 1 ? hw[1] : wi == 2 ? hw[2] : hw[3];
+                                const uint32_t lv = wi == 0 ? lw[0] : wi == 1 ? lw[1] : wi == 2 ? lw[2] : lw[3];
+                                const uint16_t hb = (uint16_t)((e & 1) ? (hv >> 16) : (hv & 0xFFFFu));
+                                const uint16_t lb = (uint16_t)((e & 1) ? (lv >> 16) : (lv & 0xFFFFu));
+                                int kk = 32 * q16 + cd;
+#pragma unroll
+                                for (int pr = 0; pr < 3; ++pr, kk += rem)
+                                    *reinterpret_cast<uint16_t*>(P + (kk >> 3) * (W_NP * 16) + (kk & 7) * 2) =
+                                        pr == 1 ? lb : hb;
+                            }
+                        }
+                    }
+                    if (s == S - 1) {
+                        // excluded points of the tile: coinciding rows (a = 0 in every slice)
+                        // and rows past n; written before this tile's last pfull
+                        uint32_t* nzs = sNz + (gtile & 1u) * W_NP;
+                        if (h == 1) nzs[r] = nz ? 1u : 0u;
+                        named_bar(2, W_CONV_THREADS);
+                        if (h == 0) {
+                            const bool keep = ok && (nz || nzs[r] != 0u);
+                            const uint32_t ex = __ballot_sync(0xffffffffu, !keep);
+                            if (lane == 0) sExcl[(gtile & 7u) * 4 + (r >> 5)] = ex;
+                        }
+                    }
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&pfull[st]);
+                }
+            }
+            // max |z| slot of this unit parity is reused two units later
+            named_bar(2, W_CONV_THREADS);
+            if (ct == 0) zmx[it & 1u] = 0.0f;
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int ct = tid - W_EPI_WARP0 * 32;
+        const int quarter = warp & 3;
+        const int half = (warp - W_EPI_WARP0) >> 2;
+        const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
+        uint32_t gacc = 0, gtile = 0;
+        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+            const WUnit w = w_unit(a, u);
+            uint32_t cnt = 0u, zsum = 0u;
+            for (int64_t t = w.t0; t < w.t1; ++t, ++gtile, ++gacc) {
+                const uint32_t buf = dbl ? (gacc & 1u) : 0u;
+                const uint32_t ph = dbl ? ((gacc >> 1) & 1u) : (gacc & 1u);
+                mbar_wait(&tfull[buf], ph);
+                tc_fence_after();
+                const uint32_t* ex = sExcl + (gtile & 7u) * 4;
+                const uint32_t keep0 = ~ex[2 * half], keep1 = ~ex[2 * half + 1];
+                const int64_t pad = (t + 1) * W_NP - a.n;
+                zsum += (uint32_t)(__popc(ex[0]) + __popc(ex[1]) + __popc(ex[2]) + __popc(ex[3])) -
+                        (uint32_t)(pad > 0 ? pad : 0);
+                const uint32_t tb = tmem + lane_base + buf * W_ACC + (uint32_t)(half * 64);
+                uint32_t y0[32], y1[32];
+                tmem_ld32(tb, y0);
+                tmem_ld32(tb + 32, y1);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[buf]);
+                uint32_t m0 = 0u, m1 = 0u;
+#pragma unroll
+                for (int j = 31; j >= 0; --j) {
+                    m0 = __funnelshift_l(y0[j], m0, 1);
+                    m1 = __funnelshift_l(y1[j], m1, 1);
+                }
+                cnt += __popc(m0 & keep0) + __popc(m1 & keep1);
+            }
+            atomicAdd(sCnt + 32 * quarter + lane, cnt);
+            named_bar(1, W_EPI_THREADS);
+            const int64_t r1 = w.t1 * W_NP < a.n ? w.t1 * W_NP : a.n;
+            const int valid = (int)(r1 - w.t0 * W_NP);
+            int* dst = a.counts + (size_t)w.q * a.mpad * 2;
+            const int j0 = w.blk * W_MD;
+            for (int c = ct; c < W_MD; c += W_EPI_THREADS) {
+                const int lt = (int)sCnt[c];
+                sCnt[c] = 0u;
+                if (j0 + c >= a.m) continue;
+                const int gtv = valid - (int)zsum - lt;
+                if (lt) atomicAdd(dst + 2 * (j0 + c) + 0, lt);
+                if (gtv) atomicAdd(dst + 2 * (j0 + c) + 1, gtv);
+            }
+            named_bar(1, W_EPI_THREADS);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(W_TMEM_COLS));
+}
+
+cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st) {
+    if (a.d <= TC_SLICE || a.d > W_MAXD || a.xmax == nullptr) return cudaErrorInvalidValue;
+    const WSmem lay;
+    if (lay.raw_stages < 2) return cudaErrorInvalidValue;
+    a.gb = 1;
+    a.groups = a.NB;
+    // chunks: >= 4 units per SM, and chunks short enough that a wave's tiles stay in L2
+    const int64_t base = (int64_t)a.Qb * a.NB;
+    int64_t chunks = (4ll * sms + base - 1) / base;
+    const int64_t l2_tiles = (int64_t)(48ll << 20) / ((int64_t)a.d * W_NP * 4);  // ~48 MB of rows per chunk
+    const int64_t min_chunks = (a.tiles + l2_tiles - 1) / (l2_tiles > 0 ? l2_tiles : 1);
+    if (chunks < min_chunks) chunks = min_chunks;
+    if (chunks < 1) chunks = 1;
+    if (chunks > a.tiles) chunks = a.tiles;
+    a.tiles_per_chunk = (a.tiles + chunks - 1) / chunks;
+    a.chunks = (int)((a.tiles + a.tiles_per_chunk - 1) / a.tiles_per_chunk);
+    a.raw_stages = lay.raw_stages;
+    const size_t smem = (size_t)lay.total;
+    cudaError_t e = cudaFuncSetAttribute(contract_tcw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t units = base * a.chunks;
+    if (units == 0) return cudaSuccess;
+    const int grid = (int)(units < sms ? units : sms);
+    contract_tcw_kernel<<<grid, W_THREADS, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace rrs

@@ -83,6 +83,7 @@ struct rrs_engine {
     int64_t ws_limit = 8ll << 30;
     // dataset
     DevBuf xb;
+    DevBuf xmax;  // [tiles * BM] max_l |x_il| (wide tensor path, 64 < d <= 256)
     int64_t n = 0;
     int d = 0;
     int64_t tiles = 0;
@@ -153,7 +154,7 @@ int validate_cfg(const rrs_config* c) {
 
 struct Plan {
     int m, mpad, MB, Qb;
-    bool tc;     // tensor-core FP16-split contraction (halfspace, d <= 64)
+    bool tc;     // tensor-core FP16-split contraction (halfspace, d <= 256; contract_tcw.cu for d > 64)
     int nb8;     // 128-direction blocks per query (tensor path operand, tc_block_bytes(d) each)
     int jchunk;  // direction blocks per store launch (projection notions)
     int tpu, chunks;
@@ -165,7 +166,7 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     p.MB = (m + BN - 1) / BN;
     p.mpad = p.MB * BN;
     p.nb8 = p.MB;
-    const bool tc_ok = notion == RRS_HALFSPACE && e->d <= 64;
+    const bool tc_ok = notion == RRS_HALFSPACE && e->d <= 256;
     p.tc = tc_ok && (e->contract_path >= 2 || (e->contract_path == 0 && e->n >= 4096));
     const int64_t d = e->d, n = e->n;
     int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * d * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 8 +
@@ -262,7 +263,10 @@ int contract_halfspace(rrs_engine* e, const Plan& p, int Qb) {
         t.NB = p.nb8;
         t.m = p.m;
         t.mpad = p.mpad;
-        if (e->contract_path == 3)
+        t.xmax = e->xmax.as<float>();
+        if (e->d > TC_SLICE)
+            CK(launch_contract_tcw(t, e->sms, e->stream));
+        else if (e->contract_path == 3)
             CK(launch_contract_tc2(t, e->sms, e->stream));
         else
             CK(launch_contract_tc(t, e->sms, e->stream));
@@ -471,7 +475,7 @@ int rrs_engine_destroy(rrs_engine* e) {
     if (!e) return RRS_OK;
     cudaSetDevice(e->device);
     cudaStreamSynchronize(e->stream);
-    for (DevBuf* b : {&e->xb, &e->zq, &e->u64, &e->u32, &e->uop, &e->counts, &e->depths, &e->y, &e->pole,
+    for (DevBuf* b : {&e->xb, &e->xmax, &e->zq, &e->u64, &e->u32, &e->uop, &e->counts, &e->depths, &e->y, &e->pole,
                       &e->reflv, &e->reflmode, &e->dmin, &e->bestcnt, &e->tmp_in, &e->tmp_out0,
                       &e->tmp_out1, &e->tmp_out2, &e->tmp_out3})
         b->release();
@@ -530,6 +534,10 @@ static int set_dataset_common(rrs_engine* e, const double* xdev, int64_t n, int3
     const int64_t tiles = (n + BM - 1) / BM;
     CK(e->xb.ensure((size_t)tiles * d * BM * 4));
     CK(launch_block_dataset(xdev, e->xb.as<float>(), n, d, tiles, e->stream));
+    if (d > TC_SLICE) {
+        CK(e->xmax.ensure((size_t)tiles * BM * 4));
+        CK(launch_row_absmax(e->xb.as<float>(), e->xmax.as<float>(), d, tiles, e->stream));
+    }
     e->n = n;
     e->d = d;
     e->tiles = tiles;

@@ -447,10 +447,9 @@ __global__ void __launch_bounds__(GV_THREADS, RRS_GEN_BLOCKS_PER_SM) cap_generat
             uint32_t w[4] = {0u, 0u, 0u, 0u};
             if (jj < nval) {
                 const double* row = val + jj * d;
-                if (8 * cc < 48 * L.q16) {
+                int p, c0;
+                if (tc_chunk_run(L, cc, p, c0)) {
                     // aligned part: one product p of 8 consecutive coordinates c0 .. c0 + 7
-                    const int st = cc >> 1, p = st / L.q16;
-                    const int c0 = 16 * (st - p * L.q16) + 8 * (cc & 1);
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         __half h0, l0, h1, l1;
@@ -684,6 +683,19 @@ __global__ void block_dataset_kernel(const double* __restrict__ x, float* __rest
     xb[idx] = (row < n) ? (float)x[row * d + c] : 0.0f;
 }
 
+// max_l |x_il| per (padded) row of the tile-blocked FP32 dataset (the wide
+// tensor path's per-point scale bound, contract_tcw.cu)
+__global__ void row_absmax_kernel(const float* __restrict__ xb, float* __restrict__ xmax, int d, int64_t tiles) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= tiles * BM) return;
+    const int64_t t = idx / BM;
+    const int i = (int)(idx % BM);
+    const float* row = xb + (size_t)t * d * BM + i;
+    float m = 0.0f;
+    for (int c = 0; c < d; ++c) m = fmaxf(m, fabsf(row[(size_t)c * BM]));
+    xmax[idx] = m;
+}
+
 __global__ void queries_to_f32_kernel(const double* __restrict__ z, float* __restrict__ zq,
                                       int64_t count) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -753,6 +765,13 @@ cudaError_t launch_block_dataset(const double* x, float* xb, int64_t n, int d, i
                                  cudaStream_t st) {
     int64_t total = tiles * d * BM;
     block_dataset_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(x, xb, n, d, tiles);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_absmax(const float* xb, float* xmax, int d, int64_t tiles, cudaStream_t st) {
+    const int64_t total = tiles * BM;
+    if (total == 0) return cudaSuccess;
+    row_absmax_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(xb, xmax, d, tiles);
     return cudaGetLastError();
 }
 

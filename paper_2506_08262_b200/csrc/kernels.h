@@ -76,7 +76,7 @@ struct ContractArgs {
 
 // Tensor-core (FP16 hi/lo split) halfspace contraction, contract_tc.cu.
 // Packed K layout of the split products, shared by the direction operand (A,
-// written by gen.cu) and the point operand (B, written by the kernel):
+// written by gen.cu) and the point operand (B, written by the kernels):
 //   d = 16 Q + r.  K steps s < 3Q (16 elements each): product p = s / Q of the
 //   coordinates 16 (s % Q) .. +15;  K steps 3Q .. 3Q + R - 1, R = ceil(3r/16):
 //   element e = kk - 48 Q < 3 r is product e / r of coordinate 16 Q + e % r,
@@ -84,43 +84,91 @@ struct ContractArgs {
 //   p = 2 else hi; B value: lo for p = 1 else hi), so
 //   sum_kk A[kk] B[kk] = sum_c (uh bh + uh bl + ul bh)  over ns = 3Q + R steps
 //   (d = 50: 10 MMAs instead of 3 x ceil(50/16) = 12).
+// d > 64 (contract_tcw.cu): coordinates in slices of 64; slice s < full is a
+// full slice (12 K steps: Q = 4, r = 0) at K steps [12 s, 12 s + 12), the last
+// slice (64 full .. d - 1, width 1..64) follows with its own Q / r.  For
+// d <= 64 (full = 0) this is the single-slice layout above.
 // Storage: canonical K-major, no swizzle: [kk / 8][row 128][8 fp16] per
 // 128-row block, i.e. ns * 4096 bytes per block.
 struct TcLayout {
-    int q16, rem, ns;
+    int q16, rem, ns;  // q16 / rem of the last slice (of d itself when d <= 64); ns: all slices
+    int full;          // full 64-coordinate slices before the last one
 };
+constexpr int TC_SLICE = 64;
+constexpr int TC_SLICE_NS = 12;
 __host__ __device__ inline TcLayout tc_layout(int d) {
     TcLayout L;
-    L.q16 = d / 16;
-    L.rem = d % 16;
-    L.ns = 3 * L.q16 + (3 * L.rem + 15) / 16;
+    L.full = d > 0 ? (d - 1) / TC_SLICE : 0;
+    const int dl = d - TC_SLICE * L.full;
+    L.q16 = dl / 16;
+    L.rem = dl % 16;
+    L.ns = TC_SLICE_NS * L.full + 3 * L.q16 + (3 * L.rem + 15) / 16;
     return L;
 }
 __host__ __device__ inline int tc_block_bytes(int d) { return tc_layout(d).ns * 4096; }
 // K position of product p of coordinate c
 __host__ __device__ inline int tc_pos(const TcLayout& L, int p, int c) {
-    return c < 16 * L.q16 ? 16 * (p * L.q16 + c / 16) + c % 16 : 48 * L.q16 + p * L.rem + (c - 16 * L.q16);
+    const int s = c / TC_SLICE;
+    if (s < L.full) {
+        const int cl = c - TC_SLICE * s;
+        return 16 * TC_SLICE_NS * s + 16 * (4 * p + cl / 16) + cl % 16;
+    }
+    const int base = 16 * TC_SLICE_NS * L.full;
+    const int cl = c - TC_SLICE * L.full;
+    return base + (cl < 16 * L.q16 ? 16 * (p * L.q16 + cl / 16) + cl % 16 : 48 * L.q16 + p * L.rem + (cl - 16 * L.q16));
 }
 // inverse: product p and coordinate c of K position kk (c = -1: zero padding)
 __host__ __device__ inline void tc_elem(const TcLayout& L, int kk, int& p, int& c) {
-    if (kk < 48 * L.q16) {
-        const int s = kk / 16;
-        p = s / L.q16;
-        c = 16 * (s % L.q16) + kk % 16;
+    const int s = kk / (16 * TC_SLICE_NS);
+    if (s < L.full) {
+        const int kl = kk - 16 * TC_SLICE_NS * s;
+        const int st = kl / 16;
+        p = st / 4;
+        c = TC_SLICE * s + 16 * (st % 4) + kl % 16;
+        return;
+    }
+    const int kl = kk - 16 * TC_SLICE_NS * L.full;
+    const int c0 = TC_SLICE * L.full;
+    if (kl < 48 * L.q16) {
+        const int st = kl / 16;
+        p = st / L.q16;
+        c = c0 + 16 * (st % L.q16) + kl % 16;
     } else {
-        const int e = kk - 48 * L.q16;
+        const int e = kl - 48 * L.q16;
         if (L.rem == 0 || e >= 3 * L.rem) {
             p = 0;
             c = -1;
         } else {
             p = e / L.rem;
-            c = 16 * L.q16 + e % L.rem;
+            c = c0 + 16 * L.q16 + e % L.rem;
         }
     }
+}
+// 16-byte chunk cc (K positions 8 cc .. 8 cc + 7): true when it holds product p
+// of the 8 consecutive coordinates c0 .. c0 + 7 (the aligned parts of slices)
+__host__ __device__ inline bool tc_chunk_run(const TcLayout& L, int cc, int& p, int& c0) {
+    const int kk = 8 * cc;
+    const int s = kk / (16 * TC_SLICE_NS);
+    int kl, q, cbase;
+    if (s < L.full) {
+        kl = kk - 16 * TC_SLICE_NS * s;
+        q = 4;
+        cbase = TC_SLICE * s;
+    } else {
+        kl = kk - 16 * TC_SLICE_NS * L.full;
+        q = L.q16;
+        cbase = TC_SLICE * L.full;
+        if (kl >= 48 * q) return false;
+    }
+    const int st = kl / 16;
+    p = st / q;
+    c0 = cbase + 16 * (st - p * q) + (kl % 16);
+    return true;
 }
 
 struct TcArgs {
     const float* xb;            // [T][d][128]
+    const float* xmax;          // [T * 128] max_l |x_il| (0 for padding rows); contract_tcw.cu only
     const float* zq;            // [Qb][d]
     const unsigned char* uop;   // [Qb][NB][tc_block_bytes(d)] direction operand
     int* counts;                // [Qb][mpad][2]
@@ -160,6 +208,8 @@ cudaError_t launch_contract_store(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
 cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st);
 cudaError_t launch_contract_tc2(TcArgs a, int sms, cudaStream_t st);  // 2-SM (cta_group::2) variant
+cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st);  // 64 < d <= 256 (contract_tcw.cu)
+cudaError_t launch_row_absmax(const float* xb, float* xmax, int d, int64_t tiles, cudaStream_t st);
 cudaError_t launch_pack_tc_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,
                                    cudaStream_t st);
 size_t contract_tc_smem_bytes();

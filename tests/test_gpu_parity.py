@@ -322,6 +322,45 @@ def test_tensor_layout_dims(b200, d):
         assert np.all(np.abs(cle - rle) <= T) and np.all(np.abs(cge - rge) <= T), d
 
 
+@pytest.mark.parametrize("d", [65, 72, 100, 128, 129, 150, 200, 256])
+def test_tensor_wide_dims(b200, d):
+    """The wide tensor path (contract_tcw.cu, 64 < d <= 256: 64-coordinate
+    slices, bound-based per-point scale, one or two accumulator buffers)
+    against FP64 within the tie zone and against the FFMA kernel, with a
+    near-duplicate query, an in-sample query (self tie) and heterogeneous
+    coordinate scales; n not a multiple of the tile, m not of the block."""
+    rng = np.random.default_rng(300 + d)
+    X = rng.standard_normal((4096 + 77, d)) * rng.uniform(0.1, 10.0, size=d)
+    U = rng.standard_normal((200, d))
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    data = b200.Dataset(X)
+    xn = np.linalg.norm(X, axis=1)
+    for z in (X[5], X[9] + 1e-4 * rng.standard_normal(d), np.full(d, 0.2)):
+        with contract_path(b200, "tensor"):
+            _, cle, cge = b200.evaluate_directions_counts(z, data, U)
+        with contract_path(b200, "ffma"):
+            _, fle, fge = b200.evaluate_directions_counts(z, data, U)
+        y = X @ U.T - (U @ z)[None, :]
+        T = (np.abs(y) < TIE_REL * np.maximum(xn, np.linalg.norm(z))[:, None]).sum(axis=0)
+        rle, rge = (y <= 0).sum(axis=0), (y >= 0).sum(axis=0)
+        assert np.all(np.abs(cle - rle) <= T) and np.all(np.abs(cge - rge) <= T), d
+        assert np.all(np.abs(cle - fle) <= T) and np.all(np.abs(cge - fge) <= T), d
+
+
+def test_tensor_wide_rrs_matches_ffma(b200):
+    """Full RRS at d = 200 (wide tensor path) against the FFMA path: identical
+    depths unless a count sits in the tie zone (Kendall tau over queries)."""
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((6000, 200))
+    data = b200.Dataset(X)
+    cfg = b200.RrsConfig(total_directions=600, refinements=3, shrink=0.9, notion="halfspace", seed=4)
+    with contract_path(b200, "tensor"):
+        dt = b200.depth_batch_arrays(X[:24], data, cfg)[0]
+    with contract_path(b200, "ffma"):
+        df = b200.depth_batch_arrays(X[:24], data, cfg)[0]
+    assert np.mean(dt == df) >= 0.9 and kendalltau(dt, df)[0] >= 0.95
+
+
 @pytest.mark.parametrize("notion", ["projection", "asym_projection"])
 @pytest.mark.parametrize("n", [53248, 60000, 60001])
 def test_tier2_large_rows(b200, notion, n):
