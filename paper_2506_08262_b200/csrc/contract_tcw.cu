@@ -38,18 +38,28 @@ namespace rrs {
 namespace {
 
 constexpr int W_CONV_WARP0 = 3;
-constexpr int W_CONV_WARPS = 8;
+#ifndef RRS_TCW_CONV_WARPS
+#define RRS_TCW_CONV_WARPS 8
+#endif
+constexpr int W_CONV_WARPS = RRS_TCW_CONV_WARPS;  // 128 points x (W_CONV_WARPS / 4) coordinate groups
+constexpr int W_GROUPS = W_CONV_WARPS / 4;            // threads per point
+constexpr int W_CPT = TC_SLICE / W_GROUPS;             // coordinates per converter thread (16 or 32)
+constexpr int W_CH = W_CPT / 8;                        // 8-coordinate chunks per thread
 constexpr int W_CONV_THREADS = W_CONV_WARPS * 32;
 constexpr int W_EPI_WARP0 = W_CONV_WARP0 + W_CONV_WARPS;
 constexpr int W_EPI_WARPS = 8;
 constexpr int W_EPI_THREADS = W_EPI_WARPS * 32;
-constexpr int W_THREADS = (W_EPI_WARP0 + W_EPI_WARPS) * 32;  // 608
+constexpr int W_THREADS = (W_EPI_WARP0 + W_EPI_WARPS) * 32;  // 864 with 16 converter warps
 constexpr int W_MAXD = 256;
 constexpr int W_MD = 128;
 constexpr int W_NP = 128;
 constexpr int W_P_STAGES = 2;
 constexpr int W_R_MAX = 4;
-constexpr int W_STAGE = TC_SLICE_NS * 4096;  // one slice of a tile / of a direction block: 48 KB
+constexpr int W_STAGE = TC_SLICE_NS * 4096;  // one slice of a tile: 48 KB
+#ifndef RRS_TCW_DSTEPS
+#define RRS_TCW_DSTEPS 4
+#endif
+constexpr int W_DSTEPS = RRS_TCW_DSTEPS;     // K steps of A per staging load (the rest of smem feeds the raw ring)
 constexpr uint32_t W_TMEM_COLS = 512;
 constexpr uint32_t W_ACC = 128;
 constexpr int W_SMEM_LIMIT = 227 * 1024;
@@ -60,10 +70,10 @@ struct WSmem {
     __host__ __device__ WSmem() {
         P = 0;
         D = P + W_P_STAGES * W_STAGE;
-        CNT = D + W_STAGE;                       // uint32 [128]
+        CNT = D + W_DSTEPS * 4096;               // uint32 [128]
         ZS = CNT + W_MD * 4;                     // float [2][256] (+ [2] max |z|)
-        NZ = ZS + 2 * W_MAXD * 4 + 16;           // uint32 [2][128] nonzero flags per point half
-        EXCL = NZ + 2 * W_NP * 4;                // uint32 [8][4]
+        NZ = ZS + 2 * W_MAXD * 4 + 16;           // uint32 [8][W_GROUPS][4] nonzero ballots (tile ring)
+        EXCL = NZ + 8 * W_GROUPS * 4 * 4;        // (unused)
         BARS = EXCL + 8 * 4 * 4;
         TADDR = BARS + NBARS * 8;
         RAW = (TADDR + 16 + 1023) & ~1023;       // [64][128] floats per stage
@@ -112,6 +122,86 @@ __device__ __forceinline__ void mma_slice(uint32_t acc, uint32_t aT, uint64_t bd
     }
 }
 
+// One converter thread's W_CPT coordinates [W_CPT h, W_CPT h + W_CPT) of a slice
+// of width ds: a = x - z (FP32, packed FADD2) into av; returns whether any a != 0.
+// FULL (ds = 64): no masking.  Otherwise rows past ds hold stale data from a
+// previous slice and are read as x = 0 (z is 0 there too; never stored).
+template <bool FULL>
+__device__ __forceinline__ bool w_load_slice(const float* X, const float* zh, int h, int ds, float2 (&av)[4 * W_CH]) {
+    uint32_t bits = 0u;  // OR of |a| bit patterns: nonzero iff some a != 0
+#pragma unroll
+    for (int c = 0; c < W_CH; ++c) {
+        if (FULL || 8 * (W_CH * h + c) < ds) {
+            const float4 z0 = *reinterpret_cast<const float4*>(zh + 8 * c);
+            const float4 z1 = *reinterpret_cast<const float4*>(zh + 8 * c + 4);
+            const float2 nzv[4] = {make_float2(-z0.x, -z0.y), make_float2(-z0.z, -z0.w), make_float2(-z1.x, -z1.y),
+                                   make_float2(-z1.z, -z1.w)};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int c0 = 8 * (W_CH * h + c) + 2 * e;
+                float x0 = X[(8 * c + 2 * e) * W_NP], x1 = X[(8 * c + 2 * e + 1) * W_NP];
+                if (!FULL) {
+                    x0 = c0 < ds ? x0 : 0.0f;
+                    x1 = c0 + 1 < ds ? x1 : 0.0f;
+                }
+                const float2 v = __fadd2_rn(make_float2(x0, x1), nzv[e]);
+                av[4 * c + e] = v;
+                bits |= (__float_as_uint(v.x) | __float_as_uint(v.y)) & 0x7FFFFFFFu;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) av[4 * c + e] = make_float2(0.0f, 0.0f);
+        }
+    }
+    return bits != 0u;
+}
+
+// Scale, FP16 hi/lo split and placement at the slice's packed K positions
+// (slice layout q16 / rem; FULL: q16 = 4, rem = 0, every chunk aligned).
+template <bool FULL>
+__device__ __forceinline__ void w_store_slice(unsigned char* P, const float2 (&av)[4 * W_CH], float scale, int h,
+                                              int ds, int q16, int rem) {
+    const int main_chunks = 2 * q16;
+    const float2 sc2 = make_float2(scale, scale);
+#pragma unroll
+    for (int c = 0; c < W_CH; ++c) {
+        const int cc = W_CH * h + c;
+        if (!FULL && 8 * cc >= ds) continue;
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 v = __fmul2_rn(av[4 * c + e], sc2);
+            const __half2 hh = __floats2half2_rn(v.x, v.y);
+            const float2 hf = __half22float2(hh);
+            const float2 res = __fadd2_rn(v, make_float2(-hf.x, -hf.y));
+            hw[e] = *reinterpret_cast<const uint32_t*>(&hh);
+            lw[e] = pack_half2(res.x, res.y);
+        }
+        if (FULL || cc < main_chunks) {
+            const int mc = FULL ? 8 : main_chunks;
+            const uint4 hv = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(P + cc * (W_NP * 16)) = hv;
+            *reinterpret_cast<uint4*>(P + (mc + cc) * (W_NP * 16)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            *reinterpret_cast<uint4*>(P + (2 * mc + cc) * (W_NP * 16)) = hv;
+        } else {
+#pragma unroll 1
+            for (int e = 0; e < 8; ++e) {
+                const int cd = 8 * cc + e;
+                if (cd >= ds) break;
+                const int wi = e >> 1;
+                const uint32_t hv = wi == 0 ? hw[0] : wi == 1 ? hw[1] : wi == 2 ? hw[2] : hw[3];
+                const uint32_t lv = wi == 0 ? lw[0] : wi == 1 ? lw[1] : wi == 2 ? lw[2] : lw[3];
+                const uint16_t hb = (uint16_t)((e & 1) ? (hv >> 16) : (hv & 0xFFFFu));
+                const uint16_t lb = (uint16_t)((e & 1) ? (lv >> 16) : (lv & 0xFFFFu));
+                int kk = 32 * q16 + cd;
+#pragma unroll
+                for (int pr = 0; pr < 3; ++pr, kk += rem)
+                    *reinterpret_cast<uint16_t*>(P + (kk >> 3) * (W_NP * 16) + (kk & 7) * 2) = pr == 1 ? lb : hb;
+            }
+        }
+    }
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs a) {
@@ -128,7 +218,6 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
     uint32_t* sCnt = reinterpret_cast<uint32_t*>(sm + lay.CNT);
     float* sZ = reinterpret_cast<float*>(sm + lay.ZS);
     uint32_t* sNz = reinterpret_cast<uint32_t*>(sm + lay.NZ);
-    uint32_t* sExcl = reinterpret_cast<uint32_t*>(sm + lay.EXCL);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + lay.BARS);
     uint64_t* pfull = &bars[0];
     uint64_t* pempty = &bars[W_P_STAGES];
@@ -186,13 +275,15 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
         for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
             const WUnit w = w_unit(a, u);
             const unsigned char* src = a.uop + ((size_t)w.q * a.NB + w.blk) * (size_t)L.ns * 4096;
-            for (int s = 0; s < S; ++s, ++g) {
-                const uint32_t bytes = (uint32_t)slice_ns(L, s) * 4096u;
-                if (g > 0) mbar_wait_sleep(dempty, (g - 1) & 1u);
-                expect_tx_elect(dfull, bytes);
-                tma_load_elect(sD, src + (size_t)s * W_STAGE, bytes, dfull);
-                __syncwarp();
-            }
+            for (int s = 0; s < S; ++s)
+                for (int k0 = 0; k0 < slice_ns(L, s); k0 += W_DSTEPS, ++g) {
+                    const int nst = slice_ns(L, s) - k0 < W_DSTEPS ? slice_ns(L, s) - k0 : W_DSTEPS;
+                    const uint32_t bytes = (uint32_t)nst * 4096u;
+                    if (g > 0) mbar_wait_sleep(dempty, (g - 1) & 1u);
+                    expect_tx_elect(dfull, bytes);
+                    tma_load_elect(sD, src + (size_t)(TC_SLICE_NS * s + k0) * 4096, bytes, dfull);
+                    __syncwarp();
+                }
         }
     } else if (warp == 1) {
         // -------------------------------------------------------- MMA issuer
@@ -200,14 +291,16 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
         uint32_t it = 0, g = 0, gs = 0, gacc = 0;
         for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
             const WUnit w = w_unit(a, u);
-            for (int s = 0; s < S; ++s, ++g) {
-                mbar_wait_sleep(dfull, g & 1u);
-                if (s == 0 && it > 0) mbar_wait(udone, (it - 1) & 1u);  // previous unit's MMAs done with A
-                tc_fence_after();
-                tmem_cp_dirblock(tmem + a_base + 8u * TC_SLICE_NS * s, umma_desc(smem_u32(sD), 2048, 128),
-                                 slice_ns(L, s));
-                mma_commit_elect(dempty);
-            }
+            for (int s = 0; s < S; ++s)
+                for (int k0 = 0; k0 < slice_ns(L, s); k0 += W_DSTEPS, ++g) {
+                    const int nst = slice_ns(L, s) - k0 < W_DSTEPS ? slice_ns(L, s) - k0 : W_DSTEPS;
+                    mbar_wait_sleep(dfull, g & 1u);
+                    if (s == 0 && k0 == 0 && it > 0) mbar_wait(udone, (it - 1) & 1u);  // previous unit done with A
+                    tc_fence_after();
+                    tmem_cp_dirblock(tmem + a_base + 8u * (TC_SLICE_NS * s + k0), umma_desc(smem_u32(sD), 2048, 128),
+                                     nst);
+                    mma_commit_elect(dempty);
+                }
             for (int64_t t = w.t0; t < w.t1; ++t, ++gacc) {
                 const uint32_t buf = dbl ? (gacc & 1u) : 0u;
                 if (dbl) {
@@ -251,7 +344,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
         // ---------------------------------- converters: (point r, 32-coordinate half h)
         const int ct = tid - W_CONV_WARP0 * 32;
         const int r = ct & (W_NP - 1);
-        const int h = ct >> 7;
+        const int h = ct >> 7;                      // coordinate group: [W_CPT h, W_CPT h + W_CPT) of a slice
         uint32_t it = 0, gs = 0, rs = 0, rph = 0, gtile = 0;
         for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
             const WUnit w = w_unit(a, u);
@@ -268,10 +361,15 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
             if (lane == 0) atomicMax(reinterpret_cast<int*>(zmx + (it & 1u)), __float_as_int(zl));
             named_bar(2, W_CONV_THREADS);
             const float zmax = zmx[it & 1u];
+            // the bound of the next tile's point is loaded one tile ahead (a global
+            // load on the critical path otherwise)
+            float xm_next = w.t0 * W_NP + r < a.n ? __ldg(a.xmax + w.t0 * W_NP + r) : 0.0f;
             for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
                 const bool ok = t * W_NP + r < a.n;
+                const float xm = xm_next;
+                if (t + 1 < w.t1) xm_next = (t + 1) * W_NP + r < a.n ? __ldg(a.xmax + (t + 1) * W_NP + r) : 0.0f;
                 // per-point scale 2^(14 - E), bound max|x_i| + max|z| < 2^E
-                const float bnd = (ok ? __ldg(a.xmax + t * W_NP + r) : 0.0f) + zmax;
+                const float bnd = (ok ? xm : 0.0f) + zmax;
                 float scale = 0.0f;
                 if (bnd > 0.0f) {
                     int E = (int)((__float_as_uint(bnd) >> 23) & 0xFF) - 126;
@@ -280,38 +378,13 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
                 }
                 bool nz = false;
                 for (int s = 0; s < S; ++s, ++gs) {
-                    const int ds = slice_width(d, s);
-                    const int q16 = s < L.full ? 4 : L.q16;
-                    const int rem = s < L.full ? 0 : L.rem;
-                    const int main_chunks = 2 * q16;
                     const uint32_t st = gs % W_P_STAGES;
                     mbar_wait(&rfull[rs], rph);
-                    const float* X = sRaw + (size_t)rs * TC_SLICE * W_NP + 32 * h * W_NP + r;
-                    const float* zh = zs + TC_SLICE * s + 32 * h;
-                    float2 av[16];
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        if (8 * (4 * h + c) < ds) {
-                            const float4 z0 = *reinterpret_cast<const float4*>(zh + 8 * c);
-                            const float4 z1 = *reinterpret_cast<const float4*>(zh + 8 * c + 4);
-                            const float2 nzv[4] = {make_float2(-z0.x, -z0.y), make_float2(-z0.z, -z0.w),
-                                                   make_float2(-z1.x, -z1.y), make_float2(-z1.z, -z1.w)};
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                // rows past the slice width hold stale data: masked to x = 0
-                                // (z is 0 there too), never stored below
-                                const int c0 = 8 * (4 * h + c) + 2 * e;
-                                const float x0 = c0 < ds ? X[(8 * c + 2 * e) * W_NP] : 0.0f;
-                                const float x1 = c0 + 1 < ds ? X[(8 * c + 2 * e + 1) * W_NP] : 0.0f;
-                                const float2 v = __fadd2_rn(make_float2(x0, x1), nzv[e]);
-                                av[4 * c + e] = v;
-                                nz |= (v.x != 0.0f) | (v.y != 0.0f);
-                            }
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) av[4 * c + e] = make_float2(0.0f, 0.0f);
-                        }
-                    }
+                    const float* X = sRaw + (size_t)rs * TC_SLICE * W_NP + W_CPT * h * W_NP + r;
+                    const float* zh = zs + TC_SLICE * s + W_CPT * h;
+                    float2 av[4 * W_CH];
+                    if (s < L.full) nz |= w_load_slice<true>(X, zh, h, TC_SLICE, av);
+                    else nz |= w_load_slice<false>(X, zh, h, d - TC_SLICE * L.full, av);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&rempty[rs]);
                     if (++rs == (uint32_t)RS) {
@@ -320,56 +393,15 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
                     }
                     if (gs >= W_P_STAGES) mbar_wait(&pempty[st], ((gs / W_P_STAGES) - 1) & 1u);
                     unsigned char* P = sP + st * W_STAGE + r * 16;
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const int cc = 4 * h + c;
-                        if (8 * cc >= ds) continue;
-                        uint32_t hw[4], lw[4];
-                        const float2 sc2 = make_float2(scale, scale);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float2 v = __fmul2_rn(av[4 * c + e], sc2);
-                            const __half2 hh = __floats2half2_rn(v.x, v.y);
-                            const float2 hf = __half22float2(hh);
-                            const float2 res = __fadd2_rn(v, make_float2(-hf.x, -hf.y));
-                            hw[e] = *reinterpret_cast<const uint32_t*>(&hh);
-                            lw[e] = pack_half2(res.x, res.y);
-                        }
-                        if (cc < main_chunks) {
-                            const uint4 hv = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-                            *reinterpret_cast<uint4*>(P + cc * (W_NP * 16)) = hv;
-                            *reinterpret_cast<uint4*>(P + (main_chunks + cc) * (W_NP * 16)) =
-                                make_uint4(lw[0], lw[1], lw[2], lw[3]);
-                            *reinterpret_cast<uint4*>(P + (2 * main_chunks + cc) * (W_NP * 16)) = hv;
-                        } else {
-#pragma unroll 1
-                            for (int e = 0; e < 8; ++e) {
-                                const int cd = 8 * cc + e;
-                                if (cd >= ds) break;
-                                const int wi = e >> 1;
-                                const uint32_t hv = wi == 0 ? hw[0] : wi == 1 ? hw[1] : wi == 2 ? hw[2] : hw[3];
-                                const uint32_t lv = wi == 0 ? lw[0] : wi == 1 ? lw[1] : wi == 2 ? lw[2] : lw[3];
-                                const uint16_t hb = (uint16_t)((e & 1) ? (hv >> 16) : (hv & 0xFFFFu));
-                                const uint16_t lb = (uint16_t)((e & 1) ? (lv >> 16) : (lv & 0xFFFFu));
-                                int kk = 32 * q16 + cd;
-#pragma unroll
-                                for (int pr = 0; pr < 3; ++pr, kk += rem)
-                                    *reinterpret_cast<uint16_t*>(P + (kk >> 3) * (W_NP * 16) + (kk & 7) * 2) =
-                                        pr == 1 ? lb : hb;
-                            }
-                        }
-                    }
+                    if (s < L.full) w_store_slice<true>(P, av, scale, h, TC_SLICE, 4, 0);
+                    else w_store_slice<false>(P, av, scale, h, d - TC_SLICE * L.full, L.q16, L.rem);
                     if (s == S - 1) {
-                        // excluded points of the tile: coinciding rows (a = 0 in every slice)
-                        // and rows past n; written before this tile's last pfull
-                        uint32_t* nzs = sNz + (gtile & 1u) * W_NP;
-                        if (h == 1) nzs[r] = nz ? 1u : 0u;
-                        named_bar(2, W_CONV_THREADS);
-                        if (h == 0) {
-                            const bool keep = ok && (nz || nzs[r] != 0u);
-                            const uint32_t ex = __ballot_sync(0xffffffffu, !keep);
-                            if (lane == 0) sExcl[(gtile & 7u) * 4 + (r >> 5)] = ex;
-                        }
+                        // counted points of the tile: valid rows with some a != 0 (coinciding
+                        // rows x = z give y = +-0 and are ties on both sides); one ballot word
+                        // per (warp's point group, coordinate group), read by the epilogue
+                        // after this tile's tfull (ordered by pfull -> MMA -> tfull)
+                        const uint32_t bal = __ballot_sync(0xffffffffu, ok && nz);
+                        if (lane == 0) sNz[((gtile & 7u) * W_GROUPS + h) * 4 + (r >> 5)] = bal;
                     }
                     fence_proxy_async();
                     __syncwarp();
@@ -395,25 +427,30 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
                 const uint32_t ph = dbl ? ((gacc >> 1) & 1u) : (gacc & 1u);
                 mbar_wait(&tfull[buf], ph);
                 tc_fence_after();
-                const uint32_t* ex = sExcl + (gtile & 7u) * 4;
-                const uint32_t keep0 = ~ex[2 * half], keep1 = ~ex[2 * half + 1];
-                const int64_t pad = (t + 1) * W_NP - a.n;
-                zsum += (uint32_t)(__popc(ex[0]) + __popc(ex[1]) + __popc(ex[2]) + __popc(ex[3])) -
-                        (uint32_t)(pad > 0 ? pad : 0);
+                uint32_t km[4] = {0u, 0u, 0u, 0u};
+                const uint32_t* nzw = sNz + (gtile & 7u) * W_GROUPS * 4;
+#pragma unroll
+                for (int g2 = 0; g2 < W_GROUPS; ++g2)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) km[k] |= nzw[g2 * 4 + k];
+                const uint32_t keep0 = km[2 * half], keep1 = km[2 * half + 1];
+                const int64_t rows = a.n - t * W_NP;
+                zsum += (uint32_t)(rows < W_NP ? rows : W_NP) -
+                        (uint32_t)(__popc(km[0]) + __popc(km[1]) + __popc(km[2]) + __popc(km[3]));
                 const uint32_t tb = tmem + lane_base + buf * W_ACC + (uint32_t)(half * 64);
-                uint32_t y0[32], y1[32];
-                tmem_ld32(tb, y0);
-                tmem_ld32(tb + 32, y1);
+                // two 32-column loads in turn (register budget of the 864-thread CTA)
+                uint32_t y[32], m0 = 0u, m1 = 0u;
+                tmem_ld32(tb, y);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 31; j >= 0; --j) m0 = __funnelshift_l(y[j], m0, 1);
+                tmem_ld32(tb + 32, y);
                 tmem_wait_ld();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[buf]);
-                uint32_t m0 = 0u, m1 = 0u;
 #pragma unroll
-                for (int j = 31; j >= 0; --j) {
-                    m0 = __funnelshift_l(y0[j], m0, 1);
-                    m1 = __funnelshift_l(y1[j], m1, 1);
-                }
+                for (int j = 31; j >= 0; --j) m1 = __funnelshift_l(y[j], m1, 1);
                 cnt += __popc(m0 & keep0) + __popc(m1 & keep1);
             }
             atomicAdd(sCnt + 32 * quarter + lane, cnt);
