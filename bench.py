@@ -306,13 +306,16 @@ def main():
     if tensor:
         # tcgen05 FP16-split path: executed tensor work = ns K-steps of M128 x N128 x K16 per
         # (128-point tile, 128-direction block); peak = measured dense bf16 (same rate as fp16)
-        L_ns = 3 * (d // 16) + (3 * (d % 16) + 15) // 16
+        full = (d - 1) // 64  # kernels.h tc_layout: 64-coordinate slices (d > 64: contract_tcw.cu)
+        dl = d - 64 * full
+        L_ns = 12 * full + 3 * (dl // 16) + (3 * (dl % 16) + 15) // 16
         tiles, blocks = -(-n // 128), -(-m // 128)
         exec_per_launch = 2.0 * 128 * 128 * 16 * L_ns * tiles * blocks * (B * args.steps * r / nl)
         executed = exec_per_launch / (avg_launch_ms / 1e3) / 1e12
         peak = peaks.get("bf16_tflops") or 2250.0
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": traffic, "kernel": "contract_tc_kernel",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "kernel": "contract_tc_kernel" if d <= 64 else "contract_tcw_kernel",
                     "peak_source": ("MEASURED_PEAKS.json bf16_tflops (dense, burst; fp16 runs at the bf16 rate)"
                                     if peaks.get("bf16_tflops") else "nominal 2.25 PFLOP/s dense fp16"),
                     "achieved_is": "algorithmic FLOPs 2*n*d*m per (query, refinement) / kernel time",
@@ -337,7 +340,8 @@ def main():
         sel_bytes = 4.0 * n * m * r * B * args.steps
         sel_gbs = sel_bytes / (select_ms / 1e3) / 1e9
         roofline = {"bound": "hbm", "achieved": sel_gbs, "peak": hbm, "unit": "GB/s", "frac": sel_gbs / hbm,
-                    "traffic": None, "kernel": "select_v2_kernel" if n <= 53248 else "select_kernel",
+                    "traffic": None, "kernel": "select_v2_kernel<256|512|1024, smem>" if n <= 52224
+                    else "select_v2_kernel<1024, global>" if n % 4 == 0 else "select_kernel",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "nominal 8 TB/s",
                     "achieved_is": "algorithmic bytes (the stored projections, 4 n per direction) / select time",
                     "kernel_share_of_step": select_ms / ms if ms else None,
