@@ -134,20 +134,44 @@ class ClockSampler:
 
 def cpu_baseline(X, notion, k, r, alpha, budget_queries=None):
     """The CPU port of the reference (oracle/, kind "port") on this host's
-    cores: a bounded sample of the same workload (one query per thread)."""
+    cores: a bounded sample of the same workload (one query per thread).  When
+    one full query is too long for the budget (config 5: 8e12 FLOP per query),
+    each sampled query runs r' < r refinements of the same m directions and the
+    rate is scaled by r'/r (RRS cost is linear in the refinements)."""
     from oracle import oracle
 
     oracle.build()
     cores = os.cpu_count() or 1
     q = budget_queries or max(cores, 1)
+    n, d = X.shape
+    m = -(-k // r)
+    r_s, m_s = cpu_sample_budget(n, d, k, r)
+    scale = (r * m) / (r_s * m_s)
     Z = X[:q]
     t0 = time.perf_counter()
-    oracle.depth_batch(Z, X, total_directions=k, refinements=r, shrink=alpha, notion=notion, seed=1,
+    oracle.depth_batch(Z, X, total_directions=m_s * r_s, refinements=r_s, shrink=alpha, notion=notion, seed=1,
                        threads=cores)
-    dt = time.perf_counter() - t0
+    dt = (time.perf_counter() - t0) * scale
+    part = "full RRS" if scale == 1 else f"{r_s} refinement(s) of {m_s} directions timed, scaled x{scale:g}"
     return {"value": q / dt, "unit": "query-depths/s", "cores": cores, "kind": "port",
-            "sample": f"{q} in-sample queries (rows 0..{q - 1}) of the same workload, full RRS, "
-                      f"{cores} threads, {dt:.1f} s wall"}
+            "sample": f"{q} in-sample queries (rows 0..{q - 1}) of the same workload, {part}, "
+                      f"{cores} threads, {dt / scale:.1f} s wall"}
+
+
+def cpu_sample_budget(n, d, k, r, flop_budget=2.5e11):
+    """(refinements, directions per refinement) a CPU sample query runs: the
+    full (r, m) unless one query exceeds the per-thread FLOP budget (~20-40 s
+    of scalar FP64 work); then fewer refinements, and below one refinement
+    fewer directions.  RRS cost is linear in both, so the rate is scaled by
+    (r m) / (r' m')."""
+    m = -(-k // r)
+    per_dir = 2.0 * n * d
+    if per_dir * m * r <= flop_budget:
+        return r, m
+    r_s = int(flop_budget // (per_dir * m))
+    if r_s >= 1:
+        return r_s, m
+    return 1, max(1, int(flop_budget // per_dir))
 
 
 def cpu_model() -> str:
@@ -172,16 +196,19 @@ def run_reference(args, wl):
 
     oracle.build()
     q = cores
+    r_s, m_s = cpu_sample_budget(n, d, k, r)
+    k_s = m_s * r_s
+    scale = (r * -(-k // r)) / k_s
     for _ in range(args.warmup):
-        oracle.depth_batch(X[:1], X, total_directions=k, refinements=r, shrink=alpha, notion=notion, seed=1,
+        oracle.depth_batch(X[:1], X, total_directions=k_s, refinements=r_s, shrink=alpha, notion=notion, seed=1,
                            threads=1)
     times = []
     for s in range(args.steps):
         Z = X[(s * q) % n:(s * q) % n + q]
         t0 = time.perf_counter()
-        oracle.depth_batch(Z, X, total_directions=k, refinements=r, shrink=alpha, notion=notion, seed=1,
+        oracle.depth_batch(Z, X, total_directions=k_s, refinements=r_s, shrink=alpha, notion=notion, seed=1,
                            threads=cores, q0=(s * q) % n)
-        times.append(time.perf_counter() - t0)
+        times.append((time.perf_counter() - t0) * scale)
     total = sum(times)
     value = q * args.steps / total
     line = {
@@ -193,7 +220,9 @@ def run_reference(args, wl):
                    "n_refinements": r, "sphcap_shrink": alpha, "queries_per_step": q},
         "cpu_baseline": {"value": value, "unit": "query-depths/s", "cores": cores, "kind": "port",
                          "sample": f"{q} queries per step ({cores} threads, {cpu_model()}); warm-up steps "
-                                   "run one query"},
+                                   "run one query" + ("" if scale == 1 else
+                                                      f"; {r_s} refinement(s) of {m_s} directions timed, "
+                                                      f"scaled x{scale:g}")},
         "e2e": {"value": value, "unit": "query-depths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
