@@ -106,10 +106,11 @@ int rrs_cap_directions_host(rrs_engine* e, const double* pole, int32_t d, double
 int rrs_philox4x32_host(rrs_engine* e, const uint32_t* ctr, int64_t N, uint32_t key0,
                         uint32_t key1, uint32_t* out);
 
-/* Halfspace contraction kernel: 0 = auto (tensor cores when d <= 64 and
+/* Halfspace contraction kernel: 0 = auto (tensor cores when d <= 256 and
  * n >= 4096), 1 = FP32 FFMA (contract.cu), 2 = tcgen05 FP16 hi/lo split with
- * FP32 accumulation (contract_tc.cu; halfspace, d <= 64), 3 = the same on SM
- * pairs with cta_group::2 MMAs (contract_tc2.cu). */
+ * FP32 accumulation (contract_tc.cu for d <= 64, contract_tcw.cu for
+ * 64 < d <= 256), 3 = the d <= 64 kernel on SM pairs with cta_group::2 MMAs
+ * (contract_tc2.cu; wider d takes contract_tcw.cu). */
 int rrs_engine_set_contract_path(rrs_engine* e, int32_t path);
 
 /* Diagnostics for the last batch: device time (ms) of each stage summed over
