@@ -12,6 +12,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:cont
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:cap_generate -c 1 -o gpurun_out/gen_c4 -f python scripts/profile_contract.py --q 1024 --r 1 > gpurun_out/ncu_gen.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:select -c 1 -o gpurun_out/select_c2 -f python scripts/profile_contract.py --notion projection --n 10000 --d 20 --q 256 --r 1 > gpurun_out/ncu_sel2.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:select -c 1 -o gpurun_out/select_c3 -f python scripts/profile_contract.py --notion asym_projection --n 50000 --d 50 --q 64 --r 1 > gpurun_out/ncu_sel3.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:contract_kernel -c 1 -o gpurun_out/contract_c5 -f python scripts/profile_contract.py --n 1000000 --d 200 --q 4 --r 1 > gpurun_out/ncu_c5.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:contract_tcw -c 1 -o gpurun_out/contract_tcw_c5 -f python scripts/profile_contract.py --n 1000000 --d 200 --q 16 --r 1 > gpurun_out/ncu_tcw_c5.log 2>&1
 for w in config2 config3 config5; do timeout 600 python bench.py --workload $w --steps 3 --warmup 3 > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; done
 echo done
