@@ -59,6 +59,19 @@ class ParallelConfig:
             raise ValueError("d_chunk must be >= 1")
 
 
+def _all_finite(x: np.ndarray) -> bool:
+    """np.isfinite(x).all(); large matrices use multi-threaded max / min
+    reductions (NaN propagates through both, +-inf shows up in one)."""
+    if x.size < (1 << 22):
+        return bool(np.isfinite(x).all())
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return bool(np.isfinite(x).all())
+    t = torch.from_numpy(x)
+    return bool(torch.isfinite(t.amax())) and bool(torch.isfinite(t.amin()))
+
+
 class Dataset:
     """An n x d row-major matrix of observations (64-bit floats, all finite)."""
 
@@ -68,7 +81,7 @@ class Dataset:
             x = x.reshape(1, -1)
         if x.ndim != 2 or x.shape[0] < 1 or x.shape[1] < 1:
             raise ValueError("dataset must be a non-empty 2-D matrix")
-        if not np.isfinite(x).all():
+        if not _all_finite(x):
             raise ValueError("dataset contains non-finite entries")
         self.x = x
         self._xt = None

@@ -527,6 +527,20 @@ int rrs_engine_stats(rrs_engine* e, rrs_stats* out) {
     return RRS_OK;
 }
 
+// 0 ok, else the first violated rule: 1 non-finite entry, 2 |x| > 1e38
+static int validate_device_dataset(rrs_engine* e, const double* xdev, int64_t count) {
+    CK(e->tmp_out0.ensure(16));
+    int* flag = e->tmp_out0.as<int>();
+    CK(cudaMemsetAsync(flag, 0, sizeof(int), e->stream));
+    CK(launch_validate_values(xdev, count, flag, e->stream));
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    if (h & 1) return fail(RRS_ERR_INVALID, "dataset contains non-finite entries");
+    if (h & 2) return fail(RRS_ERR_INVALID, "dataset entries exceed the FP32 contraction range (|x| > 1e38)");
+    return RRS_OK;
+}
+
 static int set_dataset_common(rrs_engine* e, const double* xdev, int64_t n, int32_t d) {
     if (d > MAX_D)
         return fail(RRS_ERR_INVALID, "dimension " + std::to_string(d) + " exceeds the supported maximum " +
@@ -547,14 +561,11 @@ static int set_dataset_common(rrs_engine* e, const double* xdev, int64_t n, int3
 int rrs_set_dataset_host(rrs_engine* e, const double* x, int64_t n, int32_t d) {
     if (!e || !x) return fail(RRS_ERR_INVALID, "null argument");
     if (n < 1 || d < 1) return fail(RRS_ERR_INVALID, "dataset must be a non-empty 2-D matrix");
-    for (int64_t i = 0; i < n * (int64_t)d; ++i) {
-        if (!std::isfinite(x[i])) return fail(RRS_ERR_INVALID, "dataset contains non-finite entries");
-        if (std::fabs(x[i]) > 1.0e38)
-            return fail(RRS_ERR_INVALID, "dataset entries exceed the FP32 contraction range (|x| > 1e38)");
-    }
     if (int rc = set_device(e)) return rc;
     CK(e->tmp_in.ensure((size_t)n * d * 8));
     CK(cudaMemcpyAsync(e->tmp_in.p, x, (size_t)n * d * 8, cudaMemcpyHostToDevice, e->stream));
+    // finiteness / FP32-range check on the device copy (the engine's dataset is untouched on failure)
+    if (int rc = validate_device_dataset(e, e->tmp_in.as<double>(), n * (int64_t)d)) return rc;
     int rc = set_dataset_common(e, e->tmp_in.as<double>(), n, d);
     if (rc) return rc;
     CK(cudaStreamSynchronize(e->stream));
@@ -565,6 +576,7 @@ int rrs_set_dataset_device(rrs_engine* e, const double* x_dev, int64_t n, int32_
     if (!e || !x_dev) return fail(RRS_ERR_INVALID, "null argument");
     if (n < 1 || d < 1) return fail(RRS_ERR_INVALID, "dataset must be a non-empty 2-D matrix");
     if (int rc = set_device(e)) return rc;
+    if (int rc = validate_device_dataset(e, x_dev, n * (int64_t)d)) return rc;
     return set_dataset_common(e, x_dev, n, d);
 }
 

@@ -683,6 +683,19 @@ __global__ void block_dataset_kernel(const double* __restrict__ x, float* __rest
     xb[idx] = (row < n) ? (float)x[row * d + c] : 0.0f;
 }
 
+// flag |= 1 for a non-finite entry, |= 2 for |x| > 1e38 (beyond the FP32
+// contraction range); grid-stride, one atomic per warp that found something
+__global__ void validate_values_kernel(const double* __restrict__ x, int64_t count, int* __restrict__ flag) {
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = x[i];
+        if (!isfinite(v)) bad |= 1;
+        else if (fabs(v) > 1.0e38) bad |= 2;
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (bad && (threadIdx.x & 31) == 0) atomicOr(flag, bad);
+}
+
 // max_l |x_il| per (padded) row of the tile-blocked FP32 dataset (the wide
 // tensor path's per-point scale bound, contract_tcw.cu)
 __global__ void row_absmax_kernel(const float* __restrict__ xb, float* __restrict__ xmax, int d, int64_t tiles) {
@@ -765,6 +778,14 @@ cudaError_t launch_block_dataset(const double* x, float* xb, int64_t n, int d, i
                                  cudaStream_t st) {
     int64_t total = tiles * d * BM;
     block_dataset_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(x, xb, n, d, tiles);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_validate_values(const double* x, int64_t count, int* flag, cudaStream_t st) {
+    if (count == 0) return cudaSuccess;
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    validate_values_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, count, flag);
     return cudaGetLastError();
 }
 

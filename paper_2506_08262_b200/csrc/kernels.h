@@ -209,6 +209,7 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
 cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st);
 cudaError_t launch_contract_tc2(TcArgs a, int sms, cudaStream_t st);  // 2-SM (cta_group::2) variant
 cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st);  // 64 < d <= 256 (contract_tcw.cu)
+cudaError_t launch_validate_values(const double* x, int64_t count, int* flag, cudaStream_t st);
 cudaError_t launch_row_absmax(const float* xb, float* xmax, int d, int64_t tiles, cudaStream_t st);
 cudaError_t launch_pack_tc_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,
                                    cudaStream_t st);

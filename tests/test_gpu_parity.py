@@ -408,3 +408,28 @@ def test_config5_shape(b200, notion):
         got = b200.evaluate_directions(z, data, U[:8], notion, b200.ParallelConfig(workers=1))
         ref = oracle.evaluate_directions(z, X, U[:8], notion)
         np.testing.assert_allclose(got, ref, rtol=DEPTH_RTOL, atol=0)
+
+
+def test_dataset_validation_on_device(b200):
+    """The C ABI validates datasets on the device copy (host and device entry
+    points): non-finite entries and |x| > 1e38 are refused with the
+    reference's message, and the engine keeps its previous dataset."""
+    import torch
+
+    eng = b200.engine()
+    rng = np.random.default_rng(2)
+    X = rng.standard_normal((5000, 4))
+    data = b200.Dataset(X)
+    U = rng.standard_normal((16, 4))
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    before = b200.evaluate_directions(X[3], data, U, "projection", b200.ParallelConfig(workers=1))
+    for bad, msg in ((np.nan, "non-finite"), (np.inf, "non-finite"), (3e38, "FP32 contraction range")):
+        Y = X.copy()
+        Y[4321, 2] = bad
+        with pytest.raises(ValueError, match=msg):
+            eng.set_dataset(Y, key=object())
+        with pytest.raises(ValueError, match=msg):
+            eng.set_dataset_device(torch.from_numpy(Y).cuda(), key=object())
+    eng.set_dataset(X, key=data._token)  # the previous dataset object is still served
+    after = b200.evaluate_directions(X[3], data, U, "projection", b200.ParallelConfig(workers=1))
+    np.testing.assert_array_equal(before, after)
