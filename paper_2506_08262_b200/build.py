@@ -26,6 +26,7 @@ SOURCES = {  # file -> extra flags
     "contract_tc.cu": [],
     "contract_tc2.cu": [],
     "contract_tcw.cu": [],
+    "contract_tcs.cu": [],
     "select.cu": [],
     "engine.cu": [],
 }

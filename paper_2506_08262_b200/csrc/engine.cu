@@ -155,6 +155,7 @@ int validate_cfg(const rrs_config* c) {
 struct Plan {
     int m, mpad, MB, Qb;
     bool tc;     // tensor-core FP16-split contraction (halfspace, d <= 256; contract_tcw.cu for d > 64)
+    bool tcs;    // tensor-core projection store (projection notions, d <= 50; contract_tcs.cu)
     int nb8;     // 128-direction blocks per query (tensor path operand, tc_block_bytes(d) each)
     int jchunk;  // direction blocks per store launch (projection notions)
     int tpu, chunks;
@@ -168,9 +169,13 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     p.nb8 = p.MB;
     const bool tc_ok = notion == RRS_HALFSPACE && e->d <= 256;
     p.tc = tc_ok && (e->contract_path >= 2 || (e->contract_path == 0 && e->n >= 4096));
+    const bool tcs_ok = notion != RRS_HALFSPACE && tc6_layout(e->d).ns <= 19;
+    // auto: the store is HBM-write bound at small d (y is n*m*4 bytes per query and
+    // refinement whatever computes it), the tensor store pays from d ~ 32 (config 3)
+    p.tcs = tcs_ok && (e->contract_path >= 2 || (e->contract_path == 0 && e->n >= 4096 && e->d >= 32));
     const int64_t d = e->d, n = e->n;
     int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * d * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 8 +
-                    d * 40 + 64 + (int64_t)p.nb8 * tc_block_bytes(e->d);
+                    d * 40 + 64 + (int64_t)p.nb8 * (p.tcs ? tc6_block_bytes(e->d) : tc_block_bytes(e->d));
     int64_t budget = e->ws_limit;
     int64_t qb = 4096;
     if (notion != RRS_HALFSPACE) {
@@ -217,7 +222,9 @@ int ensure_ws(rrs_engine* e, const Plan& p, int notion) {
     CK(e->reflmode.ensure(Qb * 4));
     CK(e->dmin.ensure(Qb * 8));
     CK(e->bestcnt.ensure(Qb * 8));
-    CK(e->uop.ensure(p.tc ? Qb * (size_t)p.nb8 * tc_block_bytes(e->d) : 16));
+    CK(e->uop.ensure(p.tc    ? Qb * (size_t)p.nb8 * tc_block_bytes(e->d)
+                     : p.tcs ? Qb * (size_t)p.nb8 * tc6_block_bytes(e->d)
+                             : 16));
     if (notion == RRS_HALFSPACE) {
         CK(e->counts.ensure(Qb * p.mpad * 2 * 4));
         CK(e->depths.ensure(8));
@@ -284,8 +291,26 @@ int univariate_from_store(rrs_engine* e, const Plan& p, int Qb, int notion) {
         const int jbn = (p.MB - jb0) < p.jchunk ? (p.MB - jb0) : p.jchunk;
         {
             Timer t(e, 1);
-            ContractArgs c = contract_args(e, p, Qb, jb0, jbn);
-            CK(launch_contract_store(c, e->stream));
+            if (p.tcs) {
+                TcsArgs c{};
+                c.xb = e->xb.as<float>();
+                c.zq = e->zq.as<float>();
+                c.uop = e->uop.as<unsigned char>();
+                c.y = e->y.as<float>();
+                c.n = e->n;
+                c.tiles = e->tiles;
+                c.d = e->d;
+                c.Qb = Qb;
+                c.NB = p.nb8;
+                c.m = p.m;
+                c.jb0 = jb0;
+                c.jbn = jbn;
+                CK(launch_contract_tcs(c, e->sms, e->stream));
+                e->stats.tensor_contract_launches++;
+            } else {
+                ContractArgs c = contract_args(e, p, Qb, jb0, jbn);
+                CK(launch_contract_store(c, e->stream));
+            }
             e->stats.kernel_launches++;
             e->stats.contract_launches++;
         }
@@ -363,7 +388,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 g.refl_mode = e->reflmode.as<int>();
                 g.refl_v = e->reflv.as<double>();
                 g.u64 = e->u64.as<double>();
-                g.u32 = p.tc ? nullptr : e->u32.as<float>();  // the tensor path reads uop only
+                g.u32 = (p.tc || p.tcs) ? nullptr : e->u32.as<float>();  // the tensor paths read uop only
                 g.seed = cfg->seed;
                 g.q0 = q0 + b0;
                 g.refinement = (uint32_t)l;
@@ -376,6 +401,11 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 g.NB = p.nb8;
                 CK(launch_cap_generate(g, e->stream));
                 e->stats.kernel_launches++;
+                if (p.tcs) {  // six-product operand of the projection store from the FP64 directions
+                    CK(launch_pack_tc6_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), Qb, m, p.nb8, d,
+                                               e->stream));
+                    e->stats.kernel_launches++;
+                }
             }
             if (cfg->notion == RRS_HALFSPACE) {
                 Timer t(e, 1);
@@ -644,6 +674,7 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
     CK(launch_queries_to_f32(e->tmp_in.as<double>(), e->zq.as<float>(), d, e->stream));
     CK(launch_pack_directions(e->u64.as<double>(), e->u32.as<float>(), 1, m, p.mpad, d, e->stream));
     if (p.tc) CK(launch_pack_tc_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
+    if (p.tcs) CK(launch_pack_tc6_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (notion == RRS_HALFSPACE) {
         CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.mpad * 2 * 4, e->stream));
         if (int rc = contract_halfspace(e, p, 1)) return rc;

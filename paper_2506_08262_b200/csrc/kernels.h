@@ -166,6 +166,60 @@ __host__ __device__ inline bool tc_chunk_run(const TcLayout& L, int cc, int& p, 
     return true;
 }
 
+// Six-product layout of the tensor-core projection STORE (contract_tcs.cu, d <= 64):
+// three-way FP16 split a s = ah + am + al, u 2^15 = uh + um + ul (33 bits each),
+// products p = 0..5: uh ah, uh am, um ah, uh al, ul ah, um am (the dropped
+// terms are ~2^-33), A value per product {h, h, m, h, l, m}, B value
+// {h, m, h, l, h, m}; packed along K like tc_layout with 6 products:
+// d = 16 Q + r, ns = 6 Q + ceil(6 r / 16).
+struct Tc6Layout {
+    int q16, rem, ns;
+};
+__host__ __device__ inline Tc6Layout tc6_layout(int d) {
+    Tc6Layout L;
+    L.q16 = d / 16;
+    L.rem = d % 16;
+    L.ns = 6 * L.q16 + (6 * L.rem + 15) / 16;
+    return L;
+}
+__host__ __device__ inline int tc6_block_bytes(int d) { return tc6_layout(d).ns * 4096; }
+__host__ __device__ inline int tc6_pos(const Tc6Layout& L, int p, int c) {
+    return c < 16 * L.q16 ? 16 * (p * L.q16 + c / 16) + c % 16 : 96 * L.q16 + p * L.rem + (c - 16 * L.q16);
+}
+__host__ __device__ inline void tc6_elem(const Tc6Layout& L, int kk, int& p, int& c) {
+    if (kk < 96 * L.q16) {
+        const int s = kk / 16;
+        p = s / L.q16;
+        c = 16 * (s % L.q16) + kk % 16;
+    } else {
+        const int e = kk - 96 * L.q16;
+        if (L.rem == 0 || e >= 6 * L.rem) {
+            p = 0;
+            c = -1;
+        } else {
+            p = e / L.rem;
+            c = 16 * L.q16 + e % L.rem;
+        }
+    }
+}
+// which split term (0 h, 1 m, 2 l) product p takes from A (directions) / B (points)
+__host__ __device__ inline int tc6_a_term(int p) { return (0x120100 >> (4 * p)) & 0xF; }
+__host__ __device__ inline int tc6_b_term(int p) { return (0x102010 >> (4 * p)) & 0xF; }
+
+struct TcsArgs {
+    const float* xb;            // [T][d][128]
+    const float* zq;            // [Qb][d]
+    const unsigned char* uop;   // [Qb][NB][tc6_block_bytes(d)] direction operand (six-product layout)
+    float* y;                   // [Qb][jbn * 128][n] projections y = <u, x - z> of the chunk
+    int64_t n;
+    int64_t tiles;
+    int d, Qb, NB, m;
+    int jb0, jbn;               // direction blocks of this chunk
+    // filled by launch_contract_tcs
+    int groups, chunks, raw_stages, gb;
+    int64_t tiles_per_chunk;
+};
+
 struct TcArgs {
     const float* xb;            // [T][d][128]
     const float* xmax;          // [T * 128] max_l |x_il| (0 for padding rows); contract_tcw.cu only
@@ -209,6 +263,9 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
 cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st);
 cudaError_t launch_contract_tc2(TcArgs a, int sms, cudaStream_t st);  // 2-SM (cta_group::2) variant
 cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st);  // 64 < d <= 256 (contract_tcw.cu)
+cudaError_t launch_contract_tcs(TcsArgs a, int sms, cudaStream_t st);  // projection store, d <= 64
+cudaError_t launch_pack_tc6_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,
+                                    cudaStream_t st);
 cudaError_t launch_validate_values(const double* x, int64_t count, int* flag, cudaStream_t st);
 cudaError_t launch_row_absmax(const float* xb, float* xmax, int d, int64_t tiles, cudaStream_t st);
 cudaError_t launch_pack_tc_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,

@@ -433,3 +433,46 @@ def test_dataset_validation_on_device(b200):
     eng.set_dataset(X, key=data._token)  # the previous dataset object is still served
     after = b200.evaluate_directions(X[3], data, U, "projection", b200.ParallelConfig(workers=1))
     np.testing.assert_array_equal(before, after)
+
+
+@pytest.mark.parametrize("notion", ["projection", "asym_projection"])
+@pytest.mark.parametrize("shape", [(10_000, 20, "gaussian"), (50_000, 50, "cauchy"), (53_248, 7, "cauchy"),
+                                   (4_097, 33, "gaussian"), (60_001, 48, "cauchy")])
+def test_tensor_store_projection_depths(b200, notion, shape):
+    """The tensor-core projection store (contract_tcs.cu, three-way FP16
+    split, six products): per-direction D_P / D_AP against the FP64 oracle to
+    the north_star's 1e-5 relative, at the config-2 / config-3 shapes (Cauchy
+    rows, where the two-term split failed), odd n and d, shared-memory and
+    global-memory select rows."""
+    from oracle import oracle
+    from paper_2506_08262_b200.synthetic import student_t, toeplitz_gaussian
+
+    n, d, dist = shape
+    X = toeplitz_gaussian(d, n, seed=1) if dist == "gaussian" else student_t(d, n, 1.0, seed=1)
+    rng = np.random.default_rng(n + d)
+    U = rng.standard_normal((24, d))
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    data = b200.Dataset(X)
+    cfg = b200.ParallelConfig(workers=1)
+    for z in (X[7], np.median(X, axis=0) + 0.05):
+        with contract_path(b200, "tensor"):
+            got = b200.evaluate_directions(z, data, U, notion, cfg)
+        ref = oracle.evaluate_directions(z, X, U, notion)
+        np.testing.assert_allclose(got, ref, rtol=DEPTH_RTOL, atol=0)
+
+
+def test_tensor_store_rrs_matches_ffma(b200):
+    """Full projection-depth RRS at the config-3 shape with the tensor store
+    against the FFMA store: per-query depths within the north_star tolerance
+    unless a pole update flipped on a near-tie (Kendall tau >= 0.99)."""
+    from paper_2506_08262_b200.synthetic import student_t
+
+    X = student_t(50, 20_000, 1.0, seed=0)
+    data = b200.Dataset(X)
+    cfg = b200.RrsConfig(total_directions=400, refinements=4, shrink=0.9, notion="asym_projection", seed=2)
+    with contract_path(b200, "tensor"):
+        dt = b200.depth_batch_arrays(X[:32], data, cfg)[0]
+    with contract_path(b200, "ffma"):
+        df = b200.depth_batch_arrays(X[:32], data, cfg)[0]
+    close = np.isclose(dt, df, rtol=1e-5, atol=0)
+    assert close.mean() >= 0.9 and kendalltau(dt, df)[0] >= 0.99
