@@ -335,21 +335,25 @@ def main():
     if tensor:
         # tcgen05 FP16-split path: executed tensor work = ns K-steps of M128 x N128 x K16 per
         # (128-point tile, 128-direction block); peak = measured dense bf16 (same rate as fp16)
-        full = (d - 1) // 64  # kernels.h tc_layout: 64-coordinate slices (d > 64: contract_tcw.cu)
-        dl = d - 64 * full
-        L_ns = 12 * full + 3 * (dl // 16) + (3 * (dl % 16) + 15) // 16
+        if notion == "halfspace":
+            full = (d - 1) // 64  # kernels.h tc_layout: 64-coordinate slices (d > 64: contract_tcw.cu)
+            dl = d - 64 * full
+            L_ns = 12 * full + 3 * (dl // 16) + (3 * (dl % 16) + 15) // 16
+            kname, nprod = ("contract_tc_kernel" if d <= 64 else "contract_tcw_kernel"), 3
+        else:  # projection store, kernels.h Tc6Layout (contract_tcs.cu)
+            L_ns = 6 * (d // 16) + (6 * (d % 16) + 15) // 16
+            kname, nprod = "contract_tcs_kernel", 6
         tiles, blocks = -(-n // 128), -(-m // 128)
         exec_per_launch = 2.0 * 128 * 128 * 16 * L_ns * tiles * blocks * (B * args.steps * r / nl)
         executed = exec_per_launch / (avg_launch_ms / 1e3) / 1e12
         peak = peaks.get("bf16_tflops") or 2250.0
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": traffic,
-                    "kernel": "contract_tc_kernel" if d <= 64 else "contract_tcw_kernel",
+                    "frac": achieved / peak, "traffic": traffic, "kernel": kname,
                     "peak_source": ("MEASURED_PEAKS.json bf16_tflops (dense, burst; fp16 runs at the bf16 rate)"
                                     if peaks.get("bf16_tflops") else "nominal 2.25 PFLOP/s dense fp16"),
                     "achieved_is": "algorithmic FLOPs 2*n*d*m per (query, refinement) / kernel time",
                     "executed_tensor_tflops": executed, "executed_frac": executed / peak,
-                    "executed_note": f"split-precision work: {L_ns} MMA K-steps (3 products, packed K) per "
+                    "executed_note": f"split-precision work: {L_ns} MMA K-steps ({nprod} products, packed K) per "
                                      f"128x128 tile, directions padded to {blocks * 128}",
                     "north_star_fp32": {"peak": FP32_NOMINAL_TFLOPS, "frac": achieved / FP32_NOMINAL_TFLOPS,
                                         "note": "north_star roofline: n*d*K FLOPs at the FP32 FFMA peak"}}
