@@ -476,3 +476,26 @@ def test_tensor_store_rrs_matches_ffma(b200):
         df = b200.depth_batch_arrays(X[:32], data, cfg)[0]
     close = np.isclose(dt, df, rtol=1e-5, atol=0)
     assert close.mean() >= 0.9 and kendalltau(dt, df)[0] >= 0.99
+
+
+@pytest.mark.parametrize("path", ["ffma", "tensor"])
+def test_store_direction_chunks_bitwise(b200, path):
+    """A workspace too small for a query's projections splits the store into
+    direction chunks (engine jchunk < blocks per query) and batches of one
+    query: depths bitwise equal to the unchunked run, for the FFMA and the
+    tensor-core store."""
+    from paper_2506_08262_b200.synthetic import toeplitz_gaussian
+
+    X = toeplitz_gaussian(40, 10_000, seed=2)
+    data = b200.Dataset(X)
+    cfg = b200.RrsConfig(total_directions=2000, refinements=2, shrink=0.9, notion="projection", seed=5)
+    eng = b200.engine()
+    with contract_path(b200, path):
+        full = b200.depth_batch_arrays(X[:6], data, cfg)
+        eng.set_workspace_limit(64 << 20)  # y budget 32 MB < 1024 x 10k x 4 per query
+        try:
+            chunked = b200.depth_batch_arrays(X[:6], data, cfg)
+        finally:
+            eng.set_workspace_limit(8 << 30)
+    np.testing.assert_array_equal(full[0], chunked[0])
+    np.testing.assert_array_equal(full[1], chunked[1])
