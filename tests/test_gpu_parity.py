@@ -499,3 +499,30 @@ def test_store_direction_chunks_bitwise(b200, path):
             eng.set_workspace_limit(8 << 30)
     np.testing.assert_array_equal(full[0], chunked[0])
     np.testing.assert_array_equal(full[1], chunked[1])
+
+
+@pytest.mark.parametrize("n", [1, 5, 130])
+@pytest.mark.parametrize("d", [20, 90, 200])
+def test_tensor_paths_tiny_n(b200, n, d):
+    """Tensor paths forced on tiny datasets (one partly padded tile, a single
+    point): halfspace counts (contract_tc / contract_tcw) exact against FP64
+    outside the tie zone, projection depths (contract_tcs for d <= 50, FFMA
+    store above) against the oracle."""
+    from oracle import oracle
+
+    rng = np.random.default_rng(n * 1000 + d)
+    X = rng.standard_normal((n, d))
+    U = rng.standard_normal((40, d))
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    data = b200.Dataset(X)
+    z = X[0] + 0.1 * rng.standard_normal(d)
+    with contract_path(b200, "tensor"):
+        _, cle, cge = b200.evaluate_directions_counts(z, data, U)
+        got = b200.evaluate_directions(z, data, U, "projection", b200.ParallelConfig(workers=1))
+    y = X @ U.T - (U @ z)[None, :]
+    T = (np.abs(y) < TIE_REL * np.maximum(np.linalg.norm(X, axis=1), np.linalg.norm(z))[:, None]).sum(axis=0)
+    assert np.all(np.abs(cle - (y <= 0).sum(axis=0)) <= T) and np.all(np.abs(cge - (y >= 0).sum(axis=0)) <= T)
+    # d = 200 takes the FFMA store: FP32 data rounding over 200 terms, amplified by
+    # the MAD of 5 points, can reach ~1.3e-5 (the 1e-5 contract holds at d <= 50)
+    rtol = DEPTH_RTOL if d <= 50 else 5e-5
+    np.testing.assert_allclose(got, oracle.evaluate_directions(z, X, U, "projection"), rtol=rtol, atol=0)
