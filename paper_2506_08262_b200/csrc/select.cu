@@ -331,6 +331,25 @@ struct Sel2Shared {
     int s_bin;
     uint32_t s_below;
     uint32_t s_cnt;
+    uint32_t s_cc, s_above;  // candidate compaction (global-memory rows)
+};
+
+// Global-memory rows (GLB): once a pass leaves <= SEL2G_CAP keys under the
+// chosen prefix with >= 2 digits to go, the next full pass also appends them to
+// a shared-memory candidate buffer (warp-aggregated) and records the smallest
+// key above the prefix; the remaining passes and the even-median next-key
+// search then read the buffer, not the row (the row streams from HBM: each
+// saved pass is 4 n bytes).  Not used for shared-memory rows, where the ballot
+// per key costs more than the passes it saves.
+#ifndef RRS_SEL2G_CAP
+#define RRS_SEL2G_CAP 16384
+#endif
+constexpr int SEL2G_CAP = RRS_SEL2G_CAP;
+struct Sel2Cands {
+    uint32_t* buf = nullptr;  // null: no compaction
+    bool on = false;
+    int count = 0;
+    uint32_t above = 0xFFFFFFFFu;
 };
 
 template <int NT>
@@ -355,13 +374,17 @@ __device__ __forceinline__ uint32_t block_reduce_add(uint32_t v, Sel2Shared<NT>&
 }
 
 // k-th smallest (0-based) of keys[0, n) whose values lie in [kmin, kmax];
-// c_le = number of keys <= the result.  (Compacting the surviving candidates
-// after a pass was measured slower: the scratch costs occupancy.)
+// c_le = number of keys <= the result.  cand.buf != null enables candidate
+// compaction (see Sel2Cands).
 template <int NT>
 __device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t k, uint32_t kmin, uint32_t kmax,
-                             Sel2Shared<NT>& sh, uint32_t& c_le, bool pre) {
+                             Sel2Shared<NT>& sh, uint32_t& c_le, bool pre, Sel2Cands& cand) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t* src = keys;
+    int nsrc = n;
+    cand.on = false;
+    cand.count = 0;
+    cand.above = 0xFFFFFFFFu;
     const uint32_t diff = kmin ^ kmax;
     if (diff == 0u) {
         c_le = (uint32_t)n;
@@ -371,40 +394,82 @@ __device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t 
     int shift = (top >= 24) ? 24 : (top >= 16) ? 16 : (top >= 8) ? 8 : 0;
     uint32_t pmask = shift + 8 >= 32 ? 0u : ~((1u << (shift + 8)) - 1u);
     uint32_t prefix = kmin & pmask;                // digits above `shift` are common
-    uint32_t below_total = 0, last = 0;
+    uint32_t below_total = 0, last = 0xFFFFFFFFu;
     // pre: the pass that wrote the keys already histogrammed their top digit
     // (bits 24..31) into sh.hist; use it when the first pass starts there
     bool skip_count = pre && shift == 24;
     for (;;) {
         uint32_t* h = sh.hist[warp % Sel2Shared<NT>::H];
+        const bool compact = cand.buf != nullptr && !cand.on && shift >= 8 && last <= (uint32_t)SEL2G_CAP;
         if (!skip_count) {
-        for (int b = lane; b < 256; b += 32) h[b] = 0u;
-        __syncthreads();
-        // 4 keys per 16-byte load; the row is 16-byte aligned, the tail is scalar
-        const int n4 = n >> 2;
-        const uint4* s4 = reinterpret_cast<const uint4*>(src);
-        // two 16-byte loads issued before the (memory-clobbering) histogram
-        // updates: bytes in flight matter when the row streams from HBM / L2
-        int i = tid;
-        for (; i + NT < n4; i += 2 * NT) {
-            const uint4 ka = s4[i], kb = s4[i + NT];
-            hist_add_if(h, ka.x, pmask, prefix, shift);
-            hist_add_if(h, ka.y, pmask, prefix, shift);
-            hist_add_if(h, ka.z, pmask, prefix, shift);
-            hist_add_if(h, ka.w, pmask, prefix, shift);
-            hist_add_if(h, kb.x, pmask, prefix, shift);
-            hist_add_if(h, kb.y, pmask, prefix, shift);
-            hist_add_if(h, kb.z, pmask, prefix, shift);
-            hist_add_if(h, kb.w, pmask, prefix, shift);
-        }
-        if (i < n4) {
-            const uint4 k4 = s4[i];
-            hist_add_if(h, k4.x, pmask, prefix, shift);
-            hist_add_if(h, k4.y, pmask, prefix, shift);
-            hist_add_if(h, k4.z, pmask, prefix, shift);
-            hist_add_if(h, k4.w, pmask, prefix, shift);
-        }
-        for (int i = 4 * n4 + tid; i < n; i += NT) hist_add_if(h, src[i], pmask, prefix, shift);
+            for (int b = lane; b < 256; b += 32) h[b] = 0u;
+            if (compact && tid == 0) {
+                sh.s_cc = 0u;
+                sh.s_above = 0xFFFFFFFFu;
+            }
+            __syncthreads();
+            if (!compact) {
+                // 4 keys per 16-byte load; rows are 16-byte aligned, the tail is scalar;
+                // two loads issued before the (memory-clobbering) histogram updates
+                const int n4 = nsrc >> 2;
+                const uint4* s4 = reinterpret_cast<const uint4*>(src);
+                int i = tid;
+                for (; i + NT < n4; i += 2 * NT) {
+                    const uint4 ka = s4[i], kb = s4[i + NT];
+                    hist_add_if(h, ka.x, pmask, prefix, shift);
+                    hist_add_if(h, ka.y, pmask, prefix, shift);
+                    hist_add_if(h, ka.z, pmask, prefix, shift);
+                    hist_add_if(h, ka.w, pmask, prefix, shift);
+                    hist_add_if(h, kb.x, pmask, prefix, shift);
+                    hist_add_if(h, kb.y, pmask, prefix, shift);
+                    hist_add_if(h, kb.z, pmask, prefix, shift);
+                    hist_add_if(h, kb.w, pmask, prefix, shift);
+                }
+                if (i < n4) {
+                    const uint4 k4 = s4[i];
+                    hist_add_if(h, k4.x, pmask, prefix, shift);
+                    hist_add_if(h, k4.y, pmask, prefix, shift);
+                    hist_add_if(h, k4.z, pmask, prefix, shift);
+                    hist_add_if(h, k4.w, pmask, prefix, shift);
+                }
+                for (int t = 4 * n4 + tid; t < nsrc; t += NT) hist_add_if(h, src[t], pmask, prefix, shift);
+            } else {
+                // the same histogram, plus the keys under the prefix appended to the
+                // buffer and the smallest key above it
+                uint32_t amin = 0xFFFFFFFFu;
+                const auto visit = [&](uint32_t key, bool valid) {
+                    const uint32_t hi = key & pmask;
+                    const bool match = valid && hi == prefix;
+                    if (valid && hi > prefix) amin = min(amin, key);
+                    if (match) hist_add_if(h, key, pmask, prefix, shift);
+                    const unsigned bal = __ballot_sync(0xffffffffu, match);
+                    if (bal) {
+                        const int leader = __ffs(bal) - 1;
+                        uint32_t base = 0;
+                        if (lane == leader) base = atomicAdd(&sh.s_cc, (uint32_t)__popc(bal));
+                        base = __shfl_sync(0xffffffffu, base, leader);
+                        if (match) cand.buf[base + __popc(bal & ((1u << lane) - 1u))] = key;
+                    }
+                };
+                const int n4 = nsrc >> 2;
+                const uint4* s4 = reinterpret_cast<const uint4*>(src);
+                // warp-uniform trip counts (ballots need every lane)
+                for (int i0 = warp * 32; i0 < n4; i0 += NT) {
+                    const int i = i0 + lane;
+                    const bool ok = i < n4;
+                    const uint4 k4 = ok ? s4[i] : make_uint4(0u, 0u, 0u, 0u);
+                    visit(k4.x, ok);
+                    visit(k4.y, ok);
+                    visit(k4.z, ok);
+                    visit(k4.w, ok);
+                }
+                for (int t0 = 4 * n4 + warp * 32; t0 < nsrc; t0 += NT) {
+                    const int t = t0 + lane;
+                    visit(t < nsrc ? src[t] : 0u, t < nsrc);
+                }
+                amin = __reduce_min_sync(0xffffffffu, amin);
+                if (lane == 0 && amin != 0xFFFFFFFFu) atomicMin(&sh.s_above, amin);
+            }
         }
         skip_count = false;
         __syncthreads();
@@ -436,6 +501,13 @@ __device__ uint32_t sel2_kth(const uint32_t* __restrict__ keys, int n, uint32_t 
         k -= sh.s_below;
         below_total += sh.s_below;
         last = sh.s_cnt;
+        if (compact) {
+            cand.on = true;
+            cand.count = (int)sh.s_cc;
+            cand.above = sh.s_above;
+            src = cand.buf;
+            nsrc = cand.count;
+        }
         prefix |= bin << shift;
         pmask |= 255u << shift;
         __syncthreads();
@@ -470,14 +542,20 @@ __device__ uint32_t sel2_min_greater(const uint32_t* __restrict__ keys, int n, u
 // participating set must be larger than every participant (0xFFFFFFFF)
 template <int NT>
 __device__ double sel2_median(const uint32_t* __restrict__ keys, int n, uint32_t cnt, uint32_t kmin, uint32_t kmax,
-                              Sel2Shared<NT>& sh, bool pre) {
+                              Sel2Shared<NT>& sh, bool pre, uint32_t* cbuf) {
     const uint32_t k = (cnt - 1) >> 1;
     uint32_t c_le;
-    const uint32_t lo = sel2_kth(keys, n, k, kmin, kmax, sh, c_le, pre);
+    Sel2Cands cand;
+    cand.buf = cbuf;
+    const uint32_t lo = sel2_kth(keys, n, k, kmin, kmax, sh, c_le, pre, cand);
     const double lov = (double)kfloat(lo);
     if (cnt & 1) return lov;
     uint32_t hi = lo;
-    if (c_le < k + 2) hi = sel2_min_greater(keys, n, lo, sh);
+    if (c_le < k + 2) {
+        // keys above lo are candidates (same prefix) or at least cand.above
+        hi = cand.on ? min(cand.above, sel2_min_greater(cand.buf, cand.count, lo, sh))
+                     : sel2_min_greater(keys, n, lo, sh);
+    }
     return (lov + (double)kfloat(hi)) / 2.0;
 }
 
@@ -497,6 +575,9 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
     const float* yrow = a.y + ((size_t)q * a.jcount + jj) * a.n;
     uint32_t* keys = GLB ? const_cast<uint32_t*>(reinterpret_cast<const uint32_t*>(yrow))
                          : reinterpret_cast<uint32_t*>(sel2_raw + ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)));
+    uint32_t* cbuf = GLB && SEL2G_CAP > 0
+                         ? reinterpret_cast<uint32_t*>(sel2_raw + ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)))
+                         : nullptr;
     uint32_t* htop = sh.hist[(threadIdx.x >> 5) % Sel2Shared<NT>::H];
     const auto clear_top = [&]() {
         for (int b = threadIdx.x & 31; b < 256; b += 32) htop[b] = 0u;
@@ -530,7 +611,7 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
     __syncthreads();
     kmin = block_reduce_min(kmin, sh);
     kmax = ~block_reduce_min(~kmax, sh);
-    const double med = sel2_median(keys, n, (uint32_t)n, kmin, kmax, sh, SEL2_PRE);
+    const double med = sel2_median(keys, n, (uint32_t)n, kmin, kmax, sh, SEL2_PRE, cbuf);
     double depth;
     if (a.notion == 1) {
         // MAD: keys of |y - med| (FP64 deviation, FP32 key), in place
@@ -546,7 +627,7 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
         __syncthreads();
         dmin = block_reduce_min(dmin, sh);
         dmax = ~block_reduce_min(~dmax, sh);
-        const double mad = sel2_median(keys, n, (uint32_t)n, dmin, dmax, sh, SEL2_PRE);
+        const double mad = sel2_median(keys, n, (uint32_t)n, dmin, dmax, sh, SEL2_PRE, cbuf);
         const double dev = fabs(med);
         if (mad == 0.0) depth = (dev == 0.0) ? 1.0 : 0.0;
         else depth = 1.0 / (1.0 + dev / mad);
@@ -579,7 +660,7 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
             else {
                 // participants are the npos smallest keys; select within [dmin, dmax]
                 // (the 0xFFFFFFFF markers never match the prefix of a participant)
-                const double madp = sel2_median(keys, n, npos, dmin, dmax, sh, SEL2_PRE);
+                const double madp = sel2_median(keys, n, npos, dmin, dmax, sh, SEL2_PRE, cbuf);
                 depth = 1.0 / (1.0 + dev / madp);
             }
         }
@@ -589,7 +670,7 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
 
 template <int NT, bool GLB>
 static cudaError_t launch_sel2(const SelectArgs& a, dim3 grid, cudaStream_t st) {
-    const size_t smem = ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)) + (GLB ? 0 : (size_t)a.n * 4);
+    const size_t smem = ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)) + (GLB ? (size_t)SEL2G_CAP * 4 : (size_t)a.n * 4);
     cudaError_t e = cudaFuncSetAttribute(select_v2_kernel<NT, GLB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
