@@ -116,3 +116,22 @@ def test_header_documents_reference_interfaces():
     for ref in ("optimizer.py:254-279", "optimizer.py:98-142", "directions.py:192-204",
                 "philox.py:27-65", "projection.py:44-75"):
         assert ref in text
+
+
+def test_packed_layouts_host_check(tmp_path):
+    """kernels.h's packed K layouts (tc_layout with 64-coordinate slices, the
+    six-product tc6_layout) checked on the host: compiled with g++ against the
+    CUDA headers from tests/cpp/layout_check.cpp (no GPU)."""
+    import shutil
+    import subprocess
+
+    cxx = shutil.which("g++")
+    inc = "/usr/local/cuda/include"
+    if cxx is None or not os.path.isdir(inc):
+        pytest.skip("g++ or the CUDA headers are not available")
+    here = os.path.dirname(os.path.abspath(__file__))
+    exe = tmp_path / "layout_check"
+    subprocess.run([cxx, "-std=c++17", "-O1", f"-I{inc}", "-I" + os.path.join(here, "..", "paper_2506_08262_b200", "csrc"),
+                    os.path.join(here, "cpp", "layout_check.cpp"), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.startswith("OK"), out.stdout
