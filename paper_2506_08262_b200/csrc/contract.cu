@@ -21,10 +21,21 @@
 
 namespace rrs {
 
-__host__ __device__ inline int stage_rows(int d) { return d < KC ? d : KC; }
+// d > STREAM_U_D: the direction block is streamed in K chunks next to the point
+// chunks (2 x 2 x 32 rows = 64 KB) instead of staying resident (d x 128 x 4 =
+// 100 KB at d = 200), so two CTAs fit an SM; the block is re-read from L2 per
+// point tile.
+#ifndef RRS_STREAM_U_D
+#define RRS_STREAM_U_D 128
+#endif
+constexpr int STREAM_U_D = RRS_STREAM_U_D;
+constexpr int KC_STREAM = 32;
+__host__ __device__ inline int chunk_rows(int d) { return d > STREAM_U_D ? KC_STREAM : KC; }
+__host__ __device__ inline int stage_rows(int d) { return d < chunk_rows(d) ? d : chunk_rows(d); }
 
 size_t contract_smem_bytes(int d) {
-    size_t us = (size_t)d * BN * sizeof(float);
+    const bool stream_u = d > STREAM_U_D;
+    size_t us = stream_u ? (size_t)2 * stage_rows(d) * BN * sizeof(float) : (size_t)d * BN * sizeof(float);
     size_t as = (size_t)2 * stage_rows(d) * BM * sizeof(float);
     size_t red = (size_t)8 * BN * 2 * sizeof(int);
     if (as < red) as = red;
@@ -36,8 +47,10 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int d = a.d;
     const int srows = stage_rows(d);
+    const int kchunk = chunk_rows(d);
+    const bool stream_u = d > STREAM_U_D;
     float* Us = reinterpret_cast<float*>(smem_raw);
-    float* As = Us + (size_t)d * BN;
+    float* As = Us + (stream_u ? (size_t)2 * srows * BN : (size_t)d * BN);
     size_t as_floats = (size_t)2 * srows * BM;
     if (as_floats < (size_t)8 * BN * 2) as_floats = (size_t)8 * BN * 2;
     float* zs = As + as_floats;
@@ -56,7 +69,7 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
     const int64_t t_begin = (int64_t)c * a.tiles_per_unit;
     int64_t t_end = t_begin + a.tiles_per_unit;
     if (t_end > a.tiles) t_end = a.tiles;
-    const int nkc = (d + KC - 1) / KC;
+    const int nkc = (d + kchunk - 1) / kchunk;
     const int S = (int)(t_end - t_begin) * nkc;
 
     if (tid == 0) {
@@ -67,27 +80,35 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
     }
     __syncthreads();
 
+    const float* ublk = a.u32 + ((size_t)q * a.MB + jb) * d * BN;
     auto issue = [&](int s) {
         const int64_t t = t_begin + s / nkc;
         const int kc = s % nkc;
-        const int k0 = kc * KC;
-        const int kcnt = (d - k0) < KC ? (d - k0) : KC;
+        const int k0 = kc * kchunk;
+        const int kcnt = (d - k0) < kchunk ? (d - k0) : kchunk;
         const uint32_t bytes = (uint32_t)kcnt * BM * sizeof(float);
         uint64_t* bar = &bars[1 + (s & 1)];
-        mbar_arrive_expect_tx(bar, bytes);
+        if (stream_u) {  // the matching rows of the direction block ride on the same barrier
+            mbar_arrive_expect_tx(bar, 2 * bytes);
+            bulk_g2s(Us + (size_t)(s & 1) * srows * BN, ublk + (size_t)k0 * BN, bytes, bar);
+        } else {
+            mbar_arrive_expect_tx(bar, bytes);
+        }
         bulk_g2s(As + (size_t)(s & 1) * srows * BM, a.xb + ((size_t)t * d + k0) * BM, bytes, bar);
     };
 
     if (tid == 0) {
-        const uint32_t ubytes = (uint32_t)d * BN * sizeof(float);
-        mbar_arrive_expect_tx(&bars[0], ubytes);
-        bulk_g2s(Us, a.u32 + ((size_t)q * a.MB + jb) * d * BN, ubytes, &bars[0]);
+        if (!stream_u) {
+            const uint32_t ubytes = (uint32_t)d * BN * sizeof(float);
+            mbar_arrive_expect_tx(&bars[0], ubytes);
+            bulk_g2s(Us, ublk, ubytes, &bars[0]);
+        }
         if (S > 0) issue(0);
         if (S > 1) issue(1);
     }
     for (int k = tid; k < d; k += CT_THREADS) zs[k] = a.zq[(size_t)q * d + k];
     __syncthreads();  // zs is read by every thread in the subtract pass
-    mbar_wait(&bars[0], 0);
+    if (!stream_u) mbar_wait(&bars[0], 0);
 
     float acc[8][8];
     unsigned lt[8], le[8];
@@ -101,8 +122,8 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
         const int st = s & 1;
         const int64_t t = t_begin + s / nkc;
         const int kc = s % nkc;
-        const int k0 = kc * KC;
-        const int kcnt = (d - k0) < KC ? (d - k0) : KC;
+        const int k0 = kc * kchunk;
+        const int kcnt = (d - k0) < kchunk ? (d - k0) : kchunk;
         float* Ab = As + (size_t)st * srows * BM;
         mbar_wait(&bars[1 + st], (uint32_t)((s >> 1) & 1));
 
@@ -146,7 +167,7 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
         }
 
         const float* Ap = Ab + ty * 4;
-        const float* Bp = Us + (size_t)k0 * BN + tx * 4;
+        const float* Bp = (stream_u ? Us + (size_t)st * srows * BN : Us + (size_t)k0 * BN) + tx * 4;
 #pragma unroll 2
         for (int k = 0; k < kcnt; ++k) {
             const float4 a0 = *reinterpret_cast<const float4*>(Ap + k * BM);
