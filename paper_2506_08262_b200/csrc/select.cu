@@ -295,7 +295,10 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SelectArgs a)
 constexpr int64_t SEL2_MAX_N = 53248;  // 208 KB of keys
 // 256 threads for rows up to SEL2_WIDE_N, 512 up to SEL2_WIDER_N, 1024 above
 // (one CTA per SM at n = 50k: more warps in flight for the latency-bound passes)
-constexpr int64_t SEL2_WIDE_N = 16384;
+#ifndef RRS_SEL2_WIDE_N
+#define RRS_SEL2_WIDE_N 16384
+#endif
+constexpr int64_t SEL2_WIDE_N = RRS_SEL2_WIDE_N;
 #ifndef RRS_SEL2_WIDER_N
 #define RRS_SEL2_WIDER_N 24576
 #endif
