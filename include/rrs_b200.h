@@ -70,9 +70,15 @@ int rrs_engine_synchronize(rrs_engine* e);
 int rrs_engine_set_workspace_limit(rrs_engine* e, int64_t bytes);
 
 /* Dataset(rows) -- projection.py:44-75.  x is n x d row-major FP64, finite;
- * stored on device as FP32 in tile-blocked layout. */
+ * stored on device as FP32 in tile-blocked layout.
+ * The entries are checked on the device copy: RRS_ERR_INVALID with
+ * "dataset contains non-finite entries" (projection.py's message) or "... exceed
+ * the FP32 contraction range (|x| > 1e38)"; the engine keeps its previous
+ * dataset on failure.  For 64 < d <= 256 the per-point bound max_l |x_il| of
+ * the wide tensor kernel is precomputed here. */
 int rrs_set_dataset_host(rrs_engine* e, const double* x, int64_t n, int32_t d);
-/* Same from a device FP64 buffer (n x d row-major), stream-ordered. */
+/* Same from a device FP64 buffer (n x d row-major), stream-ordered (the
+ * validation synchronises the engine stream once). */
 int rrs_set_dataset_device(rrs_engine* e, const double* x_dev, int64_t n, int32_t d);
 
 /* depth_batch(queries, data, cfg) -- optimizer.py:254-279, with
