@@ -386,14 +386,16 @@ def main():
         from paper_2506_08262_b200.distributed import depth_sharded
         from paper_2506_08262_b200.solver import depth_batch_arrays
 
-        Zh = [inputs[args.warmup + i][1].cpu().numpy() for i in range(args.steps)]
+        # host inputs in pinned memory (the e2e contract: H2D from pinned host buffers)
+        Xh = torch.from_numpy(X).pin_memory().numpy()
+        Zh = [inputs[args.warmup + i][1].cpu().pin_memory().numpy() for i in range(args.steps)]
         q0s = [inputs[args.warmup + i][0] for i in range(args.steps)]
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for i in range(args.steps):
-            data = rrs.Dataset(X)  # a fresh Dataset: validated and uploaded every call
+            data = rrs.Dataset(Xh)  # a fresh Dataset: validated and uploaded every call
             if world > 1:
                 Zall = np.concatenate([Zh[i]] * world)  # every rank passes the full list; shards by rank
                 depth_sharded(Zall, data, cfg)
