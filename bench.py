@@ -238,6 +238,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="queries per GPU per step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process group for N>1 (gloo: ranks may share one GPU, the single-GPU rehearsal)")
     ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "tensor2"],
                     help="halfspace contraction kernel (auto: the library's choice)")
     args = ap.parse_args()
@@ -254,9 +256,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":
+        local = local % torch.cuda.device_count()  # ranks may share a GPU
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    red_dev = "cuda" if args.dist_backend == "nccl" else "cpu"  # timing max-reduction
     notion, n, d, k, r, alpha, distn, B = WORKLOADS[wl]
     if args.batch:
         B = args.batch
@@ -317,7 +325,7 @@ def main():
     clk = clocks.stop()
     eng.enable_timing(False)
     ms = sum(a.elapsed_time(b) for a, b in ev)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -405,7 +413,7 @@ def main():
         if world > 1:
             dist.barrier()
         e2e_s = time.perf_counter() - t0
-        tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": world * B * args.steps / float(tt.item()), "unit": "query-depths/s",
@@ -427,6 +435,7 @@ def main():
             "config": {"workload": WORKLOAD_TEXT[wl], "notion": notion, "n": n, "d": d, "NRandom": k,
                        "n_refinements": r, "directions_per_refinement": m, "sphcap_shrink": alpha,
                        "queries_per_gpu_per_step": B, "global_batch": B * world, "parallelism": f"query-shard x{world}",
+                       "dist_backend": args.dist_backend if world > 1 else None,
                        "l2": "flushed between timed steps (256 MiB write)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,

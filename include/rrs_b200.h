@@ -107,6 +107,38 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
 int rrs_cap_directions_host(rrs_engine* e, const double* pole, int32_t d, double eps, int32_t m,
                             uint64_t seed, uint32_t refinement, uint32_t query, double* U);
 
+/* random_sphere_pole(cap, SubStream(seed, refinement, query, index_base)) and
+ * generate_batch rows from Philox direction index index_base on --
+ * directions.py:185-189, _cap_rows(..., index_base) :167-182. */
+int rrs_cap_directions_at_host(rrs_engine* e, const double* pole, int32_t d, double eps, int32_t m,
+                               uint64_t seed, uint32_t refinement, uint32_t query, uint32_t index_base,
+                               double* U);
+
+/* _unit_rows(seed, refinement, query, m, dim, v_base, index_base) --
+ * directions.py:113-135 (random_sphere(d, stream) = m 1, v_base 0,
+ * index_base stream.index, directions.py:138-147).  U: m x dim FP64. */
+int rrs_unit_rows_host(rrs_engine* e, uint64_t seed, uint32_t refinement, uint32_t query, int32_t m,
+                       int32_t dim, uint32_t v_base, uint32_t index_base, double* U);
+
+/* SubStream(seed, refinement, query, index).uniforms(count, offset) (normal 0)
+ * and .normals(count, offset) (normal 1) -- directions.py:76-94 over
+ * philox.uniforms / normals (philox.py:88-125). */
+int rrs_stream_values_host(rrs_engine* e, uint64_t seed, uint32_t refinement, uint32_t query, uint32_t index,
+                           uint32_t offset, int64_t count, int32_t normal, double* out);
+
+/* project_naive / project_parallel / project_point -- projection.py:99-168,
+ * _kernels.pyx:120-199: out[j*n + i] = sum_l U[j,l] * x[i,l] in FP64,
+ * acc = 0.0, ascending l, no FMA (bit-identical to the reference).
+ * x: n x d, U: m x d, out: m x n, all row-major FP64 host buffers. */
+int rrs_project_host(rrs_engine* e, const double* x, int64_t n, int32_t d, const double* U, int32_t m,
+                     double* out);
+
+/* depth_of_projections(notion, px, pz, out) -- univariate.py:162-184 over the
+ * span kernels _kernels.pyx:270-351: px m x n, pz m, out m (FP64 host
+ * buffers); exact FP64 order statistics, bit-identical to the reference. */
+int rrs_depth_of_projections_host(rrs_engine* e, int32_t notion, const double* px, int32_t m, int64_t n,
+                                  const double* pz, double* out);
+
 /* philox4x32 / philox4x32_words -- philox.py:27-65, _kernels.pyx:24-61, on
  * device.  ctr and out are (4, N) row-major uint32. */
 int rrs_philox4x32_host(rrs_engine* e, const uint32_t* ctr, int64_t N, uint32_t key0,

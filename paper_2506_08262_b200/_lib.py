@@ -74,6 +74,18 @@ SIGNATURES = [
       ctypes.c_uint32, _dp]),
     ("rrs_philox4x32_host", ctypes.c_int,
      [_vp, _u32p, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint32, _u32p]),
+    ("rrs_cap_directions_at_host", ctypes.c_int,
+     [_vp, _dp, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint32,
+      ctypes.c_uint32, ctypes.c_uint32, _dp]),
+    ("rrs_unit_rows_host", ctypes.c_int,
+     [_vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
+      ctypes.c_uint32, _dp]),
+    ("rrs_stream_values_host", ctypes.c_int,
+     [_vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int64,
+      ctypes.c_int32, _dp]),
+    ("rrs_project_host", ctypes.c_int, [_vp, _dp, ctypes.c_int64, ctypes.c_int32, _dp, ctypes.c_int32, _dp]),
+    ("rrs_depth_of_projections_host", ctypes.c_int,
+     [_vp, ctypes.c_int32, _dp, ctypes.c_int32, ctypes.c_int64, _dp, _dp]),
     ("rrs_engine_stats", ctypes.c_int, [_vp, ctypes.POINTER(RrsStatsC)]),
     ("rrs_engine_enable_timing", ctypes.c_int, [_vp, ctypes.c_int32]),
     ("rrs_engine_set_contract_path", ctypes.c_int, [_vp, ctypes.c_int32]),
@@ -139,9 +151,15 @@ def config_struct(cfg) -> RrsConfigC:
 
 
 class Engine:
-    """One rrs_engine (one CUDA device, one stream, resident dataset)."""
+    """One rrs_engine (one CUDA device, one stream, resident dataset).
+
+    The engine's dataset and workspace are shared state, and ctypes releases
+    the GIL for every call, so a caller that sets the dataset and then runs on
+    it must hold ``lock`` across both (solver.py does); the reference's
+    functions are safe to call concurrently."""
 
     def __init__(self, device: int = 0):
+        self.lock = threading.RLock()
         L = load_library()
         h = _vp()
         _raise(L.rrs_engine_create(int(device), ctypes.byref(h)))
@@ -234,13 +252,42 @@ class Engine:
                                                            _p(out), _p(cle, _i64p), _p(cge, _i64p)))
         return out, cle, cge
 
-    def cap_directions(self, pole, eps, m, seed, refinement, query):
+    def cap_directions(self, pole, eps, m, seed, refinement, query, index_base=0):
         pole = np.ascontiguousarray(pole, dtype=np.float64).reshape(-1)
         U = np.empty((m, pole.size))
-        _raise(load_library().rrs_cap_directions_host(self._h, _p(pole), pole.size, float(eps), int(m),
-                                                      int(seed) % (1 << 64), int(refinement) % (1 << 32),
-                                                      int(query) % (1 << 32), _p(U)))
+        _raise(load_library().rrs_cap_directions_at_host(self._h, _p(pole), pole.size, float(eps), int(m),
+                                                         int(seed) % (1 << 64), int(refinement) % (1 << 32),
+                                                         int(query) % (1 << 32), int(index_base) % (1 << 32),
+                                                         _p(U)))
         return U
+
+    def unit_rows(self, seed, refinement, query, m, dim, v_base, index_base):
+        U = np.empty((int(m), int(dim)))
+        _raise(load_library().rrs_unit_rows_host(self._h, int(seed) % (1 << 64), int(refinement) % (1 << 32),
+                                                 int(query) % (1 << 32), int(m), int(dim),
+                                                 int(v_base) % (1 << 32), int(index_base) % (1 << 32), _p(U)))
+        return U
+
+    def stream_values(self, seed, refinement, query, index, offset, count, normal: bool):
+        out = np.empty(int(count))
+        _raise(load_library().rrs_stream_values_host(self._h, int(seed) % (1 << 64), int(refinement) % (1 << 32),
+                                                     int(query) % (1 << 32), int(index) % (1 << 32),
+                                                     int(offset) % (1 << 32), int(count), 1 if normal else 0,
+                                                     _p(out)))
+        return out
+
+    def project(self, x, U):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        out = np.empty((U.shape[0], x.shape[0]))
+        _raise(load_library().rrs_project_host(self._h, _p(x), x.shape[0], x.shape[1], _p(U), U.shape[0],
+                                               _p(out)))
+        return out
+
+    def depth_of_projections(self, notion: str, px, pz, out):
+        _raise(load_library().rrs_depth_of_projections_host(self._h, NOTION_CODES[notion], _p(px), px.shape[0],
+                                                            px.shape[1], _p(pz), _p(out)))
+        return out
 
     def philox4x32(self, ctr, key0, key1):
         ctr = np.ascontiguousarray(ctr, dtype=np.uint32)

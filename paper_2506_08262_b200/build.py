@@ -28,6 +28,7 @@ SOURCES = {  # file -> extra flags
     "contract_tcw.cu": [],
     "contract_tcs.cu": [],
     "select.cu": [],
+    "api64.cu": [],
     "engine.cu": [],
 }
 

@@ -449,6 +449,21 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
     return RRS_OK;
 }
 
+// finite and inside the FP32 contraction range, like the dataset (the queries
+// are cast to FP32 for x - z; an out-of-range or NaN query would otherwise
+// count as all-tie rows and give silently wrong depths)
+int validate_host_queries(const double* z, int64_t count, int d) {
+    for (int64_t i = 0; i < count; ++i) {
+        const double v = z[i];
+        if (!std::isfinite(v))
+            return fail(RRS_ERR_INVALID, "query " + std::to_string(i / d) + " contains non-finite entries");
+        if (std::fabs(v) > 1e38)
+            return fail(RRS_ERR_INVALID, "query " + std::to_string(i / d) +
+                                             " exceeds the FP32 contraction range (|z| > 1e38)");
+    }
+    return RRS_OK;
+}
+
 int check_dataset(const rrs_engine* e) {
     if (!e) return fail(RRS_ERR_INVALID, "engine is null");
     if (e->n < 1 || e->d < 1) return fail(RRS_ERR_STATE, "no dataset set");
@@ -619,6 +634,17 @@ int rrs_depth_batch_device(rrs_engine* e, const double* queries_dev, int64_t Q, 
     if (Q == 0) return RRS_OK;
     if (!queries_dev || !depth_dev) return fail(RRS_ERR_INVALID, "null argument");
     if (int rc = set_device(e)) return rc;
+    {
+        CK(e->tmp_out0.ensure(16));
+        int* flag = e->tmp_out0.as<int>();
+        CK(cudaMemsetAsync(flag, 0, sizeof(int), e->stream));
+        CK(launch_validate_values(queries_dev, Q * (int64_t)e->d, flag, e->stream));
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        if (h & 1) return fail(RRS_ERR_INVALID, "queries contain non-finite entries");
+        if (h & 2) return fail(RRS_ERR_INVALID, "queries exceed the FP32 contraction range (|z| > 1e38)");
+    }
     reset_stats(e);
     return run_batches(e, queries_dev, Q, q0, cfg, eps, depth_dev, argmin_dev, trace_dev, min_count_dev);
 }
@@ -631,6 +657,7 @@ int rrs_depth_batch_host(rrs_engine* e, const double* queries, int64_t Q, int64_
     if (Q < 0) return fail(RRS_ERR_INVALID, "negative query count");
     if (Q == 0) return RRS_OK;
     if (!queries || !depth) return fail(RRS_ERR_INVALID, "null argument");
+    if (int rc = validate_host_queries(queries, Q * (int64_t)e->d, e->d)) return rc;
     if (int rc = set_device(e)) return rc;
     reset_stats(e);
     const int d = e->d, r = cfg->refinements;
@@ -663,6 +690,7 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
     if (!z || !U || !out) return fail(RRS_ERR_INVALID, "null argument");
     if (m < 1) return fail(RRS_ERR_INVALID, "batch size must be >= 1");
     if (notion < 0 || notion > 2) return fail(RRS_ERR_INVALID, "unknown depth notion");
+    if (int rc = validate_host_queries(z, e->d, e->d)) return rc;
     if (int rc = set_device(e)) return rc;
     reset_stats(e);
     const int d = e->d;
@@ -699,6 +727,12 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
 
 int rrs_cap_directions_host(rrs_engine* e, const double* pole, int32_t d, double eps, int32_t m,
                             uint64_t seed, uint32_t refinement, uint32_t query, double* U) {
+    return rrs_cap_directions_at_host(e, pole, d, eps, m, seed, refinement, query, 0u, U);
+}
+
+int rrs_cap_directions_at_host(rrs_engine* e, const double* pole, int32_t d, double eps, int32_t m,
+                               uint64_t seed, uint32_t refinement, uint32_t query, uint32_t index_base,
+                               double* U) {
     if (!e || !pole || !U) return fail(RRS_ERR_INVALID, "null argument");
     if (m < 1) return fail(RRS_ERR_INVALID, "batch size must be >= 1");
     if (d < 1 || d > GEN_MAX_D) return fail(RRS_ERR_INVALID, "dimension out of range");
@@ -737,6 +771,7 @@ int rrs_cap_directions_host(rrs_engine* e, const double* pole, int32_t d, double
     g.u64 = ub.as<double>();
     g.u32 = u32b.as<float>();
     g.seed = seed;
+    g.jbase = index_base;
     g.q0 = query;
     g.refinement = refinement;
     g.eps = eps;
@@ -748,6 +783,81 @@ int rrs_cap_directions_host(rrs_engine* e, const double* pole, int32_t d, double
     CK(cudaMemcpyAsync(U, ub.p, (size_t)m * d * 8, cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
     for (DevBuf* b : {&pb, &vb, &mb, &ub, &u32b}) b->release();
+    return RRS_OK;
+}
+
+int rrs_unit_rows_host(rrs_engine* e, uint64_t seed, uint32_t refinement, uint32_t query, int32_t m,
+                       int32_t dim, uint32_t v_base, uint32_t index_base, double* U) {
+    if (!e || !U) return fail(RRS_ERR_INVALID, "null argument");
+    if (m < 1) return fail(RRS_ERR_INVALID, "batch size must be >= 1");
+    if (dim < 1) return fail(RRS_ERR_INVALID, "dimension must be >= 1");
+    if (int rc = set_device(e)) return rc;
+    DevBuf ub;
+    CK(ub.ensure((size_t)m * dim * 8));
+    CK(launch_unit_rows(seed, refinement, query, m, dim, v_base, index_base, ub.as<double>(), e->stream));
+    CK(cudaMemcpyAsync(U, ub.p, (size_t)m * dim * 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    ub.release();
+    return RRS_OK;
+}
+
+int rrs_stream_values_host(rrs_engine* e, uint64_t seed, uint32_t refinement, uint32_t query, uint32_t index,
+                           uint32_t offset, int64_t count, int32_t normal, double* out) {
+    if (!e || (!out && count > 0)) return fail(RRS_ERR_INVALID, "null argument");
+    if (count < 0) return fail(RRS_ERR_INVALID, "negative count");
+    if (count == 0) return RRS_OK;
+    if (int rc = set_device(e)) return rc;
+    DevBuf ob;
+    CK(ob.ensure((size_t)count * 8));
+    CK(launch_stream_values(seed, refinement, query, index, offset, count, normal ? 1 : 0, ob.as<double>(),
+                            e->stream));
+    CK(cudaMemcpyAsync(out, ob.p, (size_t)count * 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    ob.release();
+    return RRS_OK;
+}
+
+int rrs_project_host(rrs_engine* e, const double* x, int64_t n, int32_t d, const double* U, int32_t m,
+                     double* out) {
+    if (!e || !x || !U || !out) return fail(RRS_ERR_INVALID, "null argument");
+    if (n < 1 || d < 1 || m < 1) return fail(RRS_ERR_INVALID, "empty projection");
+    if (int rc = set_device(e)) return rc;
+    DevBuf xb, ub, ob;
+    CK(xb.ensure((size_t)n * d * 8));
+    CK(ub.ensure((size_t)m * d * 8));
+    if (ob.ensure((size_t)m * n * 8) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(RRS_ERR_NOMEM, "projection matrix does not fit in device memory");
+    }
+    CK(cudaMemcpyAsync(xb.p, x, (size_t)n * d * 8, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(ub.p, U, (size_t)m * d * 8, cudaMemcpyHostToDevice, e->stream));
+    CK(launch_proj64(xb.as<double>(), ub.as<double>(), ob.as<double>(), n, m, d, e->stream));
+    CK(cudaMemcpyAsync(out, ob.p, (size_t)m * n * 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    for (DevBuf* b : {&xb, &ub, &ob}) b->release();
+    return RRS_OK;
+}
+
+int rrs_depth_of_projections_host(rrs_engine* e, int32_t notion, const double* px, int32_t m, int64_t n,
+                                  const double* pz, double* out) {
+    if (!e || !px || !pz || !out) return fail(RRS_ERR_INVALID, "null argument");
+    if (notion < 0 || notion > 2) return fail(RRS_ERR_INVALID, "unknown depth notion");
+    if (n < 1) return fail(RRS_ERR_INVALID, "empty projection");
+    if (m < 1) return RRS_OK;
+    if (int rc = set_device(e)) return rc;
+    DevBuf pb, zb, ob;
+    if (pb.ensure((size_t)m * n * 8) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(RRS_ERR_NOMEM, "projection matrix does not fit in device memory");
+    }
+    CK(zb.ensure((size_t)m * 8));
+    CK(ob.ensure((size_t)m * 8));
+    CK(cudaMemcpyAsync(pb.p, px, (size_t)m * n * 8, cudaMemcpyHostToDevice, e->stream));
+    CK(cudaMemcpyAsync(zb.p, pz, (size_t)m * 8, cudaMemcpyHostToDevice, e->stream));
+    CK(launch_span_depth64(pb.as<double>(), zb.as<double>(), ob.as<double>(), m, n, notion, e->stream));
+    CK(cudaMemcpyAsync(out, ob.p, (size_t)m * 8, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    for (DevBuf* b : {&pb, &zb, &ob}) b->release();
     return RRS_OK;
 }
 

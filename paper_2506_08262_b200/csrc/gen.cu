@@ -214,12 +214,13 @@ __device__ void gen_direction_warp(const GenArgs& a, int64_t gdir, double* g, do
     }
     const int dm = d - 1;
     double u1 = 0.0;
-    if (lane == 0) u1 = cos(uniform1(a.seed, 0u, (uint32_t)j, l, qg) * a.eps);
+    const uint32_t jp = a.jbase + (uint32_t)j;  // Philox index of this direction
+    if (lane == 0) u1 = cos(uniform1(a.seed, 0u, jp, l, qg) * a.eps);
     uint32_t vbase = 1;
     double nrm;
     for (;;) {
         for (int c = lane; c < dm; c += 32) {
-            double gv = ndtri(uniform1(a.seed, vbase + (uint32_t)c, (uint32_t)j, l, qg));
+            double gv = ndtri(uniform1(a.seed, vbase + (uint32_t)c, jp, l, qg));
             g[c] = gv;
             sc[c] = gv * gv;
         }
@@ -728,10 +729,71 @@ __global__ void philox_words_kernel(const uint32_t* __restrict__ ctr, uint32_t* 
     out[3 * N + i] = c3;
 }
 
+// ------------------------------------------------------ drop-in API helpers --
+// directions.py:97-135 (_normal_rows / _unit_rows): row j (Philox index
+// index_base + j) holds `dim` normals from value addresses v_base.., a zero-norm
+// row is redrawn from the next dim addresses, then g / |g| with numpy's pairwise
+// |g|^2 (random_sphere, directions.py:138-147).  One warp per row.
+__global__ void __launch_bounds__(256) unit_rows_kernel(uint64_t seed, uint32_t l, uint32_t q, int m, int dim,
+                                                        uint32_t v_base, uint32_t index_base, double* out) {
+    extern __shared__ double usm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = blockIdx.x * 8 + warp;
+    if (j >= m) return;
+    double* g = usm + (size_t)warp * 2 * dim;
+    double* sc = g + dim;
+    uint32_t vb = v_base;
+    double nrm = 0.0;
+    for (;;) {
+        for (int c = lane; c < dim; c += 32) {
+            const double gv = ndtri(uniform1(seed, vb + (uint32_t)c, index_base + (uint32_t)j, l, q));
+            g[c] = gv;
+            sc[c] = gv * gv;
+        }
+        __syncwarp();
+        if (lane == 0) nrm = sqrt(pw_sum(sc, dim));
+        nrm = __shfl_sync(0xffffffffu, nrm, 0);
+        __syncwarp();
+        if (nrm != 0.0) break;
+        vb += (uint32_t)dim;
+    }
+    for (int c = lane; c < dim; c += 32) out[(size_t)j * dim + c] = g[c] / nrm;
+}
+
+// SubStream.uniforms / .normals (directions.py:76-94): values offset + i of the
+// substream (seed, refinement, query, index); normals = ndtri(uniform)
+__global__ void stream_values_kernel(uint64_t seed, uint32_t l, uint32_t q, uint32_t index, uint32_t offset,
+                                     int64_t count, int normal, double* out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const double u = uniform1(seed, offset + (uint32_t)i, index, l, q);
+    out[i] = normal ? ndtri(u) : u;
+}
+
+cudaError_t launch_unit_rows(uint64_t seed, uint32_t l, uint32_t q, int m, int dim, uint32_t v_base,
+                             uint32_t index_base, double* out, cudaStream_t st) {
+    if (m < 1 || dim < 1) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)8 * 2 * dim * sizeof(double);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(unit_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    unit_rows_kernel<<<(unsigned)((m + 7) / 8), 256, smem, st>>>(seed, l, q, m, dim, v_base, index_base, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stream_values(uint64_t seed, uint32_t l, uint32_t q, uint32_t index, uint32_t offset,
+                                 int64_t count, int normal, double* out, cudaStream_t st) {
+    if (count < 1) return cudaSuccess;
+    stream_values_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(seed, l, q, index, offset, count, normal,
+                                                                          out);
+    return cudaGetLastError();
+}
+
 // ----------------------------------------------------------------- launch --
 cudaError_t launch_cap_generate(const GenArgs& a, cudaStream_t st) {
     int64_t total = (int64_t)a.Qb * a.mpad;
-    if (a.d >= 2 && a.d <= GV_MAX_D && a.mpad % GV_DIRS == 0) {
+    if (a.d >= 2 && a.d <= GV_MAX_D && a.mpad % GV_DIRS == 0 && a.jbase == 0) {
         const size_t smem = (size_t)GV_DIRS * a.d * 8 + 2 * GV_DIRS * 8 + (size_t)GV_DIRS * (a.d - 1) * 2 + 16;
         if (smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(cap_generate_v2_kernel,

@@ -15,6 +15,7 @@ struct GenArgs {
     unsigned char* uop;      // nullable: [Qb][NB][tc_block_bytes(d)] packed FP16 split operand (tensor path)
     int NB;                  // 128-direction blocks per query in uop
     uint64_t seed;
+    uint32_t jbase;          // Philox index of direction 0 (random_sphere_pole's stream.index; warp path)
     int64_t q0;              // global query index of batch row 0
     uint32_t refinement;
     double eps;
@@ -266,6 +267,14 @@ cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st);  // 64 < d 
 cudaError_t launch_contract_tcs(TcsArgs a, int sms, cudaStream_t st);  // projection store, d <= 64
 cudaError_t launch_pack_tc6_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,
                                     cudaStream_t st);
+// drop-in API helpers (api64.cu, gen.cu)
+cudaError_t launch_proj64(const double* x, const double* u, double* out, int64_t n, int m, int d, cudaStream_t st);
+cudaError_t launch_span_depth64(const double* px, const double* pz, double* out, int m, int64_t n, int notion,
+                                cudaStream_t st);
+cudaError_t launch_unit_rows(uint64_t seed, uint32_t l, uint32_t q, int m, int dim, uint32_t v_base,
+                             uint32_t index_base, double* out, cudaStream_t st);
+cudaError_t launch_stream_values(uint64_t seed, uint32_t l, uint32_t q, uint32_t index, uint32_t offset,
+                                 int64_t count, int normal, double* out, cudaStream_t st);
 cudaError_t launch_validate_values(const double* x, int64_t count, int* flag, cudaStream_t st);
 cudaError_t launch_row_absmax(const float* xb, float* xmax, int d, int64_t tiles, cudaStream_t st);
 cudaError_t launch_pack_tc_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,

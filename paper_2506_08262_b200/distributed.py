@@ -90,13 +90,30 @@ def depth_sharded_device(Z_dev, cfg, *, q_offset: int, eng, group=None):
     depth = torch.empty(S, dtype=torch.float64, device=Z_dev.device)
     argmin = torch.empty((S, d), dtype=torch.float64, device=Z_dev.device)
     count = torch.empty(S, dtype=torch.int64, device=Z_dev.device)
-    eng.depth_batch_device(Z_dev, cfg, q_offset, depth, argmin, None, count, eps=cfg.epsilons())
+    # the engine launches on its own stream unless bound to torch's: bind it to the
+    # current torch stream so the reads below are stream-ordered after the kernels
+    # (torch's legacy default stream has handle 0, which the ABI reads as "own
+    # stream", so that case synchronises instead)
+    cur = torch.cuda.current_stream(Z_dev.device)
+    with eng.lock:
+        if cur.cuda_stream:
+            eng.set_stream(cur.cuda_stream)
+        eng.depth_batch_device(Z_dev, cfg, q_offset, depth, argmin, None, count, eps=cfg.epsilons())
+        if not cur.cuda_stream:
+            eng.synchronize()
     rec[:, 0] = depth
     rec[:, 1] = count.to(torch.float64)
     rec[:, 2:] = argmin
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return rec
+    if dist.get_backend(group) != "nccl":
+        # gloo (ranks sharing one GPU in the single-GPU rehearsal): the same one
+        # all_gather, staged through host memory
+        host = rec.cpu()
+        gathered = torch.empty((world * S, 2 + d), dtype=torch.float64)
+        dist.all_gather_into_tensor(gathered, host, group=group)
+        return gathered.to(Z_dev.device)
     gathered = torch.empty((world * S, 2 + d), dtype=torch.float64, device=Z_dev.device)
     dist.all_gather_into_tensor(gathered, rec, group=group)
     return gathered

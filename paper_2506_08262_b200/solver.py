@@ -9,16 +9,23 @@ from __future__ import annotations
 
 import numpy as np
 
+from contextlib import contextmanager
+
 from . import _lib
 from .config import (CapSpec, Dataset, DepthResult, DimensionMismatch, DirectionBatch,
                      ParallelConfig, PhaseTimer, RefinementRecord, RrsConfig, NOTIONS)
 
 
-def _engine_for(data: Dataset, device=None) -> _lib.Engine:
+@contextmanager
+def _session(data: Dataset | None, device=None):
+    """The device engine with `data` resident, locked for the whole call: two
+    threads with different datasets must not swap the engine's dataset (or its
+    workspace) between set_dataset and the compute call."""
     eng = _lib.engine(device)
-    if eng.dataset_key is not data._token:
-        eng.set_dataset(data.x, key=data._token)
-    return eng
+    with eng.lock:
+        if data is not None and eng.dataset_key is not data._token:
+            eng.set_dataset(data.x, key=data._token)
+        yield eng
 
 
 def _results(depth, argmin, tr, cfg: RrsConfig) -> list[DepthResult]:
@@ -50,15 +57,15 @@ def depth_batch_arrays(queries, data: Dataset, cfg: RrsConfig, *, q0: int = 0, t
         Z = Z.reshape(1, -1)
     if Z.shape[1] != data.dim:
         raise DimensionMismatch(f"query dimension {Z.shape[1]} does not match data dimension {data.dim}")
-    eng = _engine_for(data, device)
-    if timer is not None:
-        eng.enable_timing(True)
-    try:
-        res = eng.depth_batch(Z, cfg, q0=q0, trace=trace, eps=cfg.epsilons())
-    finally:
+    with _session(data, device) as eng:
         if timer is not None:
-            _add_timer(timer, eng)
-            eng.enable_timing(False)
+            eng.enable_timing(True)
+        try:
+            res = eng.depth_batch(Z, cfg, q0=q0, trace=trace, eps=cfg.epsilons())
+        finally:
+            if timer is not None:
+                _add_timer(timer, eng)
+                eng.enable_timing(False)
     return res
 
 
@@ -120,8 +127,8 @@ def evaluate_directions(z, data: Dataset, dirs, notion: str, cfg: ParallelConfig
     z = np.ascontiguousarray(z, dtype=np.float64).reshape(-1)
     if z.size != data.dim:
         raise DimensionMismatch(f"query dimension {z.size} does not match data dimension {data.dim}")
-    eng = _engine_for(data)
-    out, _, _ = eng.evaluate_directions(z, u, notion)
+    with _session(data) as eng:
+        out, _, _ = eng.evaluate_directions(z, u, notion)
     if _buffers is not None:
         _buffers[2][: out.size] = out
         return _buffers[2]
@@ -132,14 +139,14 @@ def evaluate_directions_counts(z, data: Dataset, U):
     """Halfspace counts (#<=, #>=) per direction on injected directions (tier-1
     parity interface; the reference equivalent is rint(depth * n) plus
     project_parallel/project_point, projection.py:140-168)."""
-    eng = _engine_for(data)
-    return eng.evaluate_directions(z, U, "halfspace")
+    with _session(data) as eng:
+        return eng.evaluate_directions(z, U, "halfspace")
 
 
 def generate_batch(cap: CapSpec, m: int, seed: int, refinement: int, query: int = 0) -> DirectionBatch:
     """directions.py:192-204, generated on device (FP64)."""
     if m < 1:
         raise ValueError("batch size must be >= 1")
-    eng = _lib.engine()
-    U = eng.cap_directions(cap.pole.p, cap.epsilon, m, seed, refinement, query)
+    with _session(None) as eng:
+        U = eng.cap_directions(cap.pole.p, cap.epsilon, m, seed, refinement, query)
     return DirectionBatch(directions=U, seed_info=(seed, refinement))

@@ -1,0 +1,69 @@
+"""Tier 3 at the BASELINE.json shapes against the REAL reference.
+
+The fixtures tests/golden/tier3_<tag>.npz hold the reference's own
+``depth_batch`` outputs (optimizer.py:254-279, compiled backend, 8 cores; made
+by tests/golden/make_tier3.py) at k = 20,000, r = 20, alpha = 0.9, seed = 1:
+
+  c2  projection        n = 10k,  d = 20,  Gaussian, 64 in-sample queries
+  c3  asym_projection   n = 50k,  d = 50,  Cauchy,   32 in-sample queries
+  c4  halfspace         n = 100k, d = 50,  Gaussian, 64 off-sample (0.3 x_i, 0.15 x fresh) + 8 in-sample
+  c5h halfspace         n = 1M,   d = 200, Gaussian, 6 queries
+  c5p projection        n = 1M,   d = 200, Gaussian, 6 queries
+
+The CUDA path runs the same queries (same positions = same Philox substreams)
+through the public API and must reach Kendall tau-b >= 0.99 against the
+reference (north_star; tau from study/correlation.py, which is pinned to the
+reference's kendall_tau).  Halfspace depths are integer counts / n: their
+per-query equality with the reference is asserted as well, and the share of
+identical depths is logged for every notion.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "golden"))
+
+import tier3_data as T  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _fixture(tag):
+    path = os.path.join(HERE, "golden", f"tier3_{tag}.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"missing fixture {path} (python tests/golden/make_tier3.py {tag})")
+    return np.load(path)
+
+
+@pytest.mark.parametrize("tag", ["c2", "c3", "c4", "c5h", "c5p"])
+def test_tier3_against_reference(b200, tag):
+    from paper_2506_08262_b200.study.correlation import kendall_tau
+
+    fx = _fixture(tag)
+    notion, n, d, dist, k, r, alpha = T.CASES[tag]
+    X = T.dataset(tag)
+    assert T.digest(X) == str(fx["x_digest"]), "dataset bytes differ from the fixture's"
+    Z = T.queries(tag, X)
+    assert np.array_equal(Z, fx["z"])
+    cfg = b200.RrsConfig(total_directions=k, refinements=r, shrink=alpha, notion=notion, seed=1)
+    depth, argmin, tr, cnt = b200.depth_batch_arrays(Z, b200.Dataset(X), cfg, trace=True)
+    ref = fx["depth"]
+    same = float(np.mean(depth == ref))
+    rel = np.abs(depth - ref) / np.maximum(np.abs(ref), 1e-300)
+    tau = kendall_tau(depth, ref) if len(np.unique(ref)) > 1 else 1.0
+    print(f"\n{tag}: {notion} n={n} d={d} Q={len(Z)}: tau_b={tau:.4f}, identical depths {same:.3f}, "
+          f"max rel diff {rel.max():.2e}, trace identical "
+          f"{float(np.mean(tr[:, :, 0] == fx['trace_best'])):.3f}")
+    assert tau >= 0.99
+    if notion == "halfspace":
+        ref_cnt = np.rint(ref * n).astype(np.int64)
+        diff = np.flatnonzero(cnt != ref_cnt)
+        assert diff.size == 0, f"count differs for queries {diff}: {cnt[diff]} vs {ref_cnt[diff]}"
+    else:
+        assert rel.max() < 1e-3
+    # argmin directions are unit vectors from the same cap draws
+    assert np.allclose(np.linalg.norm(argmin, axis=1), 1.0, atol=1e-12)
