@@ -24,6 +24,7 @@ SOURCES = {  # file -> extra flags
     "gen.cu": ["-fmad=false"],
     "contract.cu": [],
     "contract_tc.cu": [],
+    "contract_tcf.cu": [],
     "contract_tc2.cu": [],
     "contract_tcw.cu": [],
     "contract_tcs.cu": [],

@@ -84,12 +84,15 @@ struct rrs_engine {
     // dataset
     DevBuf xb;
     DevBuf xmax;  // [tiles * BM] max_l |x_il| (wide tensor path, 64 < d <= 256)
+    DevBuf xr;    // [tiles * BM][tcf_dp(d)] row-major FP32 (filter-and-refine path, d <= 64)
     int64_t n = 0;
     int d = 0;
     int64_t tiles = 0;
     // workspace
     DevBuf zq, u64, u32, uop, counts, depths, y, pole, reflv, reflmode, dmin, bestcnt;
-    int contract_path = 0;  // 0 auto, 1 FFMA (contract.cu), 2 tensor cores (contract_tc.cu), 3 2-SM (contract_tc2.cu)
+    // 0 auto, 1 FFMA (contract.cu), 2 tensor cores (contract_tcf.cu filter-and-refine for d <= 64,
+    // contract_tcw.cu above), 3 2-SM split (contract_tc2.cu), 4 two-term split (contract_tc.cu)
+    int contract_path = 0;
     DevBuf tmp_in, tmp_out0, tmp_out1, tmp_out2, tmp_out3;
     // timing
     bool timing = false;
@@ -154,7 +157,8 @@ int validate_cfg(const rrs_config* c) {
 
 struct Plan {
     int m, mpad, MB, Qb;
-    bool tc;     // tensor-core FP16-split contraction (halfspace, d <= 256; contract_tcw.cu for d > 64)
+    bool tc;     // tensor-core contraction (halfspace, d <= 256; contract_tcw.cu for d > 64)
+    bool tcf;    // ... by filter and refine (contract_tcf.cu, d <= 64; u32 holds FP32 rows)
     bool tcs;    // tensor-core projection store (projection notions, d <= 50; contract_tcs.cu)
     int nb8;     // 128-direction blocks per query (tensor path operand, tc_block_bytes(d) each)
     int jchunk;  // direction blocks per store launch (projection notions)
@@ -169,13 +173,15 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     p.nb8 = p.MB;
     const bool tc_ok = notion == RRS_HALFSPACE && e->d <= 256;
     p.tc = tc_ok && (e->contract_path >= 2 || (e->contract_path == 0 && e->n >= 4096));
+    p.tcf = p.tc && e->d <= TC_SLICE && (e->contract_path == 0 || e->contract_path == 2);
     const bool tcs_ok = notion != RRS_HALFSPACE && tc6_layout(e->d).ns <= 19;
     // auto: the store is HBM-write bound at small d (y is n*m*4 bytes per query and
     // refinement whatever computes it), the tensor store pays from d ~ 32 (config 3)
     p.tcs = tcs_ok && (e->contract_path >= 2 || (e->contract_path == 0 && e->n >= 4096 && e->d >= 32));
     const int64_t d = e->d, n = e->n;
-    int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * d * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 8 +
-                    d * 40 + 64 + (int64_t)p.nb8 * (p.tcs ? tc6_block_bytes(e->d) : tc_block_bytes(e->d));
+    int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * tcf_dp((int)d) * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 8 +
+                    d * 40 + 64 +
+                    (int64_t)p.nb8 * (p.tcs ? tc6_block_bytes(e->d) : p.tcf ? tcf_block_bytes(e->d) : tc_block_bytes(e->d));
     int64_t budget = e->ws_limit;
     int64_t qb = 4096;
     if (notion != RRS_HALFSPACE) {
@@ -216,13 +222,14 @@ int ensure_ws(rrs_engine* e, const Plan& p, int notion) {
     const size_t Qb = p.Qb, d = e->d;
     CK(e->zq.ensure(Qb * d * 4));
     CK(e->u64.ensure(Qb * p.m * d * 8));
-    CK(e->u32.ensure(Qb * p.mpad * d * 4));
+    CK(e->u32.ensure(Qb * p.mpad * (p.tcf ? (size_t)tcf_dp(e->d) : d) * 4));
     CK(e->pole.ensure(Qb * d * 8));
     CK(e->reflv.ensure(Qb * d * 8));
     CK(e->reflmode.ensure(Qb * 4));
     CK(e->dmin.ensure(Qb * 8));
     CK(e->bestcnt.ensure(Qb * 8));
-    CK(e->uop.ensure(p.tc    ? Qb * (size_t)p.nb8 * tc_block_bytes(e->d)
+    CK(e->uop.ensure(p.tcf   ? Qb * (size_t)p.nb8 * tcf_block_bytes(e->d)
+                     : p.tc  ? Qb * (size_t)p.nb8 * tc_block_bytes(e->d)
                      : p.tcs ? Qb * (size_t)p.nb8 * tc6_block_bytes(e->d)
                              : 16));
     if (notion == RRS_HALFSPACE) {
@@ -257,7 +264,23 @@ ContractArgs contract_args(rrs_engine* e, const Plan& p, int Qb, int jb0, int jb
 }
 
 int contract_halfspace(rrs_engine* e, const Plan& p, int Qb) {
-    if (p.tc) {
+    if (p.tcf) {
+        TcfArgs t{};
+        t.xr = e->xr.as<float>();
+        t.zq = e->zq.as<float>();
+        t.uop = e->uop.as<unsigned char>();
+        t.u32r = e->u32.as<float>();
+        t.counts = e->counts.as<int>();
+        t.n = e->n;
+        t.tiles = e->tiles;
+        t.d = e->d;
+        t.Qb = Qb;
+        t.NB = p.nb8;
+        t.m = p.m;
+        t.mpad = p.mpad;
+        CK(launch_contract_tcf(t, e->sms, e->stream));
+        e->stats.tensor_contract_launches++;
+    } else if (p.tc) {
         TcArgs t{};
         t.xb = e->xb.as<float>();
         t.zq = e->zq.as<float>();
@@ -398,6 +421,8 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 g.mpad = p.mpad;
                 g.d = d;
                 g.uop = p.tc ? e->uop.as<unsigned char>() : nullptr;
+                g.uop_mode = p.tcf ? 1 : 0;
+                g.u32r = p.tcf ? e->u32.as<float>() : nullptr;
                 g.NB = p.nb8;
                 CK(launch_cap_generate(g, e->stream));
                 e->stats.kernel_launches++;
@@ -552,8 +577,9 @@ int rrs_engine_set_workspace_limit(rrs_engine* e, int64_t bytes) {
 
 int rrs_engine_set_contract_path(rrs_engine* e, int32_t path) {
     if (!e) return fail(RRS_ERR_INVALID, "engine is null");
-    if (path < 0 || path > 3)
-        return fail(RRS_ERR_INVALID, "contract path must be 0 (auto), 1 (FFMA), 2 (tensor) or 3 (tensor, 2-SM)");
+    if (path < 0 || path > 4)
+        return fail(RRS_ERR_INVALID,
+                    "contract path must be 0 (auto), 1 (FFMA), 2 (tensor), 3 (2-SM split) or 4 (two-term split)");
     e->contract_path = path;
     return RRS_OK;
 }
@@ -593,6 +619,10 @@ static int set_dataset_common(rrs_engine* e, const double* xdev, int64_t n, int3
     const int64_t tiles = (n + BM - 1) / BM;
     CK(e->xb.ensure((size_t)tiles * d * BM * 4));
     CK(launch_block_dataset(xdev, e->xb.as<float>(), n, d, tiles, e->stream));
+    if (d <= TC_SLICE) {
+        CK(e->xr.ensure((size_t)tiles * BM * tcf_dp(d) * 4));
+        CK(launch_rows_dataset(xdev, e->xr.as<float>(), n, d, tiles, e->stream));
+    }
     if (d > TC_SLICE) {
         CK(e->xmax.ensure((size_t)tiles * BM * 4));
         CK(launch_row_absmax(e->xb.as<float>(), e->xmax.as<float>(), d, tiles, e->stream));
@@ -700,8 +730,12 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
     CK(cudaMemcpyAsync(e->u64.p, U, (size_t)m * d * 8, cudaMemcpyHostToDevice, e->stream));
     CK(cudaMemcpyAsync(e->tmp_in.p, z, (size_t)d * 8, cudaMemcpyHostToDevice, e->stream));
     CK(launch_queries_to_f32(e->tmp_in.as<double>(), e->zq.as<float>(), d, e->stream));
-    CK(launch_pack_directions(e->u64.as<double>(), e->u32.as<float>(), 1, m, p.mpad, d, e->stream));
-    if (p.tc) CK(launch_pack_tc_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
+    if (p.tcf)
+        CK(launch_pack_tcf_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), e->u32.as<float>(), 1, m, p.nb8,
+                                   p.mpad, d, e->stream));
+    else
+        CK(launch_pack_directions(e->u64.as<double>(), e->u32.as<float>(), 1, m, p.mpad, d, e->stream));
+    if (p.tc && !p.tcf) CK(launch_pack_tc_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (p.tcs) CK(launch_pack_tc6_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (notion == RRS_HALFSPACE) {
         CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.mpad * 2 * 4, e->stream));

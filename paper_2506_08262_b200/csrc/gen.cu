@@ -146,6 +146,15 @@ __device__ double pw_rec(const double* a, int n) {
 
 __device__ __forceinline__ double pw_sum(const double* a, int n) { return 0.0 + pw_rec(a, n); }
 
+// Filter-and-refine operand (contract_tcf.cu, kernels.h): K position kk of
+// direction row (coordinates row[0..d)): fp16(u * TCF_SU), the threshold slot
+// at kk = d (1, or 4 for a padded direction), zeros after.
+__device__ __forceinline__ __half tcf_value(const double* row, int d, int kk, bool real) {
+    if (kk < d) return real ? __double2half(row[kk] * (double)TCF_SU) : __double2half(0.0);
+    if (kk == d) return __float2half_rn(real ? 1.0f : 4.0f);
+    return __double2half(0.0);
+}
+
 // Tensor-path direction operand (contract_tc.cu): u * 2^15 = hi + lo, both
 // FP16 (hi = fp16(u 2^15), lo = fp16(u 2^15 - hi), |u| <= 1), placed at the
 // three K positions of the packed split-product layout (kernels.h, tc_layout):
@@ -184,9 +193,23 @@ __device__ void gen_direction_warp(const GenArgs& a, int64_t gdir, double* g, do
     unsigned char* op = nullptr;
     if (a.uop && j < a.NB * 128)
         op = a.uop + ((size_t)q * a.NB + (j >> 7)) * tc_block_bytes(d) + (size_t)(j & 127) * 16;
+    float* u32r = a.u32r ? a.u32r + ((size_t)q * a.mpad + j) * tcf_dp(d) : nullptr;
+    if (a.uop_mode == 1) {
+        if (a.uop && j < a.NB * 128)
+            op = a.uop + ((size_t)q * a.NB + (j >> 7)) * tcf_block_bytes(d) + (size_t)(j & 127) * 16;
+        else
+            op = nullptr;
+    }
     if (j >= a.m) {
         if (u32)
             for (int c = lane; c < d; c += 32) u32[(size_t)c * BN] = 0.0f;
+        if (u32r)
+            for (int c = lane; c < tcf_dp(d); c += 32) u32r[c] = 0.0f;
+        if (op && a.uop_mode == 1) {
+            for (int kk = lane; kk < 16 * tcf_ns(d); kk += 32)
+                *reinterpret_cast<__half*>(op + (kk >> 3) * 2048 + (kk & 7) * 2) = tcf_value(nullptr, d, kk, false);
+            return;
+        }
         if (op)
             for (int kk = lane; kk < 16 * tc_layout(d).ns; kk += 32)
                 *reinterpret_cast<__half*>(op + (kk >> 3) * 2048 + (kk & 7) * 2) = __double2half(0.0);
@@ -200,6 +223,13 @@ __device__ void gen_direction_warp(const GenArgs& a, int64_t gdir, double* g, do
         if (lane == 0) {
             u64[0] = pole[0];
             if (u32) u32[0] = (float)pole[0];
+        }
+        if (u32r)
+            for (int c = lane; c < tcf_dp(d); c += 32) u32r[c] = c == 0 ? (float)pole[0] : 0.0f;
+        if (op && a.uop_mode == 1) {
+            for (int kk = lane; kk < 16 * tcf_ns(d); kk += 32)
+                *reinterpret_cast<__half*>(op + (kk >> 3) * 2048 + (kk & 7) * 2) = tcf_value(pole, d, kk, true);
+            return;
         }
         if (op) {
             const TcLayout L = tc_layout(d);
@@ -259,7 +289,13 @@ __device__ void gen_direction_warp(const GenArgs& a, int64_t gdir, double* g, do
         u64[c] = val;
         if (u32) u32[(size_t)c * BN] = (float)val;
     }
-    if (op) {
+    if (u32r)
+        for (int c = lane; c < tcf_dp(d); c += 32) u32r[c] = c < d ? (float)sc[c] : 0.0f;
+    if (op && a.uop_mode == 1) {
+        __syncwarp();
+        for (int kk = lane; kk < 16 * tcf_ns(d); kk += 32)
+            *reinterpret_cast<__half*>(op + (kk >> 3) * 2048 + (kk & 7) * 2) = tcf_value(sc, d, kk, true);
+    } else if (op) {
         const TcLayout L = tc_layout(d);
         for (int kk = lane; kk < 16 * L.ns; kk += 32) {  // zero padding positions
             int p, c;
@@ -438,7 +474,29 @@ __global__ void __launch_bounds__(GV_THREADS, RRS_GEN_BLOCKS_PER_SM) cap_generat
             u32[(size_t)c * BN + jj] = jj < nval ? (float)val[jj * d + c] : 0.0f;
         }
     }
-    if (a.uop) {
+    if (a.u32r) {  // FP32 rows for contract_tcf's refinement (zero padding)
+        const int dp = tcf_dp(d);
+        float* rows = a.u32r + ((size_t)q * a.mpad + j0) * dp;
+        for (int e = tid; e < GV_DIRS * dp; e += GV_THREADS) {
+            const int jj = e / dp, c = e - jj * dp;
+            rows[e] = (jj < nval && c < d) ? (float)val[jj * d + c] : 0.0f;
+        }
+    }
+    if (a.uop && a.uop_mode == 1) {
+        const int nchunk = 2 * tcf_ns(d);
+        unsigned char* base = a.uop + ((size_t)q * a.NB + (j0 >> 7)) * tcf_block_bytes(d) + (size_t)(j0 & 127) * 16;
+        for (int t = tid; t < GV_DIRS * nchunk; t += GV_THREADS) {
+            const int jj = t & (GV_DIRS - 1), cc = t >> 5;
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const __half h0 = tcf_value(val + jj * d, d, 8 * cc + 2 * e, jj < nval);
+                const __half h1 = tcf_value(val + jj * d, d, 8 * cc + 2 * e + 1, jj < nval);
+                w[e] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+            }
+            *reinterpret_cast<uint4*>(base + (size_t)cc * 2048 + jj * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    } else if (a.uop) {
         // packed split-product layout, one 16-byte chunk (8 K positions) per task
         const TcLayout L = tc_layout(d);
         const int nchunk = 2 * L.ns;
@@ -727,6 +785,48 @@ __global__ void philox_words_kernel(const uint32_t* __restrict__ ctr, uint32_t* 
     out[N + i] = c1;
     out[2 * N + i] = c2;
     out[3 * N + i] = c3;
+}
+
+// Explicit-direction mode for contract_tcf: hi-layout operand + FP32 rows from U64.
+__global__ void pack_tcf_operand_kernel(const double* __restrict__ u64, unsigned char* __restrict__ uop,
+                                        float* __restrict__ u32r, int Qb, int m, int NB, int mpad, int d) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one (q, j) row per thread
+    if (idx >= (int64_t)Qb * mpad) return;
+    const int q = (int)(idx / mpad), j = (int)(idx % mpad);
+    const bool real = j < m;
+    const double* row = u64 + ((size_t)q * m + (real ? j : 0)) * d;
+    const int dp = tcf_dp(d);
+    float* r32 = u32r + ((size_t)q * mpad + j) * dp;
+    for (int c = 0; c < dp; ++c) r32[c] = (real && c < d) ? (float)row[c] : 0.0f;
+    if (j >= NB * 128) return;
+    unsigned char* op = uop + ((size_t)q * NB + (j >> 7)) * tcf_block_bytes(d) + (size_t)(j & 127) * 16;
+    for (int kk = 0; kk < 16 * tcf_ns(d); ++kk)
+        *reinterpret_cast<__half*>(op + (kk >> 3) * 2048 + (kk & 7) * 2) = tcf_value(row, d, kk, real);
+}
+
+cudaError_t launch_pack_tcf_operand(const double* u64, unsigned char* uop, float* u32r, int Qb, int m, int NB,
+                                    int mpad, int d, cudaStream_t st) {
+    const int64_t total = (int64_t)Qb * mpad;
+    pack_tcf_operand_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(u64, uop, u32r, Qb, m, NB, mpad, d);
+    return cudaGetLastError();
+}
+
+// Row-major padded FP32 copy of the dataset for contract_tcf: [tiles * 128][dp],
+// zero rows past n and zero columns past d (x rounded to FP32 like block_dataset).
+__global__ void rows_dataset_kernel(const double* __restrict__ x, float* __restrict__ xr, int64_t n, int d,
+                                    int64_t tiles) {
+    const int dp = tcf_dp(d);
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= tiles * BM * dp) return;
+    const int64_t i = idx / dp;
+    const int c = (int)(idx - i * dp);
+    xr[idx] = (i < n && c < d) ? (float)x[i * d + c] : 0.0f;
+}
+
+cudaError_t launch_rows_dataset(const double* x, float* xr, int64_t n, int d, int64_t tiles, cudaStream_t st) {
+    const int64_t total = tiles * BM * tcf_dp(d);
+    rows_dataset_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(x, xr, n, d, tiles);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------ drop-in API helpers --

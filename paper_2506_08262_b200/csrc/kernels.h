@@ -12,7 +12,9 @@ struct GenArgs {
     const double* refl_v;    // [Qb][d]
     double* u64;             // [Qb][m][d]
     float* u32;              // [Qb][mpad/BN][d][BN]
-    unsigned char* uop;      // nullable: [Qb][NB][tc_block_bytes(d)] packed FP16 split operand (tensor path)
+    unsigned char* uop;      // nullable: [Qb][NB][block bytes] FP16 tensor operand (layout by uop_mode)
+    int uop_mode;            // 0: split layout (tc_layout, contract_tc/tcw), 1: hi layout (contract_tcf)
+    float* u32r;             // nullable: [Qb][mpad][tcf_dp(d)] FP32 direction rows (contract_tcf refinement)
     int NB;                  // 128-direction blocks per query in uop
     uint64_t seed;
     uint32_t jbase;          // Philox index of direction 0 (random_sphere_pole's stream.index; warp path)
@@ -235,6 +237,34 @@ struct TcArgs {
     int64_t tiles_per_chunk;
 };
 
+// Filter-and-refine halfspace contraction (contract_tcf.cu, d <= 64): one FP16
+// product per coordinate, K = d + 1.  Direction operand A (written by gen.cu):
+// coordinate l at K index l holds fp16(u_l * TCF_SU), K index d the threshold
+// slot (1, or 4 for padded directions j >= m), zeros after; canonical K-major
+// [kk/8][row 128][8 fp16] per 128-direction block, ns = ceil((d+1)/16) steps.
+// The point operand is built in the kernel (b_l = fp16(a_l * TCF_CB / ||a||)).
+// FP32 rows for the exact refinement: directions u32 = (float)u64 as
+// [Qb][mpad][dp] and the dataset as [tiles * 128][dp], dp = d rounded up to 4.
+constexpr float TCF_SU = 1024.0f;
+constexpr float TCF_CB = 0.833333313f;  // TCF_SU * TCF_CB = 2^10 / 1.2: bound margin, see contract_tcf.cu
+__host__ __device__ inline int tcf_ns(int d) { return (d + 16) / 16; }
+__host__ __device__ inline int tcf_dp(int d) { return (d + 3) & ~3; }
+__host__ __device__ inline int tcf_block_bytes(int d) { return tcf_ns(d) * 4096; }
+
+struct TcfArgs {
+    const float* xr;            // [tiles * 128][dp] row-major FP32 dataset (zero padding rows / columns)
+    const float* zq;            // [Qb][d]
+    const unsigned char* uop;   // [Qb][NB][tcf_block_bytes(d)] direction operand (hi layout)
+    const float* u32r;          // [Qb][mpad][dp] FP32 direction rows
+    int* counts;                // [Qb][mpad][2]
+    int64_t n;
+    int64_t tiles;
+    int d, Qb, NB, m, mpad;
+    // filled by launch_contract_tcf
+    int groups, chunks, gb, sa;
+    int64_t tiles_per_chunk;
+};
+
 // Univariate projection depths from stored projections y (difference form).
 struct SelectArgs {
     const float* y;          // [Qb][jcount][n] (row stride n)
@@ -262,6 +292,10 @@ cudaError_t launch_contract_count(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_contract_store(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
 cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st);
+cudaError_t launch_contract_tcf(TcfArgs a, int sms, cudaStream_t st);  // filter and refine, d <= 64
+cudaError_t launch_pack_tcf_operand(const double* u64, unsigned char* uop, float* u32r, int Qb, int m, int NB,
+                                    int mpad, int d, cudaStream_t st);
+cudaError_t launch_rows_dataset(const double* x, float* xr, int64_t n, int d, int64_t tiles, cudaStream_t st);
 cudaError_t launch_contract_tc2(TcArgs a, int sms, cudaStream_t st);  // 2-SM (cta_group::2) variant
 cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st);  // 64 < d <= 256 (contract_tcw.cu)
 cudaError_t launch_contract_tcs(TcsArgs a, int sms, cudaStream_t st);  // projection store, d <= 64

@@ -17,7 +17,9 @@ ap.add_argument("--d", type=int, default=50)
 ap.add_argument("--q", type=int, default=1024)
 ap.add_argument("--m", type=int, default=1000)
 ap.add_argument("--r", type=int, default=2)
+ap.add_argument("--path", default="auto")
 a = ap.parse_args()
+rrs.engine().set_contract_path(a.path)
 X = toeplitz_gaussian(a.d, a.n, seed=0)
 cfg = rrs.RrsConfig(total_directions=a.m * a.r, refinements=a.r, shrink=0.9, notion=a.notion, seed=1)
 out = rrs.depth_batch_arrays(X[: a.q], rrs.Dataset(X), cfg)
