@@ -35,17 +35,18 @@
 // Layout (M = 128 directions on TMEM lanes, N = 128 points, K = 16 per MMA,
 // ns = ceil((d+1)/16) K-steps; TMEM: three FP32 accumulators at columns 0,
 // 128, 256 and the unit's gb direction blocks at 384 + 8 ns b):
-//   warp 0     TMA: the unit's direction blocks (FP16, one staging buffer) and
-//              its FP32 direction rows U32 [gb*128][dp] (for refinement);
-//   warp 1     TMEM allocator + tcgen05 issuer (tcgen05.cp of the blocks per
-//              unit, ns MMAs per tile and block, commits);
-//   warp 2     TMA: raw FP32 point rows [128][dp] of each tile into a ring of
-//              S_A slots (the row-major padded copy of the dataset);
-//   warps 3-6  converters, one point per thread: a = x - z written back in
-//              place (kept for refinement), ||a||^2, scale, FP16 operand;
-//   warps 7-14 epilogue: tcgen05.ld, 2-bit classification, counts, and the
-//              refinement of the tile's ambiguous pairs through a shared queue
-//              (all 8 warps share it, 32 pairs per warp instruction).
+//   warp 0      TMA: the unit's direction blocks (FP16, one staging buffer) and
+//               its FP32 direction rows U32 [gb*128][dp] (for refinement);
+//   warp 1      TMEM allocator + tcgen05 issuer (tcgen05.cp of the blocks per
+//               unit, ns MMAs per tile and block, commits);
+//   warps 2-9   converters, thread = (point, alternate 8-coordinate chunks):
+//               x prefetched one tile ahead into registers (coalesced loads of
+//               the tile-blocked dataset), a = x - z into a ring of S_A row-major
+//               slots [128][dp] kept until the tile's refinement, ||a||^2
+//               (halves exchanged in shared memory), scale, FP16 operand;
+//   warps 10-17 epilogue: tcgen05.ld, 2-bit classification, counts, and the
+//               refinement of the tile's ambiguous pairs through a shared queue
+//               (all 8 warps share it, 32 pairs per warp instruction).
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_common.cuh"
@@ -54,12 +55,13 @@
 
 namespace rrs {
 
-constexpr int F_CONV_WARP0 = 3;
-constexpr int F_CONV_WARPS = 4;
-constexpr int F_EPI_WARP0 = F_CONV_WARP0 + F_CONV_WARPS;  // 7
+constexpr int F_CONV_WARP0 = 2;
+constexpr int F_CONV_WARPS = 8;                            // (point, half of the 8-coordinate chunks)
+constexpr int F_CONV_THREADS = F_CONV_WARPS * 32;
+constexpr int F_EPI_WARP0 = F_CONV_WARP0 + F_CONV_WARPS;  // 10
 constexpr int F_EPI_WARPS = 8;
 constexpr int F_EPI_THREADS = F_EPI_WARPS * 32;
-constexpr int F_THREADS = (F_EPI_WARP0 + F_EPI_WARPS) * 32;  // 480
+constexpr int F_THREADS = (F_EPI_WARP0 + F_EPI_WARPS) * 32;  // 576
 constexpr int F_NP = 128;
 constexpr int F_MD = 128;
 constexpr int F_NACC = 3;
@@ -67,14 +69,16 @@ constexpr int F_P_STAGES = 2;
 constexpr int F_QCAP = 2048;
 constexpr int F_GB_MAX = 3;
 constexpr int F_SA_MAX = 4;
+constexpr int F_MAXCH = 5;                                 // 8-coordinate chunks per converter thread (d <= 64)
+constexpr int F_XCH = 4;                                   // ... that hold coordinates (the 5th only the slot)
 constexpr uint32_t F_TMEM_COLS = 512;
 constexpr uint32_t F_A_TMEM = F_NACC * F_NP;  // 384
 constexpr int F_SMEM_LIMIT = 227 * 1024;
 
 struct TcfSmem {
-    int P, D, A32, U32, Q, CNT, ZS, QC, BARS, TADDR, total;
+    int P, D, A32, U32, Q, CNT, ZS, NRM, QC, BARS, TADDR, total;
     int stage_bytes, row_bytes;
-    static constexpr int NBARS = 2 * F_P_STAGES + 2 * F_NACC + 3 + 3 * F_SA_MAX + 2;
+    static constexpr int NBARS = 2 * F_P_STAGES + 2 * F_NACC + 3 + 2 * F_SA_MAX + 2;
     __host__ __device__ TcfSmem(int d, int gb, int sa) {
         const int ns = tcf_ns(d);
         row_bytes = tcf_dp(d) * 4;
@@ -85,8 +89,9 @@ struct TcfSmem {
         U32 = A32 + sa * F_NP * row_bytes;
         Q = U32 + gb * F_MD * row_bytes;
         CNT = Q + F_QCAP * 4;                 // int [F_GB_MAX][128][4]: neg, amb, fix<0, fix>0
-        ZS = CNT + F_GB_MAX * F_MD * 16;      // float [2][64]
-        QC = ZS + 2 * 64 * 4;                 // int [2] queue counters (tile parity)
+        ZS = CNT + F_GB_MAX * F_MD * 16;      // float [2][64] query per unit parity
+        NRM = ZS + 2 * 64 * 4;                // float [2][2][128] partial |a|^2 (tile parity, half)
+        QC = NRM + 2 * 2 * F_NP * 4;          // int [2] queue counters (tile parity)
         BARS = QC + 16;
         TADDR = BARS + NBARS * 8;
         total = TADDR + 16 + 1024;
@@ -144,7 +149,8 @@ __device__ __forceinline__ void tcf_mma_issue(const TcfArgs& a, int64_t units, u
     }
 }
 
-// y = sum_l u_l * a_l, fma chain ascending from +0 (contract.cu's arithmetic)
+// y = sum_l u_l * a_l, fma chain ascending from +0 (contract.cu's arithmetic;
+// padded coordinates are 0 * 0 and leave the chain unchanged)
 __device__ __forceinline__ float refine_dot(const float* arow, const float* urow, int dp4) {
     const float4* A = reinterpret_cast<const float4*>(arow);
     const float4* U = reinterpret_cast<const float4*>(urow);
@@ -160,7 +166,23 @@ __device__ __forceinline__ float refine_dot(const float* arow, const float* urow
     return acc;
 }
 
-__global__ void __launch_bounds__(F_THREADS, 1) contract_tcf_kernel(const TcfArgs a) {
+// converter: x of the thread's chunks of tile t (K-major tile-blocked dataset),
+// one coalesced 128-byte load per coordinate and warp
+__device__ __forceinline__ void load_x_chunks(const float* __restrict__ xb, int64_t t, int d, int r, int h,
+                                              float (&x)[F_XCH][8]) {
+    const float* base = xb + (size_t)t * d * F_NP + r;
+#pragma unroll
+    for (int k = 0; k < F_XCH; ++k) {
+        const int cc = 2 * k + h;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int l = 8 * cc + e;
+            x[k][e] = l < d ? __ldg(base + (size_t)l * F_NP) : 0.0f;
+        }
+    }
+}
+
+__global__ void __maxnreg__(112) contract_tcf_kernel(const TcfArgs a) {
     extern __shared__ __align__(1024) unsigned char tcf_raw[];
     unsigned char* sm = tcf_raw + ((1024u - (smem_u32(tcf_raw) & 1023u)) & 1023u);
     const int d = a.d, dp = tcf_dp(d), dp4 = dp / 4, ns = tcf_ns(d);
@@ -174,6 +196,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) contract_tcf_kernel(const TcfArg
     uint32_t* sQ = reinterpret_cast<uint32_t*>(sm + lay.Q);
     int* sCnt = reinterpret_cast<int*>(sm + lay.CNT);
     float* sZ = reinterpret_cast<float*>(sm + lay.ZS);
+    float* sNrm = reinterpret_cast<float*>(sm + lay.NRM);
     int* sQc = reinterpret_cast<int*>(sm + lay.QC);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + lay.BARS);
     uint64_t* pfull = &bars[0];
@@ -183,9 +206,8 @@ __global__ void __launch_bounds__(F_THREADS, 1) contract_tcf_kernel(const TcfArg
     uint64_t* dfull = &bars[2 * F_P_STAGES + 2 * F_NACC];
     uint64_t* dempty = dfull + 1;
     uint64_t* udone = dfull + 2;
-    uint64_t* afull = dfull + 3;               // [F_SA_MAX] point rows landed
-    uint64_t* aconv = afull + F_SA_MAX;        // [F_SA_MAX] a = x - z written (converters)
-    uint64_t* aempty = aconv + F_SA_MAX;       // [F_SA_MAX] refinements of the tile done
+    uint64_t* aconv = dfull + 3;               // [F_SA_MAX] a = x - z of a tile written (converters)
+    uint64_t* aempty = aconv + F_SA_MAX;       // [F_SA_MAX] refinements of the tile done (epilogue)
     uint64_t* ufull = aempty + F_SA_MAX;       // unit's U32 rows landed
     uint64_t* epidone = ufull + 1;             // epilogue finished a unit (U32 reusable)
     uint32_t* sTaddr = reinterpret_cast<uint32_t*>(sm + lay.TADDR);
@@ -211,7 +233,6 @@ __global__ void __launch_bounds__(F_THREADS, 1) contract_tcf_kernel(const TcfArg
         mbar_init(dempty, 1);
         mbar_init(udone, 1);
         for (int s = 0; s < F_SA_MAX; ++s) {
-            mbar_init(&afull[s], 1);
             mbar_init(&aconv[s], F_CONV_WARPS);
             mbar_init(&aempty[s], 1);
         }
@@ -257,86 +278,118 @@ __global__ void __launch_bounds__(F_THREADS, 1) contract_tcf_kernel(const TcfArg
             case 4: tcf_mma_issue<4>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
             default: tcf_mma_issue<5>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
         }
-    } else if (warp == 2) {
-        // ------------------------------------------ producer: point rows per tile
-        uint32_t g = 0;
-        const uint32_t tb = F_NP * row_bytes;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-            const TcfUnit w = tcf_unit(a, u);
-            for (int64_t t = w.t0; t < w.t1; ++t, ++g) {
-                const uint32_t s = g % (uint32_t)SA;
-                if (g >= (uint32_t)SA) mbar_wait_sleep(&aempty[s], ((g / SA) - 1) & 1u);
-                expect_tx_elect(&afull[s], tb);
-                tma_load_elect(sA32 + (size_t)s * F_NP * dp, a.xr + (size_t)t * F_NP * dp, tb, &afull[s]);
-                __syncwarp();
-            }
-        }
     } else if (warp < F_EPI_WARP0) {
-        // ----------------------------- converters: one point (row r) per thread
-        const int r = tid - F_CONV_WARP0 * 32;
+        // ----- converters: thread (point r, chunk parity h) owns the 8-coordinate
+        // chunks cc = h, h + 2, ... of its point; x is prefetched one tile ahead
+        // into registers (coalesced loads of the tile-blocked dataset)
+        const int ct = tid - F_CONV_WARP0 * 32;
+        const int r = ct & (F_NP - 1), h = ct >> 7;
+        const int cd = d >> 3;  // chunk holding the threshold slot (K index d)
         uint32_t it = 0, gtile = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
-            const TcfUnit w = tcf_unit(a, u);
+        float xn[F_XCH][8];
+        int64_t u = blockIdx.x;
+        TcfUnit w{};
+        int64_t t = 0;
+        if (u < units) {
+            w = tcf_unit(a, u);
+            t = w.t0;
+            load_x_chunks(a.xb, t, d, r, h, xn);
+        }
+        for (; u < units;) {
             float* zs = sZ + (it & 1u) * 64;
-            if (r < 64) zs[r] = r < d ? __ldg(a.zq + (size_t)w.q * d + r) : 0.0f;
-            named_bar(2, F_CONV_WARPS * 32);
-            for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
-                const uint32_t s = gtile % (uint32_t)SA;
-                const uint32_t ps = gtile % F_P_STAGES;
-                mbar_wait(&afull[s], (gtile / SA) & 1u);
-                float4* row = reinterpret_cast<float4*>(sA32 + (size_t)s * F_NP * dp + (size_t)r * dp);
-                const float4* z4 = reinterpret_cast<const float4*>(zs);
-                float4 av[16];
-                float2 ss = make_float2(0.0f, 0.0f);
+            if (t == w.t0) {
+                if (ct < 64) zs[ct] = ct < d ? __ldg(a.zq + (size_t)w.q * d + ct) : 0.0f;
+                named_bar(2, F_CONV_THREADS);
+            }
+            // next tile (possibly of the next unit) for the prefetch
+            int64_t un = u, tn = t + 1;
+            TcfUnit wn = w;
+            if (tn >= w.t1) {
+                un = u + gridDim.x;
+                if (un < units) {
+                    wn = tcf_unit(a, un);
+                    tn = wn.t0;
+                }
+            }
+            float xc[F_XCH][8];
 #pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    if (c < dp4) {
-                        const float4 x = row[c], z = z4[c];
-                        // a = x - z (contract.cu: v.x -= zk), FP32 round to nearest
-                        float4 v;
-                        v.x = __fsub_rn(x.x, z.x);
-                        v.y = __fsub_rn(x.y, z.y);
-                        v.z = __fsub_rn(x.z, z.z);
-                        v.w = __fsub_rn(x.w, z.w);
-                        av[c] = v;
-                        ss = __ffma2_rn(make_float2(v.x, v.y), make_float2(v.x, v.y), ss);
-                        ss = __ffma2_rn(make_float2(v.z, v.w), make_float2(v.z, v.w), ss);
-                        row[c] = v;  // a kept for the refinement
+            for (int k = 0; k < F_XCH; ++k)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) xc[k][e] = xn[k][e];
+            if (un < units) load_x_chunks(a.xb, tn, d, r, h, xn);
+
+            const uint32_t s = gtile % (uint32_t)SA;
+            const uint32_t ps = gtile % F_P_STAGES;
+            // a = x - z (contract.cu: v.x -= zk), FP32 round to nearest; coordinates >= d are 0
+            float ss = 0.0f;
+#pragma unroll
+            for (int k = 0; k < F_XCH; ++k) {
+                const int cc = 2 * k + h;
+                if (8 * cc < d) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int l = 8 * cc + e;
+                        const float v = l < d ? __fsub_rn(xc[k][e], zs[l]) : 0.0f;
+                        xc[k][e] = v;
+                        ss = fmaf(v, v, ss);
                     }
                 }
-                const float nrm2 = ss.x + ss.y;
-                const bool real = t * F_NP + r < a.n;
-                const bool decisive = real && nrm2 > 0x1.0p-100f && nrm2 < 0x1.0p100f;
-                const float sc = decisive ? TCF_CB * rsqrtf(nrm2) : 0.0f;
-                const __half slot = __float2half_rn(real ? 1.0f : 4.0f);
-                if (gtile >= F_P_STAGES) mbar_wait(&pempty[ps], ((gtile / F_P_STAGES) - 1) & 1u);
-                unsigned char* P = sP + ps * stage_bytes + r * 16;
-                const float2 sc2 = make_float2(sc, sc);
-                // K-major chunks of 8 coordinates: [kk/8][point][8 fp16]; the slot at K index d
+            }
+            float* nrm = sNrm + (gtile & 1u) * 2 * F_NP;
+            nrm[h * F_NP + r] = ss;
+            if (gtile >= (uint32_t)SA) mbar_wait(&aempty[s], ((gtile / SA) - 1) & 1u);  // slot's refinements done
+            // a kept for the refinement: row r of the slot, [p][dp] row-major
+            float* arow = sA32 + (size_t)s * F_NP * dp + (size_t)r * dp;
 #pragma unroll
-                for (int cc = 0; cc < 9; ++cc) {
-                    if (8 * cc <= d) {
-                        const float4 v0 = av[2 * cc < 16 ? 2 * cc : 15], v1 = av[2 * cc + 1 < 16 ? 2 * cc + 1 : 15];
-                        float f[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-                        uint32_t h[4];
+            for (int k = 0; k < F_XCH; ++k) {
+                const int cc = 2 * k + h;
+                if (8 * cc < dp)
+                    *reinterpret_cast<float4*>(arow + 8 * cc) = make_float4(xc[k][0], xc[k][1], xc[k][2], xc[k][3]);
+                if (8 * cc + 4 < dp)
+                    *reinterpret_cast<float4*>(arow + 8 * cc + 4) = make_float4(xc[k][4], xc[k][5], xc[k][6], xc[k][7]);
+            }
+            named_bar(2, F_CONV_THREADS);  // both halves' |a|^2 visible
+            const float nrm2 = nrm[r] + nrm[F_NP + r];
+            const bool real = t * F_NP + r < a.n;
+            const bool decisive = real && nrm2 > 0x1.0p-100f && nrm2 < 0x1.0p100f;
+            const float sc = decisive ? TCF_CB * rsqrtf(nrm2) : 0.0f;
+            const __half slot = __float2half_rn(real ? 1.0f : 4.0f);
+            if (gtile >= F_P_STAGES) mbar_wait(&pempty[ps], ((gtile / F_P_STAGES) - 1) & 1u);
+            unsigned char* P = sP + ps * stage_bytes + r * 16;
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int c0 = 8 * cc + 2 * e;
-                            const float2 p = __fmul2_rn(make_float2(f[2 * e], f[2 * e + 1]), sc2);
-                            __half2 hv = __floats2half2_rn(c0 < d ? p.x : 0.0f, c0 + 1 < d ? p.y : 0.0f);
-                            if (c0 == d) hv.x = slot;
-                            if (c0 + 1 == d) hv.y = slot;
-                            h[e] = *reinterpret_cast<uint32_t*>(&hv);
+            for (int k = 0; k < F_MAXCH; ++k) {
+                const int cc = 2 * k + h;
+                if (cc <= cd) {
+                    uint32_t hw[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float x0 = k < F_XCH ? xc[k < F_XCH ? k : 0][2 * e] : 0.0f;
+                        const float x1 = k < F_XCH ? xc[k < F_XCH ? k : 0][2 * e + 1] : 0.0f;
+                        const float2 p = __fmul2_rn(make_float2(x0, x1), make_float2(sc, sc));
+                        __half2 hv = __floats2half2_rn(p.x, p.y);  // coordinates >= d: a = 0
+                        if (cc == cd) {
+                            if (8 * cc + 2 * e == d) hv.x = slot;
+                            if (8 * cc + 2 * e + 1 == d) hv.y = slot;
                         }
-                        *reinterpret_cast<uint4*>(P + cc * (F_NP * 16)) = make_uint4(h[0], h[1], h[2], h[3]);
+                        hw[e] = *reinterpret_cast<uint32_t*>(&hv);
                     }
+                    *reinterpret_cast<uint4*>(P + cc * (F_NP * 16)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
                 }
-                fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&pfull[ps]);
-                    mbar_arrive(&aconv[s]);
-                }
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&pfull[ps]);
+                mbar_arrive(&aconv[s]);
+            }
+            ++gtile;
+            if (t + 1 < w.t1) {
+                ++t;
+            } else {
+                u = un;
+                w = wn;
+                t = tn;
+                ++it;
             }
         }
     } else {
@@ -355,12 +408,11 @@ __global__ void __launch_bounds__(F_THREADS, 1) contract_tcf_kernel(const TcfArg
             mbar_wait(ufull, it & 1u);  // this unit's FP32 direction rows
             for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
                 const uint32_t s = gtile % (uint32_t)SA;
-                uint32_t amb[F_GB_MAX][4];
+                uint32_t alo[F_GB_MAX], ahi[F_GB_MAX];  // ambiguous points: bit 2k / 2k+1 = point k / 16+k (+32 in ahi)
                 int mine = 0;
 #pragma unroll
                 for (int b = 0; b < F_GB_MAX; ++b) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) amb[b][k] = 0u;
+                    alo[b] = ahi[b] = 0u;
                     if (b < w.nbg) {
                         const uint32_t buf = gacc % F_NACC;
                         mbar_wait(&tfull[buf], (gacc / F_NACC) & 1u);
@@ -376,6 +428,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) contract_tcf_kernel(const TcfArg
                         if (lane == 0) mbar_arrive(&tempty[buf]);
                         // bits (31, 30) of 16 accumulators per register: 1x negative,
                         // 01 positive, 00 ambiguous (value k at bits 2k+1, 2k)
+                        uint32_t am[4];
 #pragma unroll
                         for (int qd = 0; qd < 4; ++qd) {
                             uint32_t m = 0u;
@@ -385,10 +438,13 @@ __global__ void __launch_bounds__(F_THREADS, 1) contract_tcf_kernel(const TcfArg
                                 m = __funnelshift_l(v, m, 2);
                             }
                             cneg[b] += __popc(m & 0xAAAAAAAAu);
-                            const uint32_t am = ~(m | (m >> 1)) & 0x55555555u;
-                            amb[b][qd] = am;
-                            mine += __popc(am);
+                            am[qd] = ~(m | (m >> 1)) & 0x55555555u;
                         }
+                        alo[b] = am[0] | (am[1] << 1);
+                        ahi[b] = am[2] | (am[3] << 1);
+                        const int c = __popc(alo[b]) + __popc(ahi[b]);
+                        camb[b] += c;
+                        mine += c;
                     }
                 }
                 // ---- queue this tile's ambiguous pairs (all 8 warps share one queue)
@@ -405,23 +461,19 @@ __global__ void __launch_bounds__(F_THREADS, 1) contract_tcf_kernel(const TcfArg
                 const float* slotA = sA32 + (size_t)s * F_NP * dp;
 #pragma unroll
                 for (int b = 0; b < F_GB_MAX; ++b) {
-#pragma unroll
-                    for (int qd = 0; qd < 4; ++qd) {
-                        uint32_t am = amb[b][qd];
-                        camb[b] += __popc(am);
-                        while (am) {
-                            const int k = (__ffs(am) - 1) >> 1;
-                            am &= am - 1u;
-                            const int p = half * 64 + 16 * qd + k;
-                            if (base < F_QCAP) {
-                                sQ[base] = ((uint32_t)b << 16) | ((uint32_t)jl << 8) | (uint32_t)p;
-                            } else {  // queue full (degenerate data): refine in place
-                                const float y = refine_dot(slotA + (size_t)p * dp, sU32 + (size_t)(b * F_MD + jl) * dp, dp4);
-                                if (y < 0.0f) atomicAdd(&sCnt[(b * F_MD + jl) * 4 + 2], 1);
-                                else if (y > 0.0f) atomicAdd(&sCnt[(b * F_MD + jl) * 4 + 3], 1);
-                            }
-                            ++base;
+                    uint64_t mk = (uint64_t)alo[b] | ((uint64_t)ahi[b] << 32);
+                    while (mk) {
+                        const int tb = __ffsll((long long)mk) - 1;
+                        mk &= mk - 1ull;
+                        const int p = half * 64 + ((tb >> 5) << 5) + ((tb & 31) >> 1) + ((tb & 1) << 4);
+                        if (base < F_QCAP) {
+                            sQ[base] = ((uint32_t)b << 16) | ((uint32_t)jl << 8) | (uint32_t)p;
+                        } else {  // queue full (degenerate data): refine in place
+                            const float y = refine_dot(slotA + (size_t)p * dp, sU32 + (size_t)(b * F_MD + jl) * dp, dp4);
+                            if (y < 0.0f) atomicAdd(&sCnt[(b * F_MD + jl) * 4 + 2], 1);
+                            else if (y > 0.0f) atomicAdd(&sCnt[(b * F_MD + jl) * 4 + 3], 1);
                         }
+                        ++base;
                     }
                 }
                 named_bar(1, F_EPI_THREADS);  // the tile's queue is complete
@@ -472,7 +524,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) contract_tcf_kernel(const TcfArg
 // (gb, S_A) that fit shared memory: prefer 3 direction blocks per unit (fewer
 // conversions per tile) and 3 point-row slots (TMA latency hidden)
 static bool tcf_pick(int d, int& gb, int& sa) {
-    const int cand[][2] = {{3, 3}, {2, 3}, {3, 2}, {2, 2}, {1, 3}, {1, 2}};
+    const int cand[][2] = {{3, 3}, {2, 4}, {2, 3}, {1, 4}, {1, 3}, {1, 2}};
     for (const auto& c : cand) {
         const TcfSmem lay(d, c[0], c[1]);
         if (lay.total <= F_SMEM_LIMIT) {

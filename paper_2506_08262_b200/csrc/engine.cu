@@ -84,7 +84,6 @@ struct rrs_engine {
     // dataset
     DevBuf xb;
     DevBuf xmax;  // [tiles * BM] max_l |x_il| (wide tensor path, 64 < d <= 256)
-    DevBuf xr;    // [tiles * BM][tcf_dp(d)] row-major FP32 (filter-and-refine path, d <= 64)
     int64_t n = 0;
     int d = 0;
     int64_t tiles = 0;
@@ -266,7 +265,7 @@ ContractArgs contract_args(rrs_engine* e, const Plan& p, int Qb, int jb0, int jb
 int contract_halfspace(rrs_engine* e, const Plan& p, int Qb) {
     if (p.tcf) {
         TcfArgs t{};
-        t.xr = e->xr.as<float>();
+        t.xb = e->xb.as<float>();
         t.zq = e->zq.as<float>();
         t.uop = e->uop.as<unsigned char>();
         t.u32r = e->u32.as<float>();
@@ -619,10 +618,6 @@ static int set_dataset_common(rrs_engine* e, const double* xdev, int64_t n, int3
     const int64_t tiles = (n + BM - 1) / BM;
     CK(e->xb.ensure((size_t)tiles * d * BM * 4));
     CK(launch_block_dataset(xdev, e->xb.as<float>(), n, d, tiles, e->stream));
-    if (d <= TC_SLICE) {
-        CK(e->xr.ensure((size_t)tiles * BM * tcf_dp(d) * 4));
-        CK(launch_rows_dataset(xdev, e->xr.as<float>(), n, d, tiles, e->stream));
-    }
     if (d > TC_SLICE) {
         CK(e->xmax.ensure((size_t)tiles * BM * 4));
         CK(launch_row_absmax(e->xb.as<float>(), e->xmax.as<float>(), d, tiles, e->stream));

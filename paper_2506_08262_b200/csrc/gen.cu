@@ -811,24 +811,6 @@ cudaError_t launch_pack_tcf_operand(const double* u64, unsigned char* uop, float
     return cudaGetLastError();
 }
 
-// Row-major padded FP32 copy of the dataset for contract_tcf: [tiles * 128][dp],
-// zero rows past n and zero columns past d (x rounded to FP32 like block_dataset).
-__global__ void rows_dataset_kernel(const double* __restrict__ x, float* __restrict__ xr, int64_t n, int d,
-                                    int64_t tiles) {
-    const int dp = tcf_dp(d);
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= tiles * BM * dp) return;
-    const int64_t i = idx / dp;
-    const int c = (int)(idx - i * dp);
-    xr[idx] = (i < n && c < d) ? (float)x[i * d + c] : 0.0f;
-}
-
-cudaError_t launch_rows_dataset(const double* x, float* xr, int64_t n, int d, int64_t tiles, cudaStream_t st) {
-    const int64_t total = tiles * BM * tcf_dp(d);
-    rows_dataset_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(x, xr, n, d, tiles);
-    return cudaGetLastError();
-}
-
 // ------------------------------------------------------ drop-in API helpers --
 // directions.py:97-135 (_normal_rows / _unit_rows): row j (Philox index
 // index_base + j) holds `dim` normals from value addresses v_base.., a zero-norm

@@ -244,7 +244,8 @@ struct TcArgs {
 // [kk/8][row 128][8 fp16] per 128-direction block, ns = ceil((d+1)/16) steps.
 // The point operand is built in the kernel (b_l = fp16(a_l * TCF_CB / ||a||)).
 // FP32 rows for the exact refinement: directions u32 = (float)u64 as
-// [Qb][mpad][dp] and the dataset as [tiles * 128][dp], dp = d rounded up to 4.
+// [Qb][mpad][dp], dp = d rounded up to 4 (the points' a = x - z rows are
+// formed in the kernel).
 constexpr float TCF_SU = 1024.0f;
 constexpr float TCF_CB = 0.833333313f;  // TCF_SU * TCF_CB = 2^10 / 1.2: bound margin, see contract_tcf.cu
 __host__ __device__ inline int tcf_ns(int d) { return (d + 16) / 16; }
@@ -252,7 +253,7 @@ __host__ __device__ inline int tcf_dp(int d) { return (d + 3) & ~3; }
 __host__ __device__ inline int tcf_block_bytes(int d) { return tcf_ns(d) * 4096; }
 
 struct TcfArgs {
-    const float* xr;            // [tiles * 128][dp] row-major FP32 dataset (zero padding rows / columns)
+    const float* xb;            // [T][d][128] tile-blocked FP32 dataset (the FFMA kernel's layout)
     const float* zq;            // [Qb][d]
     const unsigned char* uop;   // [Qb][NB][tcf_block_bytes(d)] direction operand (hi layout)
     const float* u32r;          // [Qb][mpad][dp] FP32 direction rows
@@ -295,7 +296,6 @@ cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st);
 cudaError_t launch_contract_tcf(TcfArgs a, int sms, cudaStream_t st);  // filter and refine, d <= 64
 cudaError_t launch_pack_tcf_operand(const double* u64, unsigned char* uop, float* u32r, int Qb, int m, int NB,
                                     int mpad, int d, cudaStream_t st);
-cudaError_t launch_rows_dataset(const double* x, float* xr, int64_t n, int d, int64_t tiles, cudaStream_t st);
 cudaError_t launch_contract_tc2(TcArgs a, int sms, cudaStream_t st);  // 2-SM (cta_group::2) variant
 cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st);  // 64 < d <= 256 (contract_tcw.cu)
 cudaError_t launch_contract_tcs(TcsArgs a, int sms, cudaStream_t st);  // projection store, d <= 64
