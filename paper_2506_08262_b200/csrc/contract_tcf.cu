@@ -44,9 +44,11 @@
 //               the tile-blocked dataset), a = x - z into a ring of S_A row-major
 //               slots [128][dp] kept until the tile's refinement, ||a||^2
 //               (halves exchanged in shared memory), scale, FP16 operand;
-//   warps 10-17 epilogue: tcgen05.ld, 2-bit classification, counts, and the
-//               refinement of the tile's ambiguous pairs through a shared queue
-//               (all 8 warps share it, 32 pairs per warp instruction).
+//   warps 10-13 epilogue, one per TMEM lane quarter: tcgen05.ld, 2-bit
+//               classification, counts, and the refinement of the tile's
+//               ambiguous pairs through a shared queue (32 pairs per warp
+//               instruction); 14 warps in all, so that 128 registers fit
+//               (at most 4 warps per SM sub-partition).
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_common.cuh"
@@ -59,9 +61,9 @@ constexpr int F_CONV_WARP0 = 2;
 constexpr int F_CONV_WARPS = 8;                            // (point, half of the 8-coordinate chunks)
 constexpr int F_CONV_THREADS = F_CONV_WARPS * 32;
 constexpr int F_EPI_WARP0 = F_CONV_WARP0 + F_CONV_WARPS;  // 10
-constexpr int F_EPI_WARPS = 8;
+constexpr int F_EPI_WARPS = 4;                             // one per TMEM lane quarter, all 128 points
 constexpr int F_EPI_THREADS = F_EPI_WARPS * 32;
-constexpr int F_THREADS = (F_EPI_WARP0 + F_EPI_WARPS) * 32;  // 576
+constexpr int F_THREADS = (F_EPI_WARP0 + F_EPI_WARPS) * 32;  // 448: <= 4 warps per SM sub-partition
 constexpr int F_NP = 128;
 constexpr int F_MD = 128;
 constexpr int F_NACC = 3;
@@ -100,30 +102,32 @@ struct TcfSmem {
 
 struct TcfUnit {
     int q, grp, nbg;
-    int64_t t0, t1;
+    int t0, t1;  // point tiles [t0, t1)
 };
 
-__device__ __forceinline__ TcfUnit tcf_unit(const TcfArgs& a, int64_t u) {
+// 32-bit unit arithmetic (launch_contract_tcf checks that units and tiles fit)
+__device__ __forceinline__ TcfUnit tcf_unit(const TcfArgs& a, int u) {
     TcfUnit r;
-    const int64_t per_q = (int64_t)a.groups * a.chunks;
-    r.q = (int)(u / per_q);
-    const int64_t rem = u - (int64_t)r.q * per_q;
-    r.grp = (int)(rem / a.chunks);
-    const int64_t c = rem - (int64_t)r.grp * a.chunks;
+    const int per_q = a.groups * a.chunks;
+    r.q = u / per_q;
+    const int rem = u - r.q * per_q;
+    r.grp = rem / a.chunks;
+    const int c = rem - r.grp * a.chunks;
     r.nbg = a.NB - r.grp * a.gb < a.gb ? a.NB - r.grp * a.gb : a.gb;
-    r.t0 = c * a.tiles_per_chunk;
-    r.t1 = r.t0 + a.tiles_per_chunk < a.tiles ? r.t0 + a.tiles_per_chunk : a.tiles;
+    const int tpc = (int)a.tiles_per_chunk, T = (int)a.tiles;
+    r.t0 = c * tpc;
+    r.t1 = r.t0 + tpc < T ? r.t0 + tpc : T;
     return r;
 }
 
 template <int NS>
-__device__ __forceinline__ void tcf_mma_issue(const TcfArgs& a, int64_t units, unsigned char* sP, unsigned char* sD,
+__device__ __forceinline__ void tcf_mma_issue(const TcfArgs& a, int units, unsigned char* sP, unsigned char* sD,
                                               uint64_t* pfull, uint64_t* pempty, uint64_t* dfull, uint64_t* dempty,
                                               uint64_t* tfull, uint64_t* tempty, uint64_t* udone) {
     constexpr uint32_t stage_bytes = NS * 4096;
     const uint32_t idesc = (1u << 4) | ((uint32_t)(F_NP >> 3) << 17) | ((uint32_t)(F_MD >> 4) << 24);
     uint32_t it = 0, gtile = 0, gacc = 0, gph = 0;
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
         const TcfUnit w = tcf_unit(a, u);
         for (int b = 0; b < w.nbg; ++b, ++gph) {
             mbar_wait_sleep(dfull, gph & 1u);
@@ -132,7 +136,7 @@ __device__ __forceinline__ void tcf_mma_issue(const TcfArgs& a, int64_t units, u
             tmem_cp_dirblock(F_A_TMEM + 8u * NS * b, umma_desc(smem_u32(sD), 2048, 128), NS);
             mma_commit_elect(dempty);
         }
-        for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
+        for (int t = w.t0; t < w.t1; ++t, ++gtile) {
             const uint32_t s = gtile % F_P_STAGES;
             mbar_wait(&pfull[s], (gtile / F_P_STAGES) & 1u);
             tc_fence_after();
@@ -168,7 +172,7 @@ __device__ __forceinline__ float refine_dot(const float* arow, const float* urow
 
 // converter: x of the thread's chunks of tile t (K-major tile-blocked dataset),
 // one coalesced 128-byte load per coordinate and warp
-__device__ __forceinline__ void load_x_chunks(const float* __restrict__ xb, int64_t t, int d, int r, int h,
+__device__ __forceinline__ void load_x_chunks(const float* __restrict__ xb, int t, int d, int r, int h,
                                               float (&x)[F_XCH][8]) {
     const float* base = xb + (size_t)t * d * F_NP + r;
 #pragma unroll
@@ -182,7 +186,7 @@ __device__ __forceinline__ void load_x_chunks(const float* __restrict__ xb, int6
     }
 }
 
-__global__ void __maxnreg__(112) contract_tcf_kernel(const TcfArgs a) {
+__global__ void __launch_bounds__(F_THREADS, 1) contract_tcf_kernel(const TcfArgs a) {
     extern __shared__ __align__(1024) unsigned char tcf_raw[];
     unsigned char* sm = tcf_raw + ((1024u - (smem_u32(tcf_raw) & 1023u)) & 1023u);
     const int d = a.d, dp = tcf_dp(d), dp4 = dp / 4, ns = tcf_ns(d);
@@ -214,7 +218,7 @@ __global__ void __maxnreg__(112) contract_tcf_kernel(const TcfArgs a) {
     const uint32_t row_bytes = (uint32_t)lay.row_bytes;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t units = (int64_t)a.Qb * a.groups * a.chunks;
+    const int units = a.Qb * a.groups * a.chunks;
 
     for (int i = tid; i < F_P_STAGES * stage_bytes / 16; i += F_THREADS)
         reinterpret_cast<uint4*>(sP)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -254,7 +258,7 @@ __global__ void __maxnreg__(112) contract_tcf_kernel(const TcfArgs a) {
     if (warp == 0) {
         // ------------------------------ producer: direction blocks, then U32 rows
         uint32_t gph = 0, it = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
             const TcfUnit w = tcf_unit(a, u);
             const int b0 = w.grp * a.gb;
             const unsigned char* src = a.uop + ((size_t)w.q * a.NB + b0) * stage_bytes;
@@ -287,9 +291,9 @@ __global__ void __maxnreg__(112) contract_tcf_kernel(const TcfArgs a) {
         const int cd = d >> 3;  // chunk holding the threshold slot (K index d)
         uint32_t it = 0, gtile = 0;
         float xn[F_XCH][8];
-        int64_t u = blockIdx.x;
+        int u = blockIdx.x;
         TcfUnit w{};
-        int64_t t = 0;
+        int t = 0;
         if (u < units) {
             w = tcf_unit(a, u);
             t = w.t0;
@@ -302,7 +306,7 @@ __global__ void __maxnreg__(112) contract_tcf_kernel(const TcfArgs a) {
                 named_bar(2, F_CONV_THREADS);
             }
             // next tile (possibly of the next unit) for the prefetch
-            int64_t un = u, tn = t + 1;
+            int un = u, tn = t + 1;
             TcfUnit wn = w;
             if (tn >= w.t1) {
                 un = u + gridDim.x;
@@ -350,7 +354,7 @@ __global__ void __maxnreg__(112) contract_tcf_kernel(const TcfArgs a) {
             }
             named_bar(2, F_CONV_THREADS);  // both halves' |a|^2 visible
             const float nrm2 = nrm[r] + nrm[F_NP + r];
-            const bool real = t * F_NP + r < a.n;
+            const bool real = (int64_t)t * F_NP + r < a.n;
             const bool decisive = real && nrm2 > 0x1.0p-100f && nrm2 < 0x1.0p100f;
             const float sc = decisive ? TCF_CB * rsqrtf(nrm2) : 0.0f;
             const __half slot = __float2half_rn(real ? 1.0f : 4.0f);
@@ -394,57 +398,64 @@ __global__ void __maxnreg__(112) contract_tcf_kernel(const TcfArgs a) {
         }
     } else {
         // ------------------------------------------------------------ epilogue
-        const int ct = tid - F_EPI_WARP0 * 32;          // 0..255
+        const int ct = tid - F_EPI_WARP0 * 32;          // 0..127
         const int quarter = warp & 3;                   // TMEM lane quarter (32 directions)
-        const int half = (warp - F_EPI_WARP0) >> 2;     // 64-point half of the tile
         const int jl = 32 * quarter + lane;             // direction within the block
         const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
         uint32_t it = 0, gacc = 0, gtile = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
             const TcfUnit w = tcf_unit(a, u);
             int cneg[F_GB_MAX], camb[F_GB_MAX];
 #pragma unroll
             for (int b = 0; b < F_GB_MAX; ++b) cneg[b] = camb[b] = 0;
             mbar_wait(ufull, it & 1u);  // this unit's FP32 direction rows
-            for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
+            for (int t = w.t0; t < w.t1; ++t, ++gtile) {
                 const uint32_t s = gtile % (uint32_t)SA;
-                uint32_t alo[F_GB_MAX], ahi[F_GB_MAX];  // ambiguous points: bit 2k / 2k+1 = point k / 16+k (+32 in ahi)
+                // ambiguous points per block and 64-point half: bit 2k / 2k+1 of
+                // word 2 hf + (0|1) = point 64 hf + 32 (0|1) + k / + 16 + k
+                uint32_t amk[F_GB_MAX][4];
                 int mine = 0;
 #pragma unroll
                 for (int b = 0; b < F_GB_MAX; ++b) {
-                    alo[b] = ahi[b] = 0u;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) amk[b][k] = 0u;
                     if (b < w.nbg) {
                         const uint32_t buf = gacc % F_NACC;
                         mbar_wait(&tfull[buf], (gacc / F_NACC) & 1u);
                         ++gacc;
                         tc_fence_after();
-                        const uint32_t tb = lane_base + buf * F_NP + (uint32_t)(half * 64);
-                        uint32_t y0[32], y1[32];
-                        tmem_ld32(tb, y0);
-                        tmem_ld32(tb + 32, y1);
-                        tmem_wait_ld();
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&tempty[buf]);
-                        // bits (31, 30) of 16 accumulators per register: 1x negative,
-                        // 01 positive, 00 ambiguous (value k at bits 2k+1, 2k)
-                        uint32_t am[4];
 #pragma unroll
-                        for (int qd = 0; qd < 4; ++qd) {
-                            uint32_t m = 0u;
-#pragma unroll
-                            for (int k = 15; k >= 0; --k) {
-                                const uint32_t v = qd < 2 ? y0[16 * qd + k] : y1[16 * (qd - 2) + k];
-                                m = __funnelshift_l(v, m, 2);
+                        for (int hf = 0; hf < 2; ++hf) {
+                            const uint32_t tb = lane_base + buf * F_NP + (uint32_t)(hf * 64);
+                            uint32_t y0[32], y1[32];
+                            tmem_ld32(tb, y0);
+                            tmem_ld32(tb + 32, y1);
+                            tmem_wait_ld();
+                            if (hf == 1) {
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive(&tempty[buf]);
                             }
-                            cneg[b] += __popc(m & 0xAAAAAAAAu);
-                            am[qd] = ~(m | (m >> 1)) & 0x55555555u;
+                            // bits (31, 30) of 16 accumulators per register: 1x negative,
+                            // 01 positive, 00 ambiguous (value k at bits 2k+1, 2k)
+                            uint32_t am[4];
+#pragma unroll
+                            for (int qd = 0; qd < 4; ++qd) {
+                                uint32_t m = 0u;
+#pragma unroll
+                                for (int k = 15; k >= 0; --k) {
+                                    const uint32_t v = qd < 2 ? y0[16 * qd + k] : y1[16 * (qd - 2) + k];
+                                    m = __funnelshift_l(v, m, 2);
+                                }
+                                cneg[b] += __popc(m & 0xAAAAAAAAu);
+                                am[qd] = ~(m | (m >> 1)) & 0x55555555u;
+                            }
+                            amk[b][2 * hf] = am[0] | (am[1] << 1);
+                            amk[b][2 * hf + 1] = am[2] | (am[3] << 1);
+                            const int c = __popc(amk[b][2 * hf]) + __popc(amk[b][2 * hf + 1]);
+                            camb[b] += c;
+                            mine += c;
                         }
-                        alo[b] = am[0] | (am[1] << 1);
-                        ahi[b] = am[2] | (am[3] << 1);
-                        const int c = __popc(alo[b]) + __popc(ahi[b]);
-                        camb[b] += c;
-                        mine += c;
                     }
                 }
                 // ---- queue this tile's ambiguous pairs (all 8 warps share one queue)
@@ -461,19 +472,23 @@ __global__ void __maxnreg__(112) contract_tcf_kernel(const TcfArgs a) {
                 const float* slotA = sA32 + (size_t)s * F_NP * dp;
 #pragma unroll
                 for (int b = 0; b < F_GB_MAX; ++b) {
-                    uint64_t mk = (uint64_t)alo[b] | ((uint64_t)ahi[b] << 32);
-                    while (mk) {
-                        const int tb = __ffsll((long long)mk) - 1;
-                        mk &= mk - 1ull;
-                        const int p = half * 64 + ((tb >> 5) << 5) + ((tb & 31) >> 1) + ((tb & 1) << 4);
-                        if (base < F_QCAP) {
-                            sQ[base] = ((uint32_t)b << 16) | ((uint32_t)jl << 8) | (uint32_t)p;
-                        } else {  // queue full (degenerate data): refine in place
-                            const float y = refine_dot(slotA + (size_t)p * dp, sU32 + (size_t)(b * F_MD + jl) * dp, dp4);
-                            if (y < 0.0f) atomicAdd(&sCnt[(b * F_MD + jl) * 4 + 2], 1);
-                            else if (y > 0.0f) atomicAdd(&sCnt[(b * F_MD + jl) * 4 + 3], 1);
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        uint64_t mk = (uint64_t)amk[b][2 * hf] | ((uint64_t)amk[b][2 * hf + 1] << 32);
+                        while (mk) {
+                            const int tb = __ffsll((long long)mk) - 1;
+                            mk &= mk - 1ull;
+                            const int p = hf * 64 + ((tb >> 5) << 5) + ((tb & 31) >> 1) + ((tb & 1) << 4);
+                            if (base < F_QCAP) {
+                                sQ[base] = ((uint32_t)b << 16) | ((uint32_t)jl << 8) | (uint32_t)p;
+                            } else {  // queue full (degenerate data): refine in place
+                                const float y =
+                                    refine_dot(slotA + (size_t)p * dp, sU32 + (size_t)(b * F_MD + jl) * dp, dp4);
+                                if (y < 0.0f) atomicAdd(&sCnt[(b * F_MD + jl) * 4 + 2], 1);
+                                else if (y > 0.0f) atomicAdd(&sCnt[(b * F_MD + jl) * 4 + 3], 1);
+                            }
+                            ++base;
                         }
-                        ++base;
                     }
                 }
                 named_bar(1, F_EPI_THREADS);  // the tile's queue is complete
@@ -498,8 +513,8 @@ __global__ void __maxnreg__(112) contract_tcf_kernel(const TcfArgs a) {
                     atomicAdd(&sCnt[(b * F_MD + jl) * 4 + 1], camb[b]);
                 }
             named_bar(1, F_EPI_THREADS);
-            const int64_t r1 = w.t1 * F_NP < a.n ? w.t1 * F_NP : a.n;
-            const int valid = (int)(r1 - w.t0 * F_NP);
+            const int64_t r1 = (int64_t)w.t1 * F_NP < a.n ? (int64_t)w.t1 * F_NP : a.n;
+            const int valid = (int)(r1 - (int64_t)w.t0 * F_NP);
             int* dst = a.counts + (size_t)w.q * a.mpad * 2;
             const int j0 = w.grp * a.gb * F_MD;
             for (int c = ct; c < w.nbg * F_MD; c += F_EPI_THREADS) {
@@ -554,6 +569,7 @@ cudaError_t launch_contract_tcf(TcfArgs a, int sms, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     const int64_t units = (int64_t)a.Qb * a.groups * a.chunks;
     if (units == 0) return cudaSuccess;
+    if (units > INT32_MAX / 2 || a.tiles > INT32_MAX / 2) return cudaErrorInvalidValue;  // 32-bit unit math
     const int grid = (int)(units < sms ? units : sms);
     contract_tcf_kernel<<<grid, F_THREADS, lay.total, st>>>(a);
     return cudaGetLastError();
