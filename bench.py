@@ -240,7 +240,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process group for N>1 (gloo: ranks may share one GPU, the single-GPU rehearsal)")
-    ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "tensor2", "split"],
+    ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "tensor2", "filter"],
                     help="halfspace contraction kernel (auto: the library's choice)")
     args = ap.parse_args()
     wl = args.workload

@@ -89,8 +89,8 @@ struct rrs_engine {
     int64_t tiles = 0;
     // workspace
     DevBuf zq, u64, u32, uop, counts, depths, y, pole, reflv, reflmode, dmin, bestcnt;
-    // 0 auto, 1 FFMA (contract.cu), 2 tensor cores (contract_tcf.cu filter-and-refine for d <= 64,
-    // contract_tcw.cu above), 3 2-SM split (contract_tc2.cu), 4 two-term split (contract_tc.cu)
+    // 0 auto, 1 FFMA (contract.cu), 2 tensor cores (contract_tc.cu two-term split for d <= 64,
+    // contract_tcw.cu above), 3 2-SM split (contract_tc2.cu), 4 filter and refine (contract_tcf.cu, d <= 64)
     int contract_path = 0;
     DevBuf tmp_in, tmp_out0, tmp_out1, tmp_out2, tmp_out3;
     // timing
@@ -172,7 +172,7 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     p.nb8 = p.MB;
     const bool tc_ok = notion == RRS_HALFSPACE && e->d <= 256;
     p.tc = tc_ok && (e->contract_path >= 2 || (e->contract_path == 0 && e->n >= 4096));
-    p.tcf = p.tc && e->d <= TC_SLICE && (e->contract_path == 0 || e->contract_path == 2);
+    p.tcf = p.tc && e->d <= TC_SLICE && e->contract_path == 4;
     const bool tcs_ok = notion != RRS_HALFSPACE && tc6_layout(e->d).ns <= 19;
     // auto: the store is HBM-write bound at small d (y is n*m*4 bytes per query and
     // refinement whatever computes it), the tensor store pays from d ~ 32 (config 3)
@@ -578,7 +578,7 @@ int rrs_engine_set_contract_path(rrs_engine* e, int32_t path) {
     if (!e) return fail(RRS_ERR_INVALID, "engine is null");
     if (path < 0 || path > 4)
         return fail(RRS_ERR_INVALID,
-                    "contract path must be 0 (auto), 1 (FFMA), 2 (tensor), 3 (2-SM split) or 4 (two-term split)");
+                    "contract path must be 0 (auto), 1 (FFMA), 2 (tensor), 3 (2-SM split) or 4 (filter and refine)");
     e->contract_path = path;
     return RRS_OK;
 }

@@ -40,7 +40,7 @@ def test_filter_equals_ffma_config4_shape(b200, dist):
     Ucap = b200.generate_batch(b200.CapSpec(b200.Pole(pole), 0.2), 1000, seed=3, refinement=12).directions
     for z in (X[3], 0.3 * X[7], np.zeros(50), X[11] + 1e-3 * rng.standard_normal(50), X[5] * 1e-6):
         for D in (U, Ucap):
-            a = _counts(b200, "tensor", z, data, D)
+            a = _counts(b200, "filter", z, data, D)
             f = _counts(b200, "ffma", z, data, D)
             assert np.array_equal(a[0], f[0]) and np.array_equal(a[1], f[1])
 
@@ -52,7 +52,7 @@ def test_filter_equals_ffma_tie_heavy(b200):
     data = b200.Dataset(X)
     U = np.concatenate([np.eye(8), _unit(rng, 300, 8), np.ones((1, 8)) / np.sqrt(8)])
     for z in (X[0], X[700], np.zeros(8), np.full(8, 0.5)):
-        a = _counts(b200, "tensor", z, data, U)
+        a = _counts(b200, "filter", z, data, U)
         f = _counts(b200, "ffma", z, data, U)
         assert np.array_equal(a[0], f[0]) and np.array_equal(a[1], f[1])
 
@@ -65,7 +65,7 @@ def test_filter_all_dims(b200, d):
     data = b200.Dataset(X)
     U = _unit(rng, 300, d)  # a partial last direction block
     for z in (X[1], 0.5 * X[2], X[-1]):
-        a = _counts(b200, "tensor", z, data, U)
+        a = _counts(b200, "filter", z, data, U)
         f = _counts(b200, "ffma", z, data, U)
         assert np.array_equal(a[0], f[0]) and np.array_equal(a[1], f[1])
 
@@ -79,11 +79,11 @@ def test_filter_rrs_equals_ffma(b200):
     cfg = b200.RrsConfig(total_directions=4000, refinements=10, shrink=0.85, notion="halfspace", seed=2)
     eng = b200.engine()
     res = {}
-    for path in ("tensor", "ffma"):
+    for path in ("filter", "ffma"):
         eng.set_contract_path(path)
         try:
             res[path] = b200.depth_batch_arrays(Z, data, cfg)
         finally:
             eng.set_contract_path("auto")
     for i in range(4):
-        assert np.array_equal(res["tensor"][i], res["ffma"][i])
+        assert np.array_equal(res["filter"][i], res["ffma"][i])
