@@ -240,6 +240,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process group for N>1 (gloo: ranks may share one GPU, the single-GPU rehearsal)")
+    ap.add_argument("--select-path", default="auto", choices=["auto", "radix"],
+                    help="order-statistic kernel of the projection notions (A/B)")
     ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "tensor2", "filter"],
                     help="halfspace contraction kernel (auto: the library's choice)")
     args = ap.parse_args()
@@ -273,6 +275,7 @@ def main():
     X = make_data(distn, n, d)
     eng = rrs.engine(local)
     eng.set_contract_path(args.contract_path)
+    eng.set_select_path(args.select_path)
     stream = torch.cuda.Stream()  # one non-default stream shared by torch and the engine
     torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)

@@ -151,6 +151,12 @@ int rrs_philox4x32_host(rrs_engine* e, const uint32_t* ctr, int64_t N, uint32_t 
  * (contract_tc2.cu; wider d takes contract_tcw.cu). */
 int rrs_engine_set_contract_path(rrs_engine* e, int32_t path);
 
+/* Order-statistic kernel for the projection notions: 0 = auto (the
+ * sample-bracket select, select.cu v3, for 2048 <= n <= 53248; radix select
+ * elsewhere), 2 = radix select v2 everywhere.  Both give bitwise equal depths
+ * (same FP32 keys, FP64 midpoints); the switch exists for A/B measurement. */
+int rrs_engine_set_select_path(rrs_engine* e, int32_t path);
+
 /* Diagnostics for the last batch: device time (ms) of each stage summed over
  * the batch (generation, contraction, univariate, update) and launch count. */
 typedef struct {
@@ -159,6 +165,7 @@ typedef struct {
     int64_t contract_launches;
     double ms_contract_total; /* sum of contraction-kernel durations */
     int64_t tensor_contract_launches; /* of contract_launches, on the tcgen05 kernel */
+    int64_t select_rows_fallback; /* projection rows whose sample bracket missed (select v3) */
 } rrs_stats;
 int rrs_engine_stats(rrs_engine* e, rrs_stats* out);
 int rrs_engine_enable_timing(rrs_engine* e, int32_t on);

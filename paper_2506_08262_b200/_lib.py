@@ -48,6 +48,7 @@ class RrsStatsC(ctypes.Structure):
         ("contract_launches", ctypes.c_int64),
         ("ms_contract_total", ctypes.c_double),
         ("tensor_contract_launches", ctypes.c_int64),
+        ("select_rows_fallback", ctypes.c_int64),
     ]
 
 
@@ -89,6 +90,7 @@ SIGNATURES = [
     ("rrs_engine_stats", ctypes.c_int, [_vp, ctypes.POINTER(RrsStatsC)]),
     ("rrs_engine_enable_timing", ctypes.c_int, [_vp, ctypes.c_int32]),
     ("rrs_engine_set_contract_path", ctypes.c_int, [_vp, ctypes.c_int32]),
+    ("rrs_engine_set_select_path", ctypes.c_int, [_vp, ctypes.c_int32]),
 ]
 
 _lib = None
@@ -197,6 +199,13 @@ class Engine:
         and refine, contract_tcf.cu, d <= 64)."""
         code = {"auto": 0, "ffma": 1, "tensor": 2, "tensor2": 3, "filter": 4}[path]
         _raise(load_library().rrs_engine_set_contract_path(self._h, code))
+
+    def set_select_path(self, path: str):
+        """'auto' | 'radix' (order-statistic kernel of the projection notions:
+        auto = the sample-bracket select v3 where it applies, radix = select v2
+        everywhere; bitwise equal depths)."""
+        code = {"auto": 0, "radix": 2}[path]
+        _raise(load_library().rrs_engine_set_select_path(self._h, code))
 
     def enable_timing(self, on: bool = True):
         _raise(load_library().rrs_engine_enable_timing(self._h, 1 if on else 0))

@@ -29,6 +29,7 @@ SOURCES = {  # file -> extra flags
     "contract_tcw.cu": [],
     "contract_tcs.cu": [],
     "select.cu": [],
+    "center.cu": [],
     "api64.cu": [],
     "engine.cu": [],
 }

@@ -84,14 +84,20 @@ struct rrs_engine {
     // dataset
     DevBuf xb;
     DevBuf xmax;  // [tiles * BM] max_l |x_il| (wide tensor path, 64 < d <= 256)
+    // centred frame of the projection notions (center.cu): m, the FP32 blocked
+    // copy of x - m, and for n < STORE64_N the FP64 row-major copy of x - m
+    DevBuf center, xcb, xc64;
     int64_t n = 0;
     int d = 0;
     int64_t tiles = 0;
     // workspace
     DevBuf zq, u64, u32, uop, counts, depths, y, pole, reflv, reflmode, dmin, bestcnt;
+    DevBuf zq0, shift;  // projection notions: zero queries for the centred store, <u, m - z> per direction
     // 0 auto, 1 FFMA (contract.cu), 2 tensor cores (contract_tc.cu two-term split for d <= 64,
     // contract_tcw.cu above), 3 2-SM split (contract_tc2.cu), 4 filter and refine (contract_tcf.cu, d <= 64)
     int contract_path = 0;
+    int select_path = 0;  // 0 auto (select v3 where it applies), 2 radix select v2
+    DevBuf fallbacks;     // device counter of select-v3 rows that left their bracket
     DevBuf tmp_in, tmp_out0, tmp_out1, tmp_out2, tmp_out3;
     // timing
     bool timing = false;
@@ -159,6 +165,7 @@ struct Plan {
     bool tc;     // tensor-core contraction (halfspace, d <= 256; contract_tcw.cu for d > 64)
     bool tcf;    // ... by filter and refine (contract_tcf.cu, d <= 64; u32 holds FP32 rows)
     bool tcs;    // tensor-core projection store (projection notions, d <= 50; contract_tcs.cu)
+    bool store64;  // FP64-accumulated store (projection notions, n < STORE64_N, no tensor store; center.cu)
     int nb8;     // 128-direction blocks per query (tensor path operand, tc_block_bytes(d) each)
     int jchunk;  // direction blocks per store launch (projection notions)
     int tpu, chunks;
@@ -177,8 +184,9 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     // auto: the store is HBM-write bound at small d (y is n*m*4 bytes per query and
     // refinement whatever computes it), the tensor store pays from d ~ 32 (config 3)
     p.tcs = tcs_ok && (e->contract_path >= 2 || (e->contract_path == 0 && e->n >= 4096 && e->d >= 32));
+    p.store64 = notion != RRS_HALFSPACE && !p.tcs && e->n < STORE64_N;
     const int64_t d = e->d, n = e->n;
-    int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * tcf_dp((int)d) * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 8 +
+    int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * tcf_dp((int)d) * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 16 +
                     d * 40 + 64 +
                     (int64_t)p.nb8 * (p.tcs ? tc6_block_bytes(e->d) : p.tcf ? tcf_block_bytes(e->d) : tc_block_bytes(e->d));
     int64_t budget = e->ws_limit;
@@ -238,6 +246,9 @@ int ensure_ws(rrs_engine* e, const Plan& p, int notion) {
         CK(e->counts.ensure(8));
         CK(e->depths.ensure(Qb * p.m * 8));
         CK(e->y.ensure(Qb * (size_t)p.jchunk * BN * e->n * 4));
+        CK(e->shift.ensure(Qb * p.m * 8));
+        CK(e->zq0.ensure(Qb * d * 4));
+        CK(cudaMemsetAsync(e->zq0.p, 0, Qb * d * 4, e->stream));
     }
     return RRS_OK;
 }
@@ -307,16 +318,28 @@ int contract_halfspace(rrs_engine* e, const Plan& p, int Qb) {
     return RRS_OK;
 }
 
-// y -> per-direction depths for the projection notions, chunked over direction blocks
-int univariate_from_store(rrs_engine* e, const Plan& p, int Qb, int notion) {
+// y -> per-direction depths for the projection notions, chunked over direction
+// blocks.  The store works in the centred frame (center.cu): y' = <u, x - m>
+// from the centred copy and zero queries, the select adds <u, m - z> (FP64,
+// from the FP64 queries zdev [Qb][d]) to the median.
+int univariate_from_store(rrs_engine* e, const Plan& p, int Qb, int notion, const double* zdev) {
+    {
+        Timer t(e, 2);
+        CK(launch_direction_shift(e->u64.as<double>(), e->center.as<double>(), zdev, e->shift.as<double>(), Qb, p.m,
+                                  e->d, e->stream));
+        e->stats.kernel_launches++;
+    }
     for (int jb0 = 0; jb0 < p.MB; jb0 += p.jchunk) {
         const int jbn = (p.MB - jb0) < p.jchunk ? (p.MB - jb0) : p.jchunk;
         {
             Timer t(e, 1);
-            if (p.tcs) {
+            if (p.store64) {
+                CK(launch_store64(e->xc64.as<double>(), e->u64.as<double>(), e->y.as<float>(), e->n, e->d, Qb, p.m,
+                                  jb0 * BN, jbn * BN, e->stream));
+            } else if (p.tcs) {
                 TcsArgs c{};
-                c.xb = e->xb.as<float>();
-                c.zq = e->zq.as<float>();
+                c.xb = e->xcb.as<float>();
+                c.zq = e->zq0.as<float>();
                 c.uop = e->uop.as<unsigned char>();
                 c.y = e->y.as<float>();
                 c.n = e->n;
@@ -331,6 +354,8 @@ int univariate_from_store(rrs_engine* e, const Plan& p, int Qb, int notion) {
                 e->stats.tensor_contract_launches++;
             } else {
                 ContractArgs c = contract_args(e, p, Qb, jb0, jbn);
+                c.xb = e->xcb.as<float>();
+                c.zq = e->zq0.as<float>();
                 CK(launch_contract_store(c, e->stream));
             }
             e->stats.kernel_launches++;
@@ -347,6 +372,9 @@ int univariate_from_store(rrs_engine* e, const Plan& p, int Qb, int notion) {
             s.j0 = jb0 * BN;
             s.m = p.m;
             s.notion = notion;
+            s.shift = e->shift.as<double>();
+            s.variant = e->select_path;
+            s.fallbacks = e->fallbacks.as<unsigned>();
             CK(launch_select(s, e->stream));
             e->stats.kernel_launches++;
         }
@@ -358,9 +386,16 @@ void reset_stats(rrs_engine* e) {
     e->stats = rrs_stats{};
     e->ev_used = 0;
     e->marks.clear();
+    if (e->fallbacks.ensure(16) == cudaSuccess) cudaMemsetAsync(e->fallbacks.p, 0, 16, e->stream);
 }
 
 int collect_stats(rrs_engine* e) {
+    if (e->fallbacks.p) {
+        unsigned fb = 0;
+        CK(cudaMemcpyAsync(&fb, e->fallbacks.p, sizeof(fb), cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        e->stats.select_rows_fallback = fb;
+    }
     if (!e->timing) return RRS_OK;
     CK(cudaStreamSynchronize(e->stream));
     for (const auto& mk : e->marks) {
@@ -437,7 +472,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 e->stats.kernel_launches++;
                 e->stats.contract_launches++;
             } else {
-                if (int rc = univariate_from_store(e, p, Qb, cfg->notion)) return rc;
+                if (int rc = univariate_from_store(e, p, Qb, cfg->notion, zdev + b0 * d)) return rc;
             }
             {
                 Timer t(e, 3);
@@ -546,7 +581,8 @@ int rrs_engine_destroy(rrs_engine* e) {
     cudaStreamSynchronize(e->stream);
     for (DevBuf* b : {&e->xb, &e->xmax, &e->zq, &e->u64, &e->u32, &e->uop, &e->counts, &e->depths, &e->y, &e->pole,
                       &e->reflv, &e->reflmode, &e->dmin, &e->bestcnt, &e->tmp_in, &e->tmp_out0,
-                      &e->tmp_out1, &e->tmp_out2, &e->tmp_out3})
+                      &e->tmp_out1, &e->tmp_out2, &e->tmp_out3, &e->center, &e->xcb, &e->xc64, &e->zq0,
+                      &e->shift, &e->fallbacks})
         b->release();
     for (auto ev : e->ev_pool) cudaEventDestroy(ev);
     if (e->own) cudaStreamDestroy(e->own);
@@ -580,6 +616,13 @@ int rrs_engine_set_contract_path(rrs_engine* e, int32_t path) {
         return fail(RRS_ERR_INVALID,
                     "contract path must be 0 (auto), 1 (FFMA), 2 (tensor), 3 (2-SM split) or 4 (filter and refine)");
     e->contract_path = path;
+    return RRS_OK;
+}
+
+int rrs_engine_set_select_path(rrs_engine* e, int32_t path) {
+    if (!e) return fail(RRS_ERR_INVALID, "engine is null");
+    if (path != 0 && path != 2) return fail(RRS_ERR_INVALID, "select path must be 0 (auto) or 2 (radix select v2)");
+    e->select_path = path;
     return RRS_OK;
 }
 
@@ -618,6 +661,14 @@ static int set_dataset_common(rrs_engine* e, const double* xdev, int64_t n, int3
     const int64_t tiles = (n + BM - 1) / BM;
     CK(e->xb.ensure((size_t)tiles * d * BM * 4));
     CK(launch_block_dataset(xdev, e->xb.as<float>(), n, d, tiles, e->stream));
+    CK(e->center.ensure((size_t)d * 8));
+    CK(launch_center_sample(xdev, n, d, e->center.as<double>(), e->stream));
+    CK(e->xcb.ensure((size_t)tiles * d * BM * 4));
+    CK(launch_block_centered(xdev, e->center.as<double>(), e->xcb.as<float>(), n, d, tiles, e->stream));
+    if (n < STORE64_N) {
+        CK(e->xc64.ensure((size_t)n * d * 8));
+        CK(launch_center_copy64(xdev, e->center.as<double>(), e->xc64.as<double>(), n, d, e->stream));
+    }
     if (d > TC_SLICE) {
         CK(e->xmax.ensure((size_t)tiles * BM * 4));
         CK(launch_row_absmax(e->xb.as<float>(), e->xmax.as<float>(), d, tiles, e->stream));
@@ -748,7 +799,7 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
         }
         return RRS_OK;
     }
-    if (int rc = univariate_from_store(e, p, 1, notion)) return rc;
+    if (int rc = univariate_from_store(e, p, 1, notion, e->tmp_in.as<double>())) return rc;
     CK(cudaMemcpyAsync(out, e->depths.p, (size_t)m * 8, cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
     return RRS_OK;

@@ -276,6 +276,9 @@ struct SelectArgs {
     int j0;                  // first direction of the chunk
     int m;
     int notion;              // 1 projection, 2 asym projection
+    const double* shift;     // nullable [Qb][m]: y = y' + shift (centred frame, center.cu); med += shift
+    int variant;             // 0 auto (sample-bracket select where it applies), 2 radix select v2
+    unsigned* fallbacks;     // nullable device counter: rows that left the sample bracket (select v3)
 };
 
 cudaError_t launch_cap_generate(const GenArgs& a, cudaStream_t st);
@@ -292,6 +295,17 @@ cudaError_t launch_philox_words(const uint32_t* ctr, uint32_t* out, int64_t N, u
 cudaError_t launch_contract_count(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_contract_store(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
+// centred frame of the projection notions (center.cu)
+constexpr int64_t STORE64_N = 4096;  // below: FP64-accumulated store from an FP64 centred copy
+cudaError_t launch_center_sample(const double* x, int64_t n, int d, double* center, cudaStream_t st);
+cudaError_t launch_block_centered(const double* x, const double* center, float* xb, int64_t n, int d, int64_t tiles,
+                                  cudaStream_t st);
+cudaError_t launch_center_copy64(const double* x, const double* center, double* xc, int64_t n, int d,
+                                 cudaStream_t st);
+cudaError_t launch_direction_shift(const double* u64, const double* center, const double* z, double* shift, int Qb,
+                                   int m, int d, cudaStream_t st);
+cudaError_t launch_store64(const double* xc, const double* u64, float* y, int64_t n, int d, int Qb, int m, int j0,
+                           int jcount, cudaStream_t st);
 cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st);
 cudaError_t launch_contract_tcf(TcfArgs a, int sms, cudaStream_t st);  // filter and refine, d <= 64
 cudaError_t launch_pack_tcf_operand(const double* u64, unsigned char* uop, float* u32r, int Qb, int m, int NB,

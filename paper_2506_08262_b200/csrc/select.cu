@@ -249,14 +249,15 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(const SelectArgs a)
     // rows start 16-byte aligned when n % 4 == 0 (y is [Qb][jcount][n] floats)
     const bool al = (n & 3) == 0;
     const double med = block_median(src, n, n, KeyMed{}, sh, al);
+    const double medz = med + (a.shift ? a.shift[(size_t)q * a.m + j] : 0.0);  // med(y) - 0 (centred frame)
     double depth;
     if (a.notion == 1) {
         const double mad = block_median(src, n, n, KeyAbsDev{med}, sh, al);
-        const double dev = fabs(med);
+        const double dev = fabs(medz);
         if (mad == 0.0) depth = (dev == 0.0) ? 1.0 : 0.0;
         else depth = 1.0 / (1.0 + dev / mad);
     } else {
-        const double dev = -med;
+        const double dev = -medz;
         if (dev <= 0.0) {
             depth = 1.0;
         } else {
@@ -615,6 +616,7 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
     kmin = block_reduce_min(kmin, sh);
     kmax = ~block_reduce_min(~kmax, sh);
     const double med = sel2_median(keys, n, (uint32_t)n, kmin, kmax, sh, SEL2_PRE, cbuf);
+    const double medz = med + (a.shift ? a.shift[(size_t)q * a.m + j] : 0.0);  // med(y) - 0 (centred frame)
     double depth;
     if (a.notion == 1) {
         // MAD: keys of |y - med| (FP64 deviation, FP32 key), in place
@@ -631,11 +633,11 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
         dmin = block_reduce_min(dmin, sh);
         dmax = ~block_reduce_min(~dmax, sh);
         const double mad = sel2_median(keys, n, (uint32_t)n, dmin, dmax, sh, SEL2_PRE, cbuf);
-        const double dev = fabs(med);
+        const double dev = fabs(medz);
         if (mad == 0.0) depth = (dev == 0.0) ? 1.0 : 0.0;
         else depth = 1.0 / (1.0 + dev / mad);
     } else {
-        const double dev = -med;
+        const double dev = -medz;
         if (dev <= 0.0) {
             depth = 1.0;
         } else {
@@ -671,6 +673,492 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
     if (threadIdx.x == 0) a.depths[(size_t)q * a.m + j] = depth;
 }
 
+// ---------------------------------------------------------------- K3 v3 --
+// Sample-bracket select (Floyd-Rivest).  The row is never copied: every pass
+// streams the projections y (FP32) from L2 / HBM and turns them into keys on
+// the fly.
+//   1. One warp sorts 256 keys taken at strided positions (register bitonic,
+//      8 keys per lane); for a target rank R of n keys the sample order
+//      statistics at R·S/n -/+ ~3 sigma give a bracket [lo, hi].
+//   2. ONE branch-free pass over the row counts the keys below lo (per-thread
+//      counters) and appends the keys inside the bracket to per-thread
+//      shared-memory slots (slot c of thread t at c·NT + t: bank-conflict
+//      free, no ballots, no atomics).
+//   3. The slots are compacted into one contiguous array (block scan of the
+//      per-thread counts) and rank R - #below is selected there by v2's radix
+//      passes (16-byte loads, per-warp histograms), starting below the common
+//      prefix of lo and hi.
+// Projection depth: median (pass 1), MAD (pass 2: the bracket comes from the
+// sample's deviations, ranked by a merge of the two monotone halves).
+// Asymmetric projection depth: median (pass 1), then the positive-deviation
+// median is the key at global rank c_le(med) + (npos-1)/2 of the SAME keys
+// (rounding y - med to FP32 is monotone in y), so pass 2 brackets that rank.
+// A row whose target leaves its bracket (or whose thread overflows its
+// slots) falls back to full radix passes over the row; counted in
+// a.fallbacks.  The arithmetic is v2's (FP32 keys, FP64 midpoints /
+// deviations), so v2 and v3 give bitwise equal depths.
+// sample size: one warp sorts it (8 / 16 keys per lane); the larger sample of
+// the 1024-thread variant narrows the bracket so 1024 threads' slots rarely overflow
+template <int NT>
+struct Sel3Cfg {
+    static constexpr int S = NT >= 1024 ? 512 : 256;
+    static constexpr double SIGMAS = NT >= 1024 ? 5.0 : 4.0;  // slot headroom
+};
+constexpr int SMAX = 512;
+constexpr int64_t SEL3_MIN_N = 2048;
+constexpr int64_t SEL3_MAX_N = 53248;
+
+template <int NT>
+struct Sel3Shared {
+    static constexpr int W = NT / 32;
+    alignas(16) uint32_t hist[2048];
+    alignas(16) uint32_t sorted[Sel3Cfg<NT>::S];  // sorted sample keys (deviation keys for the MAD)
+    uint32_t sdev[Sel3Cfg<NT>::S];
+    uint32_t tiny[32];
+    uint32_t wsum[W];
+    uint32_t s_bin, s_below, s_cnt, s_ntiny, s_ovf, s_res, s_cle;
+};
+
+template <int NT>
+__device__ __forceinline__ uint32_t s3_reduce_add(uint32_t v, Sel3Shared<NT>& sh) {
+    v = __reduce_add_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0) sh.wsum[threadIdx.x >> 5] = v;
+    __syncthreads();
+    uint32_t r = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) r += sh.wsum[w];
+    __syncthreads();
+    return r;
+}
+template <int NT>
+__device__ __forceinline__ uint32_t s3_reduce_min(uint32_t v, Sel3Shared<NT>& sh) {
+    v = __reduce_min_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0) sh.wsum[threadIdx.x >> 5] = v;
+    __syncthreads();
+    uint32_t r = 0xFFFFFFFFu;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) r = min(r, sh.wsum[w]);
+    __syncthreads();
+    return r;
+}
+
+// every thread calls f(y) for its share of the row (16-byte loads when aligned,
+// four in flight)
+template <int NT, typename F>
+__device__ __forceinline__ void s3_row_each(const float* __restrict__ row, int n, F&& f) {
+    if ((n & 3) == 0) {
+        const float4* r4 = reinterpret_cast<const float4*>(row);
+        const int n4 = n >> 2;
+        int i = threadIdx.x;
+        for (; i + 3 * NT < n4; i += 4 * NT) {
+            const float4 v0 = __ldg(r4 + i), v1 = __ldg(r4 + i + NT), v2 = __ldg(r4 + i + 2 * NT),
+                         v3 = __ldg(r4 + i + 3 * NT);
+            f(v0.x), f(v0.y), f(v0.z), f(v0.w);
+            f(v1.x), f(v1.y), f(v1.z), f(v1.w);
+            f(v2.x), f(v2.y), f(v2.z), f(v2.w);
+            f(v3.x), f(v3.y), f(v3.z), f(v3.w);
+        }
+        for (; i < n4; i += NT) {
+            const float4 v = __ldg(r4 + i);
+            f(v.x), f(v.y), f(v.z), f(v.w);
+        }
+    } else {
+        for (int i = threadIdx.x; i < n; i += NT) f(__ldg(row + i));
+    }
+}
+
+// contiguous shared-memory keys [0, cnt): 16-byte loads (cand is 16-byte aligned)
+template <int NT, typename F>
+__device__ __forceinline__ void s3_arr_each(const uint32_t* __restrict__ cand, int cnt, F&& f) {
+    const uint4* c4 = reinterpret_cast<const uint4*>(cand);
+    const int n4 = cnt >> 2;
+    for (int i = threadIdx.x; i < n4; i += NT) {
+        const uint4 v = c4[i];
+        f(v.x), f(v.y), f(v.z), f(v.w);
+    }
+    for (int i = 4 * n4 + threadIdx.x; i < cnt; i += NT) f(cand[i]);
+}
+
+// t-th smallest (0-based) of the keys enumerated by each(f), all of which lie
+// in [lo, hi] (total of them: count); c_le = number of them <= the result.
+// Histograms of 11-bit digits of the offset key - lo in shared memory (one
+// 2048-bin histogram, predicated red.shared), starting at the top bit of
+// hi - lo; once the chosen bin holds <= 32 keys they are gathered and one warp
+// ranks them.
+template <int NT, typename Each>
+__device__ uint32_t s3_kth(Each&& each, uint32_t t, uint32_t lo, uint32_t hi, uint32_t count, Sel3Shared<NT>& sh,
+                           uint32_t& c_le) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int PER = 2048 / NT;  // bins per thread in the scan
+    uint32_t base = lo, span = hi - lo, below = 0, wcnt = count;
+    for (;;) {
+        if (span == 0u) {  // one key value left in the window
+            c_le = below + wcnt;
+            return base;
+        }
+        if (wcnt <= 32u) {
+            // gather the window's keys, rank them in one warp
+            if (tid == 0) sh.s_ntiny = 0u;
+            __syncthreads();
+            each([&](uint32_t key) {
+                if (key - base <= span) sh.tiny[atomicAdd(&sh.s_ntiny, 1u)] = key;
+            });
+            __syncthreads();
+            if (warp == 0) {
+                const uint32_t mine = (uint32_t)lane < wcnt ? sh.tiny[lane] : 0xFFFFFFFFu;
+                uint32_t lt = 0, eq_before = 0, le = 0;
+                for (int j2 = 0; j2 < (int)wcnt; ++j2) {
+                    const uint32_t o = __shfl_sync(0xffffffffu, mine, j2);
+                    lt += o < mine;
+                    eq_before += (o == mine && j2 < lane);
+                }
+                const uint32_t rank = lt + eq_before;
+                if ((uint32_t)lane < wcnt && rank == t) sh.s_res = mine;
+                __syncwarp();
+                const uint32_t res = sh.s_res;
+                for (int j2 = 0; j2 < (int)wcnt; ++j2) le += __shfl_sync(0xffffffffu, mine, j2) <= res;
+                if (lane == 0) sh.s_cle = below + le;
+            }
+            __syncthreads();
+            c_le = sh.s_cle;
+            return sh.s_res;
+        }
+        const int bits = 32 - __clz(span);
+        const int shift = bits > 11 ? bits - 11 : 0;
+        {
+            uint4* h4 = reinterpret_cast<uint4*>(sh.hist);
+            for (int i = tid; i < 512; i += NT) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        __syncthreads();
+        const uint32_t hbase = smem_u32(sh.hist);
+        each([&](uint32_t key) {
+            const uint32_t off = key - base;
+            const uint32_t addr = hbase + ((off >> shift) << 2);
+            asm volatile("{\n.reg .pred p;\nsetp.le.u32 p, %0, %1;\n@p red.shared.add.u32 [%2], 1;\n}\n" ::"r"(off),
+                         "r"(span), "r"(addr)
+                         : "memory");
+        });
+        __syncthreads();
+        // exclusive scan over the 2048 bins (PER consecutive bins per thread)
+        uint32_t hv[PER];
+        uint32_t local = 0;
+#pragma unroll
+        for (int b = 0; b < PER; ++b) {
+            hv[b] = sh.hist[tid * PER + b];
+            local += hv[b];
+        }
+        uint32_t incl = local;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += o;
+        }
+        if (lane == 31) sh.wsum[warp] = incl;
+        __syncthreads();
+        uint32_t run = incl - local;
+        for (int w = 0; w < warp; ++w) run += sh.wsum[w];
+        if (run <= t && t < run + local) {
+#pragma unroll
+            for (int b = 0; b < PER; ++b) {
+                if (run <= t && t < run + hv[b]) {
+                    sh.s_bin = (uint32_t)(tid * PER + b);
+                    sh.s_below = run;
+                    sh.s_cnt = hv[b];
+                }
+                run += hv[b];
+            }
+        }
+        __syncthreads();
+        const uint32_t bin = sh.s_bin;
+        t -= sh.s_below;
+        below += sh.s_below;
+        wcnt = sh.s_cnt;
+        const uint32_t start = bin << shift;
+        base += start;
+        span = min(span - start, (shift ? (1u << shift) : 1u) - 1u);
+        __syncthreads();
+    }
+}
+
+// bitonic sort (one warp) of 32·E keys held E per lane (index lane·E + e)
+template <int E>
+__device__ __forceinline__ void s3_sort_warp(uint32_t (&v)[E], int lane) {
+    const int l8 = lane * E;
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= E) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, v[e], j / E);
+                    const bool keep_min = ((l8 & j) == 0) == (((l8 + e) & k) == 0);
+                    v[e] = keep_min ? min(v[e], o) : max(v[e], o);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if ((e & j) == 0) {
+                        const bool up = ((l8 + e) & k) == 0;
+                        const uint32_t a = v[e], b = v[e | j];
+                        const uint32_t mn = min(a, b), mx = max(a, b);
+                        v[e] = up ? mn : mx;
+                        v[e | j] = up ? mx : mn;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// bracket [lo, hi] of population ranks [R, R2] of N keys from a sorted sample of S
+template <int S>
+__device__ __forceinline__ void s3_bracket(const uint32_t* sorted, uint32_t R, uint32_t R2, uint32_t N, uint32_t& lo,
+                                           uint32_t& hi) {
+    const float p = ((float)R + 0.5f) / (float)N;
+    const float M = 3.0f * sqrtf((float)S * fmaxf(p * (1.0f - p), 1.0f / S)) + 2.0f;
+    const float ra = ((float)R + 0.5f) * S / (float)N - 0.5f - M;
+    const float rb = ((float)R2 + 0.5f) * S / (float)N - 0.5f + M;
+    const int a = (int)floorf(ra), b = (int)ceilf(rb);
+    lo = a < 0 ? 0u : sorted[a];
+    hi = b >= S ? 0xFFFFFFFFu : sorted[b];
+}
+
+// keys at ranks R and R + 1 (if need_next) of the n keys kf(y) over the row;
+// c_le = number of keys <= key(R).  Returns false when the bracket missed or
+// a thread's slots overflowed (the caller falls back).
+template <int NT, typename KF>
+__device__ bool s3_select(const float* __restrict__ row, int n, KF kf, uint32_t R, bool need_next, uint32_t lo,
+                          uint32_t hi, uint32_t* slots, int cap, uint32_t* cand, Sel3Shared<NT>& sh, uint32_t& kR,
+                          uint32_t& kN, uint32_t& c_le) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t span = hi - lo;
+    uint32_t below = 0;
+    const uint32_t a0 = smem_u32(slots + tid);
+    // slot overflow goes to one scratch slot past the thread's last one
+    const uint32_t alim = a0 + (uint32_t)cap * NT * 4u;
+    uint32_t addr = a0;
+    __syncthreads();  // the previous selection's readers of the slots / candidates are done
+    s3_row_each<NT>(row, n, [&](float y) {
+        const uint32_t key = kf(y);
+        asm volatile(
+            "{\n.reg .pred pin, plo;\n.reg .u32 off, a;\n"
+            "sub.u32 off, %2, %3;\n"
+            "setp.le.u32 pin, off, %4;\n"
+            "setp.lt.u32 plo, %2, %3;\n"
+            "@plo add.u32 %0, %0, 1;\n"
+            "min.u32 a, %1, %5;\n"
+            "@pin st.shared.u32 [a], %2;\n"
+            "@pin add.u32 %1, %1, %6;\n}\n"
+            : "+r"(below), "+r"(addr)
+            : "r"(key), "r"(lo), "r"(span), "r"(alim), "r"((uint32_t)(NT * 4))
+            : "memory");
+    });
+    const uint32_t c = (addr - a0) / (NT * 4u);
+    const bool ovf = c > (uint32_t)cap;
+    // block exclusive scan of the per-thread candidate counts (c <= n < 2^16)
+    // with the below counts packed in the high half (n < 2^16)
+    const uint32_t v = (below << 16) | c;
+    uint32_t incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    const unsigned ovw = __ballot_sync(0xffffffffu, ovf);
+    if (lane == 31) sh.wsum[warp] = incl;
+    if (lane == 0 && ovw) sh.s_ovf = 1u;
+    __syncthreads();
+    uint32_t woff = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+        const uint32_t t = sh.wsum[w];
+        woff += w < warp ? t : 0u;
+        total += t;
+    }
+    const uint32_t c_lo = total >> 16, c_mid = total & 0xFFFFu;
+    const bool overflow = sh.s_ovf != 0u;
+    if (overflow || R < c_lo || R >= c_lo + c_mid) return false;  // block-uniform
+    // compact the slots into one contiguous array
+    const uint32_t off = (woff + incl - v) & 0xFFFFu;
+    for (uint32_t i = 0; i < c; ++i) cand[off + i] = slots[(size_t)i * NT + tid];
+    __syncthreads();
+    const auto each = [&](auto&& f) { s3_arr_each<NT>(cand, (int)c_mid, f); };
+    uint32_t cl;
+    kR = s3_kth<NT>(each, R - c_lo, lo, hi, c_mid, sh, cl);
+    c_le = c_lo + cl;
+    kN = kR;
+    if (need_next && c_le < R + 2) {
+        uint32_t best = 0xFFFFFFFFu;
+        if (R + 1 >= c_lo + c_mid) {  // the next key lies above the bracket
+            s3_row_each<NT>(row, n, [&](float y) {
+                const uint32_t k2 = kf(y);
+                best = min(best, k2 > hi ? k2 : 0xFFFFFFFFu);
+            });
+        } else {
+            each([&](uint32_t k2) { best = min(best, k2 > kR ? k2 : 0xFFFFFFFFu); });
+        }
+        kN = s3_reduce_min<NT>(best, sh);
+    }
+    return true;
+}
+
+struct S3KeyY {
+    __device__ __forceinline__ uint32_t operator()(float y) const { return fkey(y); }
+};
+struct S3KeyAbsDev {
+    double med;
+    __device__ __forceinline__ uint32_t operator()(float y) const { return fkey((float)fabs((double)y - med)); }
+};
+
+template <int NT, typename KF>
+__device__ __forceinline__ void s3_rank(const float* row, int n, KF kf, uint32_t R, bool need_next,
+                                        const uint32_t* sorted, uint32_t* slots, int cap, uint32_t* cand,
+                                        Sel3Shared<NT>& sh, uint32_t& kR, uint32_t& kN, uint32_t& c_le,
+                                        unsigned* fallbacks) {
+    uint32_t lo, hi;
+    s3_bracket<Sel3Cfg<NT>::S>(sorted, R, need_next ? R + 1 : R, (uint32_t)n, lo, hi);
+    if (!s3_select<NT>(row, n, kf, R, need_next, lo, hi, slots, cap, cand, sh, kR, kN, c_le)) {
+        if (fallbacks && threadIdx.x == 0) atomicAdd(fallbacks, 1u);
+        __syncthreads();
+        if (threadIdx.x == 0) sh.s_ovf = 0u;
+        const auto each = [&](auto&& f) { s3_row_each<NT>(row, n, [&](float y) { f(kf(y)); }); };
+        kR = s3_kth<NT>(each, R, 0u, 0xFFFFFFFFu, (uint32_t)n, sh, c_le);
+        kN = kR;
+        if (need_next && c_le < R + 2) {
+            uint32_t best = 0xFFFFFFFFu;
+            each([&](uint32_t k2) { best = min(best, k2 > kR ? k2 : 0xFFFFFFFFu); });
+            kN = s3_reduce_min<NT>(best, sh);
+        }
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) select_v3_kernel(const SelectArgs a, int cap) {
+    extern __shared__ __align__(16) unsigned char sel3_raw[];
+    Sel3Shared<NT>& sh = *reinterpret_cast<Sel3Shared<NT>*>(sel3_raw);
+    const int jj = blockIdx.x;
+    const int q = blockIdx.y;
+    const int j = a.j0 + jj;
+    if (j >= a.m) return;
+    const int tid = threadIdx.x;
+    const int n = (int)a.n;
+    const float* row = a.y + ((size_t)q * a.jcount + jj) * a.n;
+    uint32_t* slots = reinterpret_cast<uint32_t*>(sel3_raw + ((sizeof(Sel3Shared<NT>) + 15) & ~size_t(15)));
+    uint32_t* cand = slots + (size_t)(cap + 1) * NT;  // 16-byte aligned: NT is a multiple of 4
+
+    // sample: S strided keys of y, sorted by warp 0
+    constexpr int S = Sel3Cfg<NT>::S, E = S / 32;
+    if (tid < 32) {
+        uint32_t v[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            v[e] = fkey(__ldg(row + (int)(((int64_t)(2 * (tid * E + e) + 1) * n) / (2 * S))));
+        s3_sort_warp<E>(v, tid);
+        uint4* s4 = reinterpret_cast<uint4*>(sh.sorted + tid * E);
+#pragma unroll
+        for (int e = 0; e < E; e += 4) s4[e / 4] = make_uint4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+        if (tid == 0) sh.s_ovf = 0u;
+    }
+    __syncthreads();
+
+    // median of y (v2: midpoint of the central pair, FP64)
+    const uint32_t k = (uint32_t)(n - 1) >> 1;
+    const bool even = (n & 1) == 0;
+    uint32_t kR, kN, c_le;
+    s3_rank<NT>(row, n, S3KeyY{}, k, even, sh.sorted, slots, cap, cand, sh, kR, kN, c_le, a.fallbacks);
+    const double lov = (double)kfloat(kR);
+    const double med = even ? (lov + (double)kfloat(kN)) / 2.0 : lov;
+    const double medz = med + (a.shift ? a.shift[(size_t)q * a.m + j] : 0.0);  // med(y) - 0 (centred frame)
+
+    double depth;
+    if (a.notion == 1) {
+        // sample deviations: non-increasing over the sample's keys <= med,
+        // non-decreasing above; rank each by a binary search in the other half
+        uint32_t dk = 0u, le = 0u;
+        if (tid < S) {
+            const double yv = (double)kfloat(sh.sorted[tid]);
+            dk = fkey((float)fabs(yv - med));
+            le = yv <= med ? 1u : 0u;
+            sh.sdev[tid] = dk;
+        }
+        const uint32_t nl = s3_reduce_add<NT>(le, sh);  // also orders the sdev writes
+        if (tid < S) {
+            uint32_t rank;
+            if ((uint32_t)tid < nl) {
+                // # of upper-half deviations < dk (sdev[nl..S) non-decreasing)
+                uint32_t lo_i = nl, hi_i = S;
+                while (lo_i < hi_i) {
+                    const uint32_t mid = (lo_i + hi_i) >> 1;
+                    if (sh.sdev[mid] < dk) lo_i = mid + 1;
+                    else hi_i = mid;
+                }
+                rank = (nl - 1 - tid) + (lo_i - nl);
+            } else {
+                // # of lower-half deviations <= dk (sdev[0..nl) non-increasing: a suffix)
+                uint32_t lo_i = 0, hi_i = nl;
+                while (lo_i < hi_i) {
+                    const uint32_t mid = (lo_i + hi_i) >> 1;
+                    if (sh.sdev[mid] <= dk) hi_i = mid;
+                    else lo_i = mid + 1;
+                }
+                rank = (tid - nl) + (nl - lo_i);
+            }
+            sh.sorted[rank] = dk;  // the sample's keys are dead after the median
+        }
+        __syncthreads();
+        uint32_t mR, mN, mc;
+        s3_rank<NT>(row, n, S3KeyAbsDev{med}, k, even, sh.sorted, slots, cap, cand, sh, mR, mN, mc, a.fallbacks);
+        const double mlo = (double)kfloat(mR);
+        const double mad = even ? (mlo + (double)kfloat(mN)) / 2.0 : mlo;
+        const double dev = fabs(medz);
+        if (mad == 0.0) depth = (dev == 0.0) ? 1.0 : 0.0;
+        else depth = 1.0 / (1.0 + dev / mad);
+    } else {
+        const double dev = -medz;
+        // y > med  <=>  key(y) > kR (no key lies strictly between kR and kN)
+        const uint32_t npos = (uint32_t)n - c_le;
+        if (dev <= 0.0) {
+            depth = 1.0;
+        } else if (npos == 0u) {
+            depth = 0.0;
+        } else {
+            // median of the positive deviations: keys at global ranks
+            // c_le + (npos-1)/2 (and + 1 for even npos) of the same y keys
+            const uint32_t A = c_le + ((npos - 1u) >> 1);
+            const bool pe = (npos & 1u) == 0u;
+            uint32_t aR, aN, ac;
+            s3_rank<NT>(row, n, S3KeyY{}, A, pe, sh.sorted, slots, cap, cand, sh, aR, aN, ac, a.fallbacks);
+            const double ta = (double)(float)((double)kfloat(aR) - med);
+            const double madp = pe ? (ta + (double)(float)((double)kfloat(aN) - med)) / 2.0 : ta;
+            depth = 1.0 / (1.0 + dev / madp);
+        }
+    }
+    if (tid == 0) a.depths[(size_t)q * a.m + j] = depth;
+}
+
+// candidate slots per thread: mean + 4 sigma of a ~21 % bracket over the
+// thread's share of the row (an overflowing row falls back)
+template <int NT>
+static int sel3_cap(int64_t n) {
+    const double kpt = (n % 4 == 0) ? 4.0 * (double)((n / 4 + NT - 1) / NT) : (double)((n + NT - 1) / NT);
+    const double S = Sel3Cfg<NT>::S;
+    const double f = (6.0 * sqrt(S * 0.25) + 6.0) / S;  // bracket share of the row at p = 1/2
+    const double mean = kpt * f;
+    return (int)ceil(mean + Sel3Cfg<NT>::SIGMAS * sqrt(mean * (1.0 - f))) + 2;
+}
+
+template <int NT>
+static cudaError_t launch_sel3(const SelectArgs& a, dim3 grid, cudaStream_t st) {
+    const int cap = sel3_cap<NT>(a.n);
+    // slots [cap][NT] + one overflow slot row + the contiguous candidate array
+    const size_t smem = ((sizeof(Sel3Shared<NT>) + 15) & ~size_t(15)) + (size_t)(2 * cap + 1) * NT * 4;
+    cudaError_t e = cudaFuncSetAttribute(select_v3_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    select_v3_kernel<NT><<<grid, NT, smem, st>>>(a, cap);
+    return cudaGetLastError();
+}
+
 template <int NT, bool GLB>
 static cudaError_t launch_sel2(const SelectArgs& a, dim3 grid, cudaStream_t st) {
     const size_t smem = ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)) + (GLB ? (size_t)SEL2G_CAP * 4 : (size_t)a.n * 4);
@@ -684,6 +1172,10 @@ static cudaError_t launch_sel2(const SelectArgs& a, dim3 grid, cudaStream_t st) 
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
     if (a.Qb == 0 || a.jcount == 0) return cudaSuccess;
     dim3 grid((unsigned)a.jcount, (unsigned)a.Qb);
+    if (a.variant != 2 && a.n >= SEL3_MIN_N && a.n <= SEL3_MAX_N) {
+        if (a.n <= SEL2_WIDE_N) return launch_sel3<256>(a, grid, st);
+        return launch_sel3<1024>(a, grid, st);
+    }
     if (a.n <= SEL2_MAX_N) {
         if (a.n <= SEL2_WIDE_N) return launch_sel2<256, false>(a, grid, st);
         if (a.n <= SEL2_WIDER_N) return launch_sel2<512, false>(a, grid, st);

@@ -385,10 +385,11 @@ def test_tier2_large_rows(b200, notion, n):
 
 @pytest.mark.parametrize("notion", ["halfspace", "projection"])
 def test_config5_shape(b200, notion):
-    """The config-5 shape (d = 200, past the tensor path's d <= 64: FFMA
-    contraction; n past the shared-memory select: global-memory select) at
-    n = 400k, Cauchy data, against FP64: halfspace counts within the tie zone,
-    projection depths to DEPTH_RTOL."""
+    """The config-5 shape class (d = 200: the wide tensor contraction for
+    halfspace, the FFMA centred store for projection; n past the shared-memory
+    select: global-memory select) at n = 400k, Cauchy data, 48 directions,
+    against FP64: halfspace counts within the tie zone, projection depths to
+    DEPTH_RTOL."""
     from oracle import oracle
     from paper_2506_08262_b200.synthetic import student_t
 
@@ -406,8 +407,8 @@ def test_config5_shape(b200, notion):
         rle, rge = (y <= 0).sum(axis=0), (y >= 0).sum(axis=0)
         assert np.all(np.abs(cle - rle) <= T) and np.all(np.abs(cge - rge) <= T)
     else:
-        got = b200.evaluate_directions(z, data, U[:8], notion, b200.ParallelConfig(workers=1))
-        ref = oracle.evaluate_directions(z, X, U[:8], notion)
+        got = b200.evaluate_directions(z, data, U, notion, b200.ParallelConfig(workers=1))
+        ref = oracle.evaluate_directions(z, X, U, notion)
         np.testing.assert_allclose(got, ref, rtol=DEPTH_RTOL, atol=0)
 
 
@@ -523,7 +524,6 @@ def test_tensor_paths_tiny_n(b200, n, d):
     y = X @ U.T - (U @ z)[None, :]
     T = (np.abs(y) < TIE_REL * np.maximum(np.linalg.norm(X, axis=1), np.linalg.norm(z))[:, None]).sum(axis=0)
     assert np.all(np.abs(cle - (y <= 0).sum(axis=0)) <= T) and np.all(np.abs(cge - (y >= 0).sum(axis=0)) <= T)
-    # d = 200 takes the FFMA store: FP32 data rounding over 200 terms, amplified by
-    # the MAD of 5 points, can reach ~1.3e-5 (the 1e-5 contract holds at d <= 50)
-    rtol = DEPTH_RTOL if d <= 50 else 5e-5
-    np.testing.assert_allclose(got, oracle.evaluate_directions(z, X, U, "projection"), rtol=rtol, atol=0)
+    # d > 50 at these sizes takes the FP64-accumulated centred store (center.cu):
+    # the MAD of a handful of points can sit far below the projections' spread
+    np.testing.assert_allclose(got, oracle.evaluate_directions(z, X, U, "projection"), rtol=DEPTH_RTOL, atol=0)
