@@ -240,7 +240,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process group for N>1 (gloo: ranks may share one GPU, the single-GPU rehearsal)")
-    ap.add_argument("--select-path", default="auto", choices=["auto", "radix"],
+    ap.add_argument("--select-path", default="auto", choices=["auto", "radix", "wide"],
                     help="order-statistic kernel of the projection notions (A/B)")
     ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "tensor2", "filter"],
                     help="halfspace contraction kernel (auto: the library's choice)")
@@ -384,7 +384,10 @@ def main():
         sel_bytes = 4.0 * n * m * r * B * args.steps
         sel_gbs = sel_bytes / (select_ms / 1e3) / 1e9
         roofline = {"bound": "hbm", "achieved": sel_gbs, "peak": hbm, "unit": "GB/s", "frac": sel_gbs / hbm,
-                    "traffic": None, "kernel": "select_v2_kernel<256|512|1024, smem>" if n <= 52224
+                    "traffic": None,
+                    "kernel": ("select_v2_kernel<256|512|1024, smem>" if args.select_path == "radix"
+                               else "select_v3_kernel<256>" if n <= 16384
+                               else "select_v3_kernel<512|1024>") if 2048 <= n <= 53248
                     else "select_v2_kernel<1024, global>" if n % 4 == 0 else "select_kernel",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "nominal 8 TB/s",
                     "achieved_is": "algorithmic bytes (the stored projections, 4 n per direction) / select time",

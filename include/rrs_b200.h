@@ -153,7 +153,8 @@ int rrs_engine_set_contract_path(rrs_engine* e, int32_t path);
 
 /* Order-statistic kernel for the projection notions: 0 = auto (the
  * sample-bracket select, select.cu v3, for 2048 <= n <= 53248; radix select
- * elsewhere), 2 = radix select v2 everywhere.  Both give bitwise equal depths
+ * elsewhere), 2 = radix select v2 everywhere, 3 = v3 with 1024-thread CTAs
+ * above n = 16384.  All give bitwise equal depths
  * (same FP32 keys, FP64 midpoints); the switch exists for A/B measurement. */
 int rrs_engine_set_select_path(rrs_engine* e, int32_t path);
 

@@ -201,10 +201,11 @@ class Engine:
         _raise(load_library().rrs_engine_set_contract_path(self._h, code))
 
     def set_select_path(self, path: str):
-        """'auto' | 'radix' (order-statistic kernel of the projection notions:
-        auto = the sample-bracket select v3 where it applies, radix = select v2
-        everywhere; bitwise equal depths)."""
-        code = {"auto": 0, "radix": 2}[path]
+        """'auto' | 'radix' | 'wide' (order-statistic kernel of the projection
+        notions: auto = the sample-bracket select v3 where it applies, radix =
+        select v2 everywhere, wide = v3 with 1024-thread CTAs above n = 16k;
+        bitwise equal depths)."""
+        code = {"auto": 0, "radix": 2, "wide": 3}[path]
         _raise(load_library().rrs_engine_set_select_path(self._h, code))
 
     def enable_timing(self, on: bool = True):

@@ -621,7 +621,8 @@ int rrs_engine_set_contract_path(rrs_engine* e, int32_t path) {
 
 int rrs_engine_set_select_path(rrs_engine* e, int32_t path) {
     if (!e) return fail(RRS_ERR_INVALID, "engine is null");
-    if (path != 0 && path != 2) return fail(RRS_ERR_INVALID, "select path must be 0 (auto) or 2 (radix select v2)");
+    if (path != 0 && path != 2 && path != 3)
+        return fail(RRS_ERR_INVALID, "select path must be 0 (auto), 2 (radix select v2) or 3 (v3, 1024 threads)");
     e->select_path = path;
     return RRS_OK;
 }

@@ -701,19 +701,26 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
 // the 1024-thread variant narrows the bracket so 1024 threads' slots rarely overflow
 template <int NT>
 struct Sel3Cfg {
-    static constexpr int S = NT >= 1024 ? 512 : 256;
+    static constexpr int S = NT >= 512 ? 512 : 256;
     static constexpr double SIGMAS = NT >= 1024 ? 5.0 : 4.0;  // slot headroom
+    static constexpr int MINB = NT >= 1024 ? 1 : NT >= 512 ? 2 : 5;  // CTAs per SM targeted
 };
 constexpr int SMAX = 512;
 constexpr int64_t SEL3_MIN_N = 2048;
 constexpr int64_t SEL3_MAX_N = 53248;
 
+constexpr int S3_BITS = 10, S3_BINS = 1 << S3_BITS;  // digit width of the candidate select
+
 template <int NT>
 struct Sel3Shared {
     static constexpr int W = NT / 32;
-    alignas(16) uint32_t hist[2048];
+    // hist (candidate select) and sdev (sample-sort scratch, the MAD sample's
+    // deviations) are never live at the same time
+    union {
+        alignas(16) uint32_t hist[S3_BINS];
+        uint32_t sdev[Sel3Cfg<NT>::S];
+    };
     alignas(16) uint32_t sorted[Sel3Cfg<NT>::S];  // sorted sample keys (deviation keys for the MAD)
-    uint32_t sdev[Sel3Cfg<NT>::S];
     uint32_t tiny[32];
     uint32_t wsum[W];
     uint32_t s_bin, s_below, s_cnt, s_ntiny, s_ovf, s_res, s_cle;
@@ -781,15 +788,15 @@ __device__ __forceinline__ void s3_arr_each(const uint32_t* __restrict__ cand, i
 
 // t-th smallest (0-based) of the keys enumerated by each(f), all of which lie
 // in [lo, hi] (total of them: count); c_le = number of them <= the result.
-// Histograms of 11-bit digits of the offset key - lo in shared memory (one
-// 2048-bin histogram, predicated red.shared), starting at the top bit of
+// Histograms of 10-bit digits of the offset key - lo in shared memory (one
+// 1024-bin histogram, predicated red.shared), starting at the top bit of
 // hi - lo; once the chosen bin holds <= 32 keys they are gathered and one warp
 // ranks them.
 template <int NT, typename Each>
 __device__ uint32_t s3_kth(Each&& each, uint32_t t, uint32_t lo, uint32_t hi, uint32_t count, Sel3Shared<NT>& sh,
                            uint32_t& c_le) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int PER = 2048 / NT;  // bins per thread in the scan
+    constexpr int PER = S3_BINS / NT;  // bins per thread in the scan
     uint32_t base = lo, span = hi - lo, below = 0, wcnt = count;
     for (;;) {
         if (span == 0u) {  // one key value left in the window
@@ -824,10 +831,10 @@ __device__ uint32_t s3_kth(Each&& each, uint32_t t, uint32_t lo, uint32_t hi, ui
             return sh.s_res;
         }
         const int bits = 32 - __clz(span);
-        const int shift = bits > 11 ? bits - 11 : 0;
+        const int shift = bits > S3_BITS ? bits - S3_BITS : 0;
         {
             uint4* h4 = reinterpret_cast<uint4*>(sh.hist);
-            for (int i = tid; i < 512; i += NT) h4[i] = make_uint4(0u, 0u, 0u, 0u);
+            for (int i = tid; i < S3_BINS / 4; i += NT) h4[i] = make_uint4(0u, 0u, 0u, 0u);
         }
         __syncthreads();
         const uint32_t hbase = smem_u32(sh.hist);
@@ -839,8 +846,8 @@ __device__ uint32_t s3_kth(Each&& each, uint32_t t, uint32_t lo, uint32_t hi, ui
                          : "memory");
         });
         __syncthreads();
-        // exclusive scan over the 2048 bins (PER consecutive bins per thread)
-        uint32_t hv[PER];
+        // exclusive scan over the bins (PER consecutive bins per thread; PER >= 1)
+        uint32_t hv[PER > 0 ? PER : 1];
         uint32_t local = 0;
 #pragma unroll
         for (int b = 0; b < PER; ++b) {
@@ -880,35 +887,46 @@ __device__ uint32_t s3_kth(Each&& each, uint32_t t, uint32_t lo, uint32_t hi, ui
     }
 }
 
-// bitonic sort (one warp) of 32·E keys held E per lane (index lane·E + e)
-template <int E>
-__device__ __forceinline__ void s3_sort_warp(uint32_t (&v)[E], int lane) {
-    const int l8 = lane * E;
+// sort the S sample keys (thread t < S holds one): each warp sorts its 32 by
+// a shuffle bitonic network, then every key's rank is its lane plus, in every
+// other chunk, the count of keys below it (ties go to the lower chunk) found
+// by a branch-free binary search -- all S/32 warps work, no warp waits on one
+template <int NT>
+__device__ __forceinline__ void s3_sort_sample(uint32_t v, Sel3Shared<NT>& sh) {
+    constexpr int S = Sel3Cfg<NT>::S, C = S / 32;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (w < C) {
 #pragma unroll
-    for (int k = 2; k <= 32 * E; k <<= 1) {
+        for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= E) {
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const uint32_t o = __shfl_xor_sync(0xffffffffu, v[e], j / E);
-                    const bool keep_min = ((l8 & j) == 0) == (((l8 + e) & k) == 0);
-                    v[e] = keep_min ? min(v[e], o) : max(v[e], o);
-                }
-            } else {
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    if ((e & j) == 0) {
-                        const bool up = ((l8 + e) & k) == 0;
-                        const uint32_t a = v[e], b = v[e | j];
-                        const uint32_t mn = min(a, b), mx = max(a, b);
-                        v[e] = up ? mn : mx;
-                        v[e | j] = up ? mx : mn;
-                    }
-                }
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                const uint32_t o = __shfl_xor_sync(0xffffffffu, v, j);
+                const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+                v = keep_min ? min(v, o) : max(v, o);
             }
         }
+        sh.sdev[tid] = v;
     }
+    __syncthreads();
+    if (w < C) {
+        uint32_t rank = (uint32_t)lane;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            if (c == w) continue;
+            const uint32_t* ch = sh.sdev + 32 * c;
+            const bool le = c < w;  // earlier chunk: its equal keys rank first
+            uint32_t pos = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t t = ch[pos + step - 1];
+                pos += (le ? t <= v : t < v) ? (uint32_t)step : 0u;
+            }
+            const uint32_t t = ch[pos];
+            rank += pos + ((le ? t <= v : t < v) ? 1u : 0u);
+        }
+        sh.sorted[rank] = v;
+    }
+    __syncthreads();
 }
 
 // bracket [lo, hi] of population ranks [R, R2] of N keys from a sorted sample of S
@@ -929,7 +947,7 @@ __device__ __forceinline__ void s3_bracket(const uint32_t* sorted, uint32_t R, u
 // a thread's slots overflowed (the caller falls back).
 template <int NT, typename KF>
 __device__ bool s3_select(const float* __restrict__ row, int n, KF kf, uint32_t R, bool need_next, uint32_t lo,
-                          uint32_t hi, uint32_t* slots, int cap, uint32_t* cand, Sel3Shared<NT>& sh, uint32_t& kR,
+                          uint32_t hi, uint32_t* slots, int cap, int cmax, uint32_t* cand, Sel3Shared<NT>& sh, uint32_t& kR,
                           uint32_t& kN, uint32_t& c_le) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t span = hi - lo;
@@ -977,7 +995,7 @@ __device__ bool s3_select(const float* __restrict__ row, int n, KF kf, uint32_t 
         total += t;
     }
     const uint32_t c_lo = total >> 16, c_mid = total & 0xFFFFu;
-    const bool overflow = sh.s_ovf != 0u;
+    const bool overflow = sh.s_ovf != 0u || c_mid > (uint32_t)cmax;
     if (overflow || R < c_lo || R >= c_lo + c_mid) return false;  // block-uniform
     // compact the slots into one contiguous array
     const uint32_t off = (woff + incl - v) & 0xFFFFu;
@@ -1013,12 +1031,12 @@ struct S3KeyAbsDev {
 
 template <int NT, typename KF>
 __device__ __forceinline__ void s3_rank(const float* row, int n, KF kf, uint32_t R, bool need_next,
-                                        const uint32_t* sorted, uint32_t* slots, int cap, uint32_t* cand,
+                                        const uint32_t* sorted, uint32_t* slots, int cap, int cmax, uint32_t* cand,
                                         Sel3Shared<NT>& sh, uint32_t& kR, uint32_t& kN, uint32_t& c_le,
                                         unsigned* fallbacks) {
     uint32_t lo, hi;
     s3_bracket<Sel3Cfg<NT>::S>(sorted, R, need_next ? R + 1 : R, (uint32_t)n, lo, hi);
-    if (!s3_select<NT>(row, n, kf, R, need_next, lo, hi, slots, cap, cand, sh, kR, kN, c_le)) {
+    if (!s3_select<NT>(row, n, kf, R, need_next, lo, hi, slots, cap, cmax, cand, sh, kR, kN, c_le)) {
         if (fallbacks && threadIdx.x == 0) atomicAdd(fallbacks, 1u);
         __syncthreads();
         if (threadIdx.x == 0) sh.s_ovf = 0u;
@@ -1034,7 +1052,7 @@ __device__ __forceinline__ void s3_rank(const float* row, int n, KF kf, uint32_t
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) select_v3_kernel(const SelectArgs a, int cap) {
+__global__ void __launch_bounds__(NT, Sel3Cfg<NT>::MINB) select_v3_kernel(const SelectArgs a, int cap, int cmax) {
     extern __shared__ __align__(16) unsigned char sel3_raw[];
     Sel3Shared<NT>& sh = *reinterpret_cast<Sel3Shared<NT>*>(sel3_raw);
     const int jj = blockIdx.x;
@@ -1047,26 +1065,18 @@ __global__ void __launch_bounds__(NT) select_v3_kernel(const SelectArgs a, int c
     uint32_t* slots = reinterpret_cast<uint32_t*>(sel3_raw + ((sizeof(Sel3Shared<NT>) + 15) & ~size_t(15)));
     uint32_t* cand = slots + (size_t)(cap + 1) * NT;  // 16-byte aligned: NT is a multiple of 4
 
-    // sample: S strided keys of y, sorted by warp 0
-    constexpr int S = Sel3Cfg<NT>::S, E = S / 32;
-    if (tid < 32) {
-        uint32_t v[E];
-#pragma unroll
-        for (int e = 0; e < E; ++e)
-            v[e] = fkey(__ldg(row + (int)(((int64_t)(2 * (tid * E + e) + 1) * n) / (2 * S))));
-        s3_sort_warp<E>(v, tid);
-        uint4* s4 = reinterpret_cast<uint4*>(sh.sorted + tid * E);
-#pragma unroll
-        for (int e = 0; e < E; e += 4) s4[e / 4] = make_uint4(v[e], v[e + 1], v[e + 2], v[e + 3]);
-        if (tid == 0) sh.s_ovf = 0u;
-    }
-    __syncthreads();
+    // sample: S strided keys of y, sorted
+    constexpr int S = Sel3Cfg<NT>::S;
+    uint32_t sv = 0u;
+    if (tid < S) sv = fkey(__ldg(row + (int)(((int64_t)(2 * tid + 1) * n) / (2 * S))));
+    if (tid == 0) sh.s_ovf = 0u;
+    s3_sort_sample<NT>(sv, sh);
 
     // median of y (v2: midpoint of the central pair, FP64)
     const uint32_t k = (uint32_t)(n - 1) >> 1;
     const bool even = (n & 1) == 0;
     uint32_t kR, kN, c_le;
-    s3_rank<NT>(row, n, S3KeyY{}, k, even, sh.sorted, slots, cap, cand, sh, kR, kN, c_le, a.fallbacks);
+    s3_rank<NT>(row, n, S3KeyY{}, k, even, sh.sorted, slots, cap, cmax, cand, sh, kR, kN, c_le, a.fallbacks);
     const double lov = (double)kfloat(kR);
     const double med = even ? (lov + (double)kfloat(kN)) / 2.0 : lov;
     const double medz = med + (a.shift ? a.shift[(size_t)q * a.m + j] : 0.0);  // med(y) - 0 (centred frame)
@@ -1108,7 +1118,7 @@ __global__ void __launch_bounds__(NT) select_v3_kernel(const SelectArgs a, int c
         }
         __syncthreads();
         uint32_t mR, mN, mc;
-        s3_rank<NT>(row, n, S3KeyAbsDev{med}, k, even, sh.sorted, slots, cap, cand, sh, mR, mN, mc, a.fallbacks);
+        s3_rank<NT>(row, n, S3KeyAbsDev{med}, k, even, sh.sorted, slots, cap, cmax, cand, sh, mR, mN, mc, a.fallbacks);
         const double mlo = (double)kfloat(mR);
         const double mad = even ? (mlo + (double)kfloat(mN)) / 2.0 : mlo;
         const double dev = fabs(medz);
@@ -1128,7 +1138,7 @@ __global__ void __launch_bounds__(NT) select_v3_kernel(const SelectArgs a, int c
             const uint32_t A = c_le + ((npos - 1u) >> 1);
             const bool pe = (npos & 1u) == 0u;
             uint32_t aR, aN, ac;
-            s3_rank<NT>(row, n, S3KeyY{}, A, pe, sh.sorted, slots, cap, cand, sh, aR, aN, ac, a.fallbacks);
+            s3_rank<NT>(row, n, S3KeyY{}, A, pe, sh.sorted, slots, cap, cmax, cand, sh, aR, aN, ac, a.fallbacks);
             const double ta = (double)(float)((double)kfloat(aR) - med);
             const double madp = pe ? (ta + (double)(float)((double)kfloat(aN) - med)) / 2.0 : ta;
             depth = 1.0 / (1.0 + dev / madp);
@@ -1139,23 +1149,51 @@ __global__ void __launch_bounds__(NT) select_v3_kernel(const SelectArgs a, int c
 
 // candidate slots per thread: mean + 4 sigma of a ~21 % bracket over the
 // thread's share of the row (an overflowing row falls back)
+// bracket share of the row at p = 1/2 (2M + 1 sample gaps) and its spread:
+// the population share between two sample order statistics M apart is
+// Beta-distributed with sd ~ sqrt(2M) / S
+template <int NT>
+static void sel3_share(double& f, double& fsd) {
+    const double S = Sel3Cfg<NT>::S;
+    const double M = 3.0 * sqrt(S * 0.25) + 2.0;
+    f = (2.0 * M + 1.0) / S;
+    fsd = sqrt(2.0 * M) / S;
+}
+// candidate slots per thread: mean + SIGMAS sigma of the thread's share of the
+// row in a bracket of typical share (an overflowing row falls back)
 template <int NT>
 static int sel3_cap(int64_t n) {
     const double kpt = (n % 4 == 0) ? 4.0 * (double)((n / 4 + NT - 1) / NT) : (double)((n + NT - 1) / NT);
-    const double S = Sel3Cfg<NT>::S;
-    const double f = (6.0 * sqrt(S * 0.25) + 6.0) / S;  // bracket share of the row at p = 1/2
+    double f, fsd;
+    sel3_share<NT>(f, fsd);
     const double mean = kpt * f;
     return (int)ceil(mean + Sel3Cfg<NT>::SIGMAS * sqrt(mean * (1.0 - f))) + 2;
+}
+// contiguous candidates: the bracket's share + 4 sd (rarely exceeded: fallback)
+template <int NT>
+static int sel3_cmax(int64_t n, int cap) {
+    double f, fsd;
+    sel3_share<NT>(f, fsd);
+    const int64_t c = (int64_t)ceil((double)n * (f + 4.0 * fsd)) + 64;
+    const int64_t lim = (int64_t)cap * NT;
+    return (int)((c < lim ? c : lim) + 3) & ~3;
+}
+
+template <int NT>
+static size_t sel3_smem(int64_t n) {
+    const int cap = sel3_cap<NT>(n);
+    // slots [cap][NT] + one overflow slot row + the contiguous candidate array
+    return ((sizeof(Sel3Shared<NT>) + 15) & ~size_t(15)) + ((size_t)(cap + 1) * NT + sel3_cmax<NT>(n, cap)) * 4;
 }
 
 template <int NT>
 static cudaError_t launch_sel3(const SelectArgs& a, dim3 grid, cudaStream_t st) {
     const int cap = sel3_cap<NT>(a.n);
-    // slots [cap][NT] + one overflow slot row + the contiguous candidate array
-    const size_t smem = ((sizeof(Sel3Shared<NT>) + 15) & ~size_t(15)) + (size_t)(2 * cap + 1) * NT * 4;
+    const int cmax = sel3_cmax<NT>(a.n, cap);
+    const size_t smem = sel3_smem<NT>(a.n);
     cudaError_t e = cudaFuncSetAttribute(select_v3_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    select_v3_kernel<NT><<<grid, NT, smem, st>>>(a, cap);
+    select_v3_kernel<NT><<<grid, NT, smem, st>>>(a, cap, cmax);
     return cudaGetLastError();
 }
 
@@ -1174,6 +1212,8 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
     dim3 grid((unsigned)a.jcount, (unsigned)a.Qb);
     if (a.variant != 2 && a.n >= SEL3_MIN_N && a.n <= SEL3_MAX_N) {
         if (a.n <= SEL2_WIDE_N) return launch_sel3<256>(a, grid, st);
+        // two 512-thread CTAs per SM when their shared memory fits (variant 3: 1024 threads)
+        if (a.variant != 3 && sel3_smem<512>(a.n) <= 113 * 1024) return launch_sel3<512>(a, grid, st);
         return launch_sel3<1024>(a, grid, st);
     }
     if (a.n <= SEL2_MAX_N) {
