@@ -151,6 +151,13 @@ int rrs_philox4x32_host(rrs_engine* e, const uint32_t* ctr, int64_t N, uint32_t 
  * (contract_tc2.cu; wider d takes contract_tcw.cu). */
 int rrs_engine_set_contract_path(rrs_engine* e, int32_t path);
 
+/* Page-locked host buffers (cudaHostAlloc, portable): the matrix loaders
+ * (io.read_matrix(..., pinned=True)) read DFMX payloads straight into one, so
+ * rrs_set_dataset_host / rrs_depth_batch_host copy from it by DMA.  Replaces
+ * the reference's pageable np.frombuffer / np.array results (io.py:63-110). */
+int rrs_host_alloc(int64_t bytes, void** out);
+int rrs_host_free(void* p);
+
 /* Order-statistic kernel for the projection notions: 0 = auto (the
  * sample-bracket select, select.cu v3, for 2048 <= n <= 53248; radix select
  * elsewhere), 2 = radix select v2 everywhere, 3 = v3 with 1024-thread CTAs

@@ -91,6 +91,8 @@ SIGNATURES = [
     ("rrs_engine_enable_timing", ctypes.c_int, [_vp, ctypes.c_int32]),
     ("rrs_engine_set_contract_path", ctypes.c_int, [_vp, ctypes.c_int32]),
     ("rrs_engine_set_select_path", ctypes.c_int, [_vp, ctypes.c_int32]),
+    ("rrs_host_alloc", ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    ("rrs_host_free", ctypes.c_int, [ctypes.c_void_p]),
 ]
 
 _lib = None
@@ -138,6 +140,33 @@ def _raise(rc):
     if rc == RRS_ERR_NOMEM:
         raise MemoryError(msg)
     raise RuntimeError(f"librrs_b200: {msg}")
+
+
+class _PinnedBlock:
+    """Owner of one page-locked host allocation (rrs_host_alloc); freed when
+    the last numpy view of it goes away."""
+
+    def __init__(self, nbytes: int):
+        ptr = ctypes.c_void_p()
+        _raise(load_library().rrs_host_alloc(int(nbytes), ctypes.byref(ptr)))
+        self.ptr = ptr.value
+        self.nbytes = int(nbytes)
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.rrs_host_free(ctypes.c_void_p(self.ptr))
+            self.ptr = None
+
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """Uninitialised numpy array in page-locked host memory (H2D by DMA)."""
+    shape = tuple(int(s) for s in np.atleast_1d(shape))
+    dt = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dt.itemsize
+    block = _PinnedBlock(max(nbytes, 1))
+    buf = (ctypes.c_char * max(nbytes, 1)).from_address(block.ptr)
+    buf._owner = block  # the ctypes buffer keeps the block alive; numpy keeps the buffer
+    return np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
 
 
 def device_count() -> int:

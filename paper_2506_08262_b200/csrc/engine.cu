@@ -619,6 +619,26 @@ int rrs_engine_set_contract_path(rrs_engine* e, int32_t path) {
     return RRS_OK;
 }
 
+int rrs_host_alloc(int64_t bytes, void** out) {
+    if (!out) return fail(RRS_ERR_INVALID, "out is null");
+    *out = nullptr;
+    if (bytes < 0) return fail(RRS_ERR_INVALID, "negative size");
+    if (bytes == 0) bytes = 16;
+    cudaError_t ce = cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable);
+    if (ce != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return fail(ce == cudaErrorMemoryAllocation ? RRS_ERR_NOMEM : RRS_ERR_CUDA,
+                    std::string("cudaHostAlloc: ") + cudaGetErrorString(ce));
+    }
+    return RRS_OK;
+}
+
+int rrs_host_free(void* p) {
+    if (p) CK(cudaFreeHost(p));
+    return RRS_OK;
+}
+
 int rrs_engine_set_select_path(rrs_engine* e, int32_t path) {
     if (!e) return fail(RRS_ERR_INVALID, "engine is null");
     if (path != 0 && path != 2 && path != 3)

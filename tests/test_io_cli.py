@@ -2,6 +2,7 @@
 except the end-to-end depth command, which needs the device."""
 
 import json
+import os
 import struct
 
 import numpy as np
@@ -147,3 +148,68 @@ def test_cli_depth_matches_api(b200, tmp_path, capsys):
         assert got["depth"] == want.depth and got["directions_used"] == want.directions_used
         assert np.array_equal(got["argmin_direction"], want.argmin_direction)
         assert len(got["trace"]) == 5 and got["trace"][0]["epsilon"] == want.trace[0].epsilon
+
+
+GOLD_CLI = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cli")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["halfspace_dfmx", "projection_csv", "asymprojection_dfmx", "halfspace_inline",
+                                  "mahalanobis_csv"])
+def test_cli_depth_matches_reference_golden(b200, name, capsys, monkeypatch):
+    """`depth` replayed on the files and argument lists the REAL reference CLI
+    was run on (tests/golden/make_cli_golden.py, cli.py:113-171): same payload
+    keys and header fields, halfspace depths / traces identical, projection
+    notions within the tier-2 tolerance, argmin directions to 1e-12."""
+    with open(os.path.join(GOLD_CLI, f"{name}.json")) as fh:
+        gold = json.load(fh)
+    monkeypatch.chdir(GOLD_CLI)
+    assert cli.main(gold["argv"]) == 0
+    got, want = json.loads(capsys.readouterr().out), gold["stdout"]
+    assert set(got) == set(want)
+    assert want["backend"] == "compiled" and got["backend"] == "b200"
+    for key in set(want) - {"backend", "results"}:
+        assert got[key] == want[key], key
+    exact = want["notion"] == "halfspace"
+    for g, w in zip(got["results"], want["results"], strict=True):
+        assert set(g) == set(w)
+        if want["notion"] == "mahalanobis":
+            assert g["depth"] == pytest.approx(w["depth"], rel=1e-12)
+            continue
+        if exact:
+            assert g["depth"] == w["depth"]
+        else:
+            assert g["depth"] == pytest.approx(w["depth"], rel=1e-5)
+        assert g["directions_used"] == w["directions_used"]
+        np.testing.assert_allclose(g["argmin_direction"], w["argmin_direction"], rtol=0, atol=1e-12)
+        if "trace" in w:
+            assert len(g["trace"]) == len(w["trace"])
+            for gt, wt in zip(g["trace"], w["trace"]):
+                assert gt["epsilon"] == wt["epsilon"]
+                if exact:
+                    assert gt["best_depth"] == wt["best_depth"]
+                else:
+                    assert gt["best_depth"] == pytest.approx(wt["best_depth"], rel=1e-5)
+                np.testing.assert_allclose(gt["pole"], wt["pole"], rtol=0, atol=1e-12)
+
+
+@pytest.mark.gpu
+def test_read_matrix_pinned(b200, tmp_path):
+    """read_matrix(..., pinned=True): same values as the pageable read, in
+    page-locked memory (DFMX read straight into it, CSV copied once)."""
+    import torch
+
+    X = np.random.default_rng(8).standard_normal((3001, 7))
+    for fname in ("x.dfmx", "x.csv"):
+        io.write_matrix(tmp_path / fname, X)
+        a = io.read_matrix(tmp_path / fname)
+        p = io.read_matrix(tmp_path / fname, pinned=True)
+        assert np.array_equal(a, p) and np.array_equal(p, X)
+        assert torch.from_numpy(p).is_pinned()
+        data = b200.Dataset(p)
+        cfg = b200.RrsConfig(total_directions=300, refinements=3, shrink=0.9, notion="halfspace", seed=2)
+        assert np.array_equal(b200.depth_batch_arrays(p[:4], data, cfg)[0],
+                              b200.depth_batch_arrays(a[:4], b200.Dataset(a), cfg)[0])
+    (tmp_path / "bad.dfmx").write_bytes((tmp_path / "x.dfmx").read_bytes()[:-8])
+    with pytest.raises(io.MatrixFormatError):
+        io.read_matrix(tmp_path / "bad.dfmx", pinned=True)
