@@ -30,6 +30,7 @@ SOURCES = {  # file -> extra flags
     "contract_tcs.cu": [],
     "select.cu": [],
     "center.cu": [],
+    "contract64.cu": [],
     "api64.cu": [],
     "engine.cu": [],
 }

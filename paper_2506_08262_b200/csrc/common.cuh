@@ -11,7 +11,7 @@ constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int KC = 64;            // coordinates per staged X chunk
 constexpr int CT_THREADS = 256;
-constexpr int MAX_D = 256;        // Us holds all d coordinates of a direction block
+constexpr int MAX_D = 1024;       // any d the generation kernel takes (GEN_MAX_D); > 256: contract64.cu
 constexpr int GEN_MAX_D = 1024;
 
 struct DeviceData {

@@ -87,6 +87,7 @@ struct rrs_engine {
     // centred frame of the projection notions (center.cu): m, the FP32 blocked
     // copy of x - m, and for n < STORE64_N the FP64 row-major copy of x - m
     DevBuf center, xcb, xc64;
+    DevBuf x64;  // d > 256: FP64 row-major copy of the data (contract64.cu)
     int64_t n = 0;
     int d = 0;
     int64_t tiles = 0;
@@ -166,6 +167,7 @@ struct Plan {
     bool tcf;    // ... by filter and refine (contract_tcf.cu, d <= 64; u32 holds FP32 rows)
     bool tcs;    // tensor-core projection store (projection notions, d <= 50; contract_tcs.cu)
     bool store64;  // FP64-accumulated store (projection notions, n < STORE64_N, no tensor store; center.cu)
+    bool wide;     // d > 256: FP64 contraction (contract64.cu) for counts and the store
     int nb8;     // 128-direction blocks per query (tensor path operand, tc_block_bytes(d) each)
     int jchunk;  // direction blocks per store launch (projection notions)
     int tpu, chunks;
@@ -185,6 +187,7 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     // refinement whatever computes it), the tensor store pays from d ~ 32 (config 3)
     p.tcs = tcs_ok && (e->contract_path >= 2 || (e->contract_path == 0 && e->n >= 4096 && e->d >= 32));
     p.store64 = notion != RRS_HALFSPACE && !p.tcs && e->n < STORE64_N;
+    p.wide = e->d > TC_MAX_D;
     const int64_t d = e->d, n = e->n;
     int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * tcf_dp((int)d) * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 16 +
                     d * 40 + 64 +
@@ -273,8 +276,23 @@ ContractArgs contract_args(rrs_engine* e, const Plan& p, int Qb, int jb0, int jb
     return c;
 }
 
-int contract_halfspace(rrs_engine* e, const Plan& p, int Qb) {
-    if (p.tcf) {
+int contract_halfspace(rrs_engine* e, const Plan& p, int Qb, const double* zdev) {
+    if (p.wide) {
+        Contract64Args c{};
+        c.x64 = e->x64.as<double>();
+        c.c = zdev;
+        c.c_stride = e->d;
+        c.u64 = e->u64.as<double>();
+        c.counts = e->counts.as<int>();
+        c.n = e->n;
+        c.d = e->d;
+        c.m = p.m;
+        c.mpad = p.mpad;
+        c.jbase = 0;
+        c.jcount = p.m;
+        c.Qb = Qb;
+        CK(launch_contract64(c, false, e->stream));
+    } else if (p.tcf) {
         TcfArgs t{};
         t.xb = e->xb.as<float>();
         t.zq = e->zq.as<float>();
@@ -333,7 +351,22 @@ int univariate_from_store(rrs_engine* e, const Plan& p, int Qb, int notion, cons
         const int jbn = (p.MB - jb0) < p.jchunk ? (p.MB - jb0) : p.jchunk;
         {
             Timer t(e, 1);
-            if (p.store64) {
+            if (p.wide && !p.store64) {
+                Contract64Args c{};
+                c.x64 = e->x64.as<double>();
+                c.c = e->center.as<double>();  // centred frame, the same m for every query
+                c.c_stride = 0;
+                c.u64 = e->u64.as<double>();
+                c.y = e->y.as<float>();
+                c.n = e->n;
+                c.d = e->d;
+                c.m = p.m;
+                c.mpad = p.mpad;
+                c.jbase = jb0 * BN;
+                c.jcount = jbn * BN;
+                c.Qb = Qb;
+                CK(launch_contract64(c, true, e->stream));
+            } else if (p.store64) {
                 CK(launch_store64(e->xc64.as<double>(), e->u64.as<double>(), e->y.as<float>(), e->n, e->d, Qb, p.m,
                                   jb0 * BN, jbn * BN, e->stream));
             } else if (p.tcs) {
@@ -468,7 +501,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
             }
             if (cfg->notion == RRS_HALFSPACE) {
                 Timer t(e, 1);
-                if (int rc = contract_halfspace(e, p, Qb)) return rc;
+                if (int rc = contract_halfspace(e, p, Qb, zdev + b0 * d)) return rc;
                 e->stats.kernel_launches++;
                 e->stats.contract_launches++;
             } else {
@@ -582,7 +615,7 @@ int rrs_engine_destroy(rrs_engine* e) {
     for (DevBuf* b : {&e->xb, &e->xmax, &e->zq, &e->u64, &e->u32, &e->uop, &e->counts, &e->depths, &e->y, &e->pole,
                       &e->reflv, &e->reflmode, &e->dmin, &e->bestcnt, &e->tmp_in, &e->tmp_out0,
                       &e->tmp_out1, &e->tmp_out2, &e->tmp_out3, &e->center, &e->xcb, &e->xc64, &e->zq0,
-                      &e->shift, &e->fallbacks})
+                      &e->shift, &e->fallbacks, &e->x64})
         b->release();
     for (auto ev : e->ev_pool) cudaEventDestroy(ev);
     if (e->own) cudaStreamDestroy(e->own);
@@ -689,6 +722,10 @@ static int set_dataset_common(rrs_engine* e, const double* xdev, int64_t n, int3
     if (n < STORE64_N) {
         CK(e->xc64.ensure((size_t)n * d * 8));
         CK(launch_center_copy64(xdev, e->center.as<double>(), e->xc64.as<double>(), n, d, e->stream));
+    }
+    if (d > TC_MAX_D) {
+        CK(e->x64.ensure((size_t)n * d * 8));
+        CK(cudaMemcpyAsync(e->x64.p, xdev, (size_t)n * d * 8, cudaMemcpyDeviceToDevice, e->stream));
     }
     if (d > TC_SLICE) {
         CK(e->xmax.ensure((size_t)tiles * BM * 4));
@@ -806,7 +843,7 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
     if (p.tcs) CK(launch_pack_tc6_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (notion == RRS_HALFSPACE) {
         CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.mpad * 2 * 4, e->stream));
-        if (int rc = contract_halfspace(e, p, 1)) return rc;
+        if (int rc = contract_halfspace(e, p, 1, e->tmp_in.as<double>())) return rc;
         std::vector<int> cnt((size_t)p.mpad * 2);
         CK(cudaMemcpyAsync(cnt.data(), e->counts.p, cnt.size() * 4, cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));

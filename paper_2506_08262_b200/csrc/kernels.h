@@ -295,6 +295,20 @@ cudaError_t launch_philox_words(const uint32_t* ctr, uint32_t* out, int64_t N, u
 cudaError_t launch_contract_count(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_contract_store(const ContractArgs& a, cudaStream_t st);
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
+// FP64 contraction for d > 256 (contract64.cu): count mode (halfspace) or
+// store mode (centred projection rows)
+constexpr int TC_MAX_D = 256;        // the FP32 / tensor paths; above it contract64
+struct Contract64Args {
+    const double* x64;       // [n][d] FP64 data (row-major)
+    const double* c;         // centre per query: c + q * c_stride (z for halfspace, m for the store)
+    int64_t c_stride;
+    const double* u64;       // [Qb][m][d]
+    int* counts;             // [Qb][mpad][2] (#y<0, #y>0), count mode
+    float* y;                // [Qb][jcount][n], store mode
+    int64_t n;
+    int d, m, mpad, jbase, jcount, Qb;
+};
+cudaError_t launch_contract64(const Contract64Args& a, bool store, cudaStream_t st);
 // centred frame of the projection notions (center.cu)
 constexpr int64_t STORE64_N = 4096;  // below: FP64-accumulated store from an FP64 centred copy
 cudaError_t launch_center_sample(const double* x, int64_t n, int d, double* center, cudaStream_t st);

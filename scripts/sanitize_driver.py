@@ -21,7 +21,8 @@ cases = [
     (4100, 50, "halfspace", "filter", "auto"),     # contract_tcf
     (4100, 80, "halfspace", "tensor", "auto"),     # contract_tcw
     (1000, 5, "halfspace", "ffma", "auto"),        # contract_kernel<count>
-    (1000, 300, "halfspace", "ffma", "auto"),      # d > 256: FFMA K-chunks (if supported)
+    (1000, 300, "halfspace", "auto", "auto"),      # d > 256: contract64 count
+    (5000, 300, "projection", "auto", "auto"),     # d > 256: contract64 store
     (5000, 40, "projection", "tensor", "auto"),    # contract_tcs + select v3<256>
     (20000, 20, "asym_projection", "ffma", "auto"),  # contract_kernel<store> + select v3<512>
     (20000, 20, "projection", "ffma", "wide"),     # select v3<1024>

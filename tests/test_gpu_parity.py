@@ -527,3 +527,36 @@ def test_tensor_paths_tiny_n(b200, n, d):
     # d > 50 at these sizes takes the FP64-accumulated centred store (center.cu):
     # the MAD of a handful of points can sit far below the projections' spread
     np.testing.assert_allclose(got, oracle.evaluate_directions(z, X, U, "projection"), rtol=DEPTH_RTOL, atol=0)
+
+
+@pytest.mark.parametrize("d", [257, 384, 1024])
+def test_wide_dimensions(b200, d):
+    """d > 256 (contract64.cu, FP64): halfspace counts equal the FP64 oracle's
+    outside the tie zone (here: everywhere, the FP64 path has no slack to use),
+    projection / asymmetric depths within DEPTH_RTOL, and a short RRS run whose
+    halfspace depths equal the oracle's RRS (reference: _kernels.pyx:139-155,
+    no dimension limit)."""
+    from oracle import oracle
+    from paper_2506_08262_b200.synthetic import toeplitz_gaussian
+
+    n = 5000
+    X = toeplitz_gaussian(d, n, seed=4)
+    rng = np.random.default_rng(d)
+    U = rng.standard_normal((96, d))
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    data = b200.Dataset(X)
+    z = X[11] + 0.05 * rng.standard_normal(d)
+    _, cle, cge = b200.evaluate_directions_counts(z, data, U)
+    y = X @ U.T - (U @ z)[None, :]
+    T = tie_zone(X, z, U)
+    assert np.all(np.abs(cle - (y <= 0).sum(axis=0)) <= T) and np.all(np.abs(cge - (y >= 0).sum(axis=0)) <= T)
+    ref_h = oracle.evaluate_directions(z, X, U, "halfspace")
+    np.testing.assert_array_equal(b200.evaluate_directions(z, data, U, "halfspace", b200.ParallelConfig()), ref_h)
+    for notion in ("projection", "asym_projection"):
+        got = b200.evaluate_directions(z, data, U, notion, b200.ParallelConfig())
+        np.testing.assert_allclose(got, oracle.evaluate_directions(z, X, U, notion), rtol=DEPTH_RTOL, atol=0)
+    cfg = b200.RrsConfig(total_directions=600, refinements=3, shrink=0.9, notion="halfspace", seed=7)
+    Z = np.vstack([X[:3], 0.2 * X[3:5]])
+    dg = b200.depth_batch_arrays(Z, data, cfg)[0]
+    dr = oracle.depth_batch(Z, X, total_directions=600, refinements=3, shrink=0.9, notion="halfspace", seed=7)[0]
+    assert np.array_equal(dg, dr), (dg, dr)
