@@ -242,6 +242,9 @@ def main():
                     help="process group for N>1 (gloo: ranks may share one GPU, the single-GPU rehearsal)")
     ap.add_argument("--select-path", default="auto", choices=["auto", "radix", "wide"],
                     help="order-statistic kernel of the projection notions (A/B)")
+    ap.add_argument("--early-exit", action="store_true",
+                    help="RrsConfig(early_exit=True): exact early exit of finished halfspace queries "
+                         "(outputs bitwise unchanged; not the default, which does the reference's full work)")
     ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "tensor2", "filter"],
                     help="halfspace contraction kernel (auto: the library's choice)")
     args = ap.parse_args()
@@ -271,7 +274,8 @@ def main():
     if args.batch:
         B = args.batch
     m = -(-k // r)
-    cfg = rrs.RrsConfig(total_directions=k, refinements=r, shrink=alpha, notion=notion, seed=1)
+    cfg = rrs.RrsConfig(total_directions=k, refinements=r, shrink=alpha, notion=notion, seed=1,
+                        early_exit=args.early_exit)
     X = make_data(distn, n, d)
     eng = rrs.engine(local)
     eng.set_contract_path(args.contract_path)
@@ -311,10 +315,11 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    recs = []
     for i in range(args.steps):
         flush.zero_()  # L2 flush between timed iterations (outside the events)
         ev[i][0].record(stream)
-        run_step(args.warmup + i)
+        recs.append(run_step(args.warmup + i))
         ev[i][1].record(stream)
         st = eng.stats()  # syncs; per-kernel event times of this step
         launches += st["kernel_launches"]
@@ -333,6 +338,37 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     value = world * B * args.steps / (ms_max / 1e3)
+
+    # Side measurement, not the headline: the same steps with RrsConfig(early_exit=True)
+    # (halfspace: a query stops once its best count equals the rows coinciding with it;
+    # outputs must be bitwise those of the full-work steps above, checked here)
+    early = None
+    if notion == "halfspace" and not args.early_exit:
+        import dataclasses
+
+        cfg_full = cfg
+        cfg = dataclasses.replace(cfg_full, early_exit=True)
+        run_step(0)  # warm-up of the early-exit variant
+        torch.cuda.synchronize()
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        same = True
+        for i in range(args.steps):
+            flush.zero_()
+            ev2[i][0].record(stream)
+            rec = run_step(args.warmup + i)
+            ev2[i][1].record(stream)
+            same = same and bool(torch.equal(rec, recs[i]))
+        torch.cuda.synchronize()
+        ms2 = sum(a.elapsed_time(b) for a, b in ev2)
+        t2 = torch.tensor([ms2, 0.0 if same else 1.0], dtype=torch.float64, device=red_dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        early = {"value": world * B * args.steps / (float(t2[0].item()) / 1e3), "unit": "query-depths/s",
+                 "ms_per_step": float(t2[0].item()) / args.steps,
+                 "outputs_bitwise_equal_to_full_run": bool(t2[1].item() == 0.0),
+                 "what": "RrsConfig(early_exit=True): the same steps with finished queries stopped "
+                         "(best count == rows coinciding with the query); not the headline value"}
+        cfg = cfg_full
 
     # roofline of the dominant kernel (K2 contraction)
     flops_total = 2.0 * n * d * m * r * B * args.steps  # algorithmic: 2 n d m per (query, refinement)
@@ -442,8 +478,9 @@ def main():
                        "n_refinements": r, "directions_per_refinement": m, "sphcap_shrink": alpha,
                        "queries_per_gpu_per_step": B, "global_batch": B * world, "parallelism": f"query-shard x{world}",
                        "dist_backend": args.dist_backend if world > 1 else None,
-                       "l2": "flushed between timed steps (256 MiB write)"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "early_exit": bool(args.early_exit)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "early_exit": early,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define RRS_ABI_VERSION 2
+#define RRS_ABI_VERSION 3
 
 typedef enum {
     RRS_OK = 0,
@@ -51,6 +51,12 @@ typedef struct {
     int32_t notion;           /* rrs_notion                                   */
     uint64_t seed;            /* seed mod 2^64 (philox.py:68-71)              */
     int32_t pole_update;      /* rrs_pole_update                              */
+    int32_t early_exit;       /* halfspace: skip a query's remaining refinements
+                                 once its best count equals the number of data
+                                 rows coinciding with it (no direction can go
+                                 strictly below: depth, argmin and trace are
+                                 bitwise those of the full run).  0 = off (the
+                                 reference's cost model), 1 = on.             */
 } rrs_config;
 
 typedef struct rrs_engine rrs_engine;

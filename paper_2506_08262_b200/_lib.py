@@ -35,6 +35,7 @@ class RrsConfigC(ctypes.Structure):
         ("notion", ctypes.c_int32),
         ("seed", ctypes.c_uint64),
         ("pole_update", ctypes.c_int32),
+        ("early_exit", ctypes.c_int32),
     ]
 
 
@@ -117,7 +118,7 @@ def load_library():
                 fn = getattr(L, name)
                 fn.restype = res
                 fn.argtypes = args
-            if L.rrs_abi_version() != 2:
+            if L.rrs_abi_version() != 3:
                 raise RuntimeError("librrs_b200.so ABI version mismatch")
             _lib = L
     return _lib
@@ -178,7 +179,7 @@ def device_count() -> int:
 def config_struct(cfg) -> RrsConfigC:
     return RrsConfigC(int(cfg.total_directions), int(cfg.refinements), float(cfg.shrink),
                       NOTION_CODES[cfg.notion], int(cfg.seed) % (1 << 64),
-                      POLE_UPDATE_CODES[cfg.pole_update])
+                      POLE_UPDATE_CODES[cfg.pole_update], 1 if getattr(cfg, "early_exit", False) else 0)
 
 
 class Engine:

@@ -117,6 +117,11 @@ class RrsConfig:
     seed: int = 0
     parallel: ParallelConfig = field(default_factory=ParallelConfig)
     pole_update: str = "per_refinement"
+    # B200 extension (halfspace): stop a query once its best count equals the
+    # number of data rows coinciding with it -- the strict-< update
+    # (optimizer.py:202) can then never fire again, so depth, argmin and trace
+    # are bitwise those of the full run; off by default (the reference's cost)
+    early_exit: bool = False
 
     def __post_init__(self):
         if self.refinements < 1 or self.total_directions < self.refinements:

@@ -118,6 +118,33 @@ __global__ void store64_kernel(const double* __restrict__ xc, const double* __re
     out[i] = (float)s;
 }
 
+// early exit (halfspace): rows equal to the query in FP32 in every coordinate
+// (x - z == 0 in the contraction, ties for every direction), per query
+__global__ void __launch_bounds__(BM) coincide32_kernel(const float* __restrict__ xb, const float* __restrict__ zq,
+                                                        int64_t n, int d, int64_t tiles, long long* __restrict__ c0) {
+    const int q = blockIdx.y;
+    const float* z = zq + (size_t)q * d;
+    int cnt = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        if (t * BM + threadIdx.x >= n) continue;
+        const float* xr = xb + (size_t)t * d * BM + threadIdx.x;
+        int l = 0;
+        while (l < d && xr[(size_t)l * BM] == z[l]) ++l;
+        cnt += l == d;
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(reinterpret_cast<unsigned long long*>(c0 + q), (unsigned long long)cnt);
+}
+
+cudaError_t launch_coincide_count32(const float* xb, const float* zq, int64_t n, int d, int64_t tiles, int Qb,
+                                    long long* c0, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(c0, 0, (size_t)Qb * 8, st);
+    if (e != cudaSuccess) return e;
+    const int64_t blocks = tiles < 64 ? tiles : 64;
+    coincide32_kernel<<<dim3((unsigned)blocks, (unsigned)Qb), BM, 0, st>>>(xb, zq, n, d, tiles, c0);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_center_sample(const double* x, int64_t n, int d, double* center, cudaStream_t st) {
     center_sample_kernel<<<d, 512, 0, st>>>(x, n, d, center);
     return cudaGetLastError();

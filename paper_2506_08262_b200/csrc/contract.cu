@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
     const int jbl = rem / a.chunks;
     const int c = rem - jbl * a.chunks;
     const int jb = a.jb0 + jbl;
+    if (!STORE && a.done && a.done[q]) return;  // early exit (before any barrier / TMA)
     const int64_t t_begin = (int64_t)c * a.tiles_per_unit;
     int64_t t_end = t_begin + a.tiles_per_unit;
     if (t_end > a.tiles) t_end = a.tiles;

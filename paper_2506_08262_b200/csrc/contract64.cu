@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(C64_T) contract64_kernel(const Contract64Args 
     const int64_t p0 = (int64_t)blockIdx.x * C64_P;
     const int j0 = blockIdx.y * C64_J;  // direction within the launch's range
     const int q = blockIdx.z;
+    if (!STORE && a.done && a.done[q]) return;  // early exit
     const int d = a.d;
     const double* cq = a.c + (size_t)q * a.c_stride;
     const double* ub = a.u64 + ((size_t)q * a.m + a.jbase) * d;
@@ -106,6 +107,32 @@ __global__ void __launch_bounds__(C64_T) contract64_kernel(const Contract64Args 
             }
         }
     }
+}
+
+// rows of the FP64 data equal to the query in every coordinate, per query
+__global__ void coincide64_kernel(const double* __restrict__ x, const double* __restrict__ z, int64_t n, int d,
+                                  long long* __restrict__ c0) {
+    const int q = blockIdx.y;
+    const double* zq = z + (size_t)q * d;
+    int cnt = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double* xr = x + i * d;
+        int l = 0;
+        while (l < d && xr[l] == zq[l]) ++l;
+        cnt += l == d;
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(reinterpret_cast<unsigned long long*>(c0 + q), (unsigned long long)cnt);
+}
+
+cudaError_t launch_coincide_count64(const double* x64, const double* z, int64_t n, int d, int Qb, long long* c0,
+                                    cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(c0, 0, (size_t)Qb * 8, st);
+    if (e != cudaSuccess) return e;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 64) blocks = 64;
+    coincide64_kernel<<<dim3((unsigned)blocks, (unsigned)Qb), 256, 0, st>>>(x64, z, n, d, c0);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_contract64(const Contract64Args& a, bool store, cudaStream_t st) {

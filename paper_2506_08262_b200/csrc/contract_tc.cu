@@ -107,6 +107,17 @@ struct TcUnit {
     int64_t t0, t1;      // point tiles [t0, t1)
 };
 
+// first unit >= u of this CTA's stride whose query is still live (early exit:
+// done[] is written by the previous update kernel and read-only here, so every
+// warp role walks the same unit sequence)
+__device__ __forceinline__ int64_t tc_next(const TcArgs& a, int64_t u, int64_t units) {
+    if (a.done) {
+        const int64_t per_q = (int64_t)a.groups * a.chunks;
+        while (u < units && a.done[u / per_q]) u += gridDim.x;
+    }
+    return u;
+}
+
 __device__ __forceinline__ TcUnit tc_unit(const TcArgs& a, int64_t u) {
     TcUnit r;
     const int64_t per_q = (int64_t)a.groups * a.chunks;
@@ -129,7 +140,7 @@ __device__ __forceinline__ void mma_issue(const TcArgs& a, int64_t units, unsign
     // F32 accumulate, FP16 A and B, K-major both, N = 128, M = 128
     const uint32_t idesc = (1u << 4) | ((uint32_t)(TC_NP >> 3) << 17) | ((uint32_t)(TC_MD >> 4) << 24);
     uint32_t it = 0, gtile = 0, gacc = 0, gph = 0;
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+    for (int64_t u = tc_next(a, blockIdx.x, units); u < units; u = tc_next(a, u + gridDim.x, units), ++it) {
         const TcUnit w = tc_unit(a, u);
         for (int b = 0; b < w.nbg; ++b, ++gph) {
             mbar_wait_sleep(dfull, gph & 1u);
@@ -230,7 +241,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     if (warp == 0) {
         // -------------------------------- producer: unit direction blocks, one at a time
         uint32_t gph = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int64_t u = tc_next(a, blockIdx.x, units); u < units; u = tc_next(a, u + gridDim.x, units)) {
             const TcUnit w = tc_unit(a, u);
             const unsigned char* src = a.uop + ((size_t)w.q * a.NB + (size_t)w.grp * a.gb) * stage_bytes;
             for (int b = 0; b < w.nbg; ++b, ++gph) {
@@ -259,7 +270,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     } else if (warp == 2) {
         // -------------------------------------- producer: raw FP32 point tiles
         uint32_t g = 0, rs = 0, rph = 0;  // ring slot and its phase, advanced incrementally
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int64_t u = tc_next(a, blockIdx.x, units); u < units; u = tc_next(a, u + gridDim.x, units)) {
             const TcUnit w = tc_unit(a, u);
             for (int64_t t = w.t0; t < w.t1; ++t, ++g) {
                 if (g >= (uint32_t)RS) mbar_wait_sleep(&rempty[rs], rph ^ 1u);
@@ -279,7 +290,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
         const int h = ct >> 7;                    // coordinates [32 h, 32 h + 32)
         const int main_chunks = 2 * L.q16;        // 8-coordinate chunks in the aligned part
         uint32_t it = 0, gtile = 0, rs = 0, rph = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+        for (int64_t u = tc_next(a, blockIdx.x, units); u < units; u = tc_next(a, u + gridDim.x, units), ++it) {
             const TcUnit w = tc_unit(a, u);
             float* zs = sZ + (it & 1u) * TC_MAXD;
             if (ct < TC_MAXD) zs[ct] = ct < d ? __ldg(a.zq + (size_t)w.q * d + ct) : 0.0f;
@@ -394,7 +405,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
         const int half = (warp - TC_EPI_WARP0) >> 2;   // 64-point half of the tile
         const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
         uint32_t it = 0, gacc = 0, gtile = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+        for (int64_t u = tc_next(a, blockIdx.x, units); u < units; u = tc_next(a, u + gridDim.x, units), ++it) {
             const TcUnit w = tc_unit(a, u);
             uint32_t cnt[TC_GB_MAX];  // #(y<0) per resident block
 #pragma unroll

@@ -101,6 +101,15 @@ __device__ __forceinline__ WUnit w_unit(const TcArgs& a, int64_t u) {
     return r;
 }
 
+// first unit >= u of this CTA's stride whose query is still live (early exit)
+__device__ __forceinline__ int64_t w_next(const TcArgs& a, int64_t u, int64_t units) {
+    if (a.done) {
+        const int64_t per_c = (int64_t)a.Qb * a.NB;
+        while (u < units && a.done[(u % per_c) / a.NB]) u += gridDim.x;
+    }
+    return u;
+}
+
 __device__ __forceinline__ int slice_width(int d, int s) {
     const int w = d - TC_SLICE * s;
     return w < TC_SLICE ? w : TC_SLICE;
@@ -272,7 +281,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
     if (warp == 0) {
         // ----------------------- producer: the unit's direction block, slice by slice
         uint32_t g = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int64_t u = w_next(a, blockIdx.x, units); u < units; u = w_next(a, u + gridDim.x, units)) {
             const WUnit w = w_unit(a, u);
             const unsigned char* src = a.uop + ((size_t)w.q * a.NB + w.blk) * (size_t)L.ns * 4096;
             for (int s = 0; s < S; ++s)
@@ -289,7 +298,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
         // -------------------------------------------------------- MMA issuer
         const uint32_t idesc = (1u << 4) | ((uint32_t)(W_NP >> 3) << 17) | ((uint32_t)(W_MD >> 4) << 24);
         uint32_t it = 0, g = 0, gs = 0, gacc = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+        for (int64_t u = w_next(a, blockIdx.x, units); u < units; u = w_next(a, u + gridDim.x, units), ++it) {
             const WUnit w = w_unit(a, u);
             for (int s = 0; s < S; ++s)
                 for (int k0 = 0; k0 < slice_ns(L, s); k0 += W_DSTEPS, ++g) {
@@ -323,7 +332,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
     } else if (warp == 2) {
         // --------------------------------- producer: raw FP32 rows per (tile, slice)
         uint32_t g = 0, rs = 0, rph = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int64_t u = w_next(a, blockIdx.x, units); u < units; u = w_next(a, u + gridDim.x, units)) {
             const WUnit w = w_unit(a, u);
             for (int64_t t = w.t0; t < w.t1; ++t) {
                 for (int s = 0; s < S; ++s, ++g) {
@@ -346,7 +355,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
         const int r = ct & (W_NP - 1);
         const int h = ct >> 7;                      // coordinate group: [W_CPT h, W_CPT h + W_CPT) of a slice
         uint32_t it = 0, gs = 0, rs = 0, rph = 0, gtile = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+        for (int64_t u = w_next(a, blockIdx.x, units); u < units; u = w_next(a, u + gridDim.x, units), ++it) {
             const WUnit w = w_unit(a, u);
             float* zs = sZ + (it & 1u) * W_MAXD;
             float zl = 0.0f;
@@ -419,7 +428,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
         const int half = (warp - W_EPI_WARP0) >> 2;
         const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
         uint32_t gacc = 0, gtile = 0;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int64_t u = w_next(a, blockIdx.x, units); u < units; u = w_next(a, u + gridDim.x, units)) {
             const WUnit w = w_unit(a, u);
             uint32_t cnt = 0u, zsum = 0u;
             for (int64_t t = w.t0; t < w.t1; ++t, ++gtile, ++gacc) {

@@ -94,6 +94,7 @@ struct rrs_engine {
     // workspace
     DevBuf zq, u64, u32, uop, counts, depths, y, pole, reflv, reflmode, dmin, bestcnt;
     DevBuf zq0, shift;  // projection notions: zero queries for the centred store, <u, m - z> per direction
+    DevBuf done, c0;    // early exit (halfspace): finished flags, coinciding-row counts per query
     // 0 auto, 1 FFMA (contract.cu), 2 tensor cores (contract_tc.cu two-term split for d <= 64,
     // contract_tcw.cu above), 3 2-SM split (contract_tc2.cu), 4 filter and refine (contract_tcf.cu, d <= 64)
     int contract_path = 0;
@@ -156,6 +157,7 @@ int validate_cfg(const rrs_config* c) {
     if (c->notion < 0 || c->notion > 2) return fail(RRS_ERR_INVALID, "unknown depth notion");
     if (c->pole_update < 0 || c->pole_update > 1)
         return fail(RRS_ERR_INVALID, "unknown pole update mode");
+    if (c->early_exit < 0 || c->early_exit > 1) return fail(RRS_ERR_INVALID, "early_exit must be 0 or 1");
     if ((c->total_directions + c->refinements - 1) / c->refinements > (int64_t)1 << 24)
         return fail(RRS_ERR_INVALID, "directions per refinement exceed 2^24");
     return RRS_OK;
@@ -276,7 +278,7 @@ ContractArgs contract_args(rrs_engine* e, const Plan& p, int Qb, int jb0, int jb
     return c;
 }
 
-int contract_halfspace(rrs_engine* e, const Plan& p, int Qb, const double* zdev) {
+int contract_halfspace(rrs_engine* e, const Plan& p, int Qb, const double* zdev, const int* done) {
     if (p.wide) {
         Contract64Args c{};
         c.x64 = e->x64.as<double>();
@@ -291,6 +293,7 @@ int contract_halfspace(rrs_engine* e, const Plan& p, int Qb, const double* zdev)
         c.jbase = 0;
         c.jcount = p.m;
         c.Qb = Qb;
+        c.done = done;
         CK(launch_contract64(c, false, e->stream));
     } else if (p.tcf) {
         TcfArgs t{};
@@ -322,6 +325,7 @@ int contract_halfspace(rrs_engine* e, const Plan& p, int Qb, const double* zdev)
         t.m = p.m;
         t.mpad = p.mpad;
         t.xmax = e->xmax.as<float>();
+        t.done = done;
         if (e->d > TC_SLICE)
             CK(launch_contract_tcw(t, e->sms, e->stream));
         else if (e->contract_path == 3)
@@ -331,6 +335,7 @@ int contract_halfspace(rrs_engine* e, const Plan& p, int Qb, const double* zdev)
         e->stats.tensor_contract_launches++;
     } else {
         ContractArgs c = contract_args(e, p, Qb, 0, p.MB);
+        c.done = done;
         CK(launch_contract_count(c, e->stream));
     }
     return RRS_OK;
@@ -463,9 +468,26 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
     if (cfg->notion == RRS_HALFSPACE)
         CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.Qb * p.mpad * 2 * 4, e->stream));
     const int d = e->d;
+    // early exit (halfspace; not on the experimental 2-SM / filter kernels)
+    const bool early = cfg->notion == RRS_HALFSPACE && cfg->early_exit != 0 && !p.tcf &&
+                       !(p.tc && e->contract_path == 3 && e->d <= TC_SLICE);
+    int* done = nullptr;
+    long long* c0 = nullptr;
+    if (early) {
+        CK(e->done.ensure((size_t)p.Qb * 4));
+        CK(e->c0.ensure((size_t)p.Qb * 8));
+        done = e->done.as<int>();
+        c0 = e->c0.as<long long>();
+    }
     for (int64_t b0 = 0; b0 < Q; b0 += p.Qb) {
         const int Qb = (int)((Q - b0) < p.Qb ? (Q - b0) : p.Qb);
         CK(launch_queries_to_f32(zdev + b0 * d, e->zq.as<float>(), (int64_t)Qb * d, e->stream));
+        if (early) {
+            CK(cudaMemsetAsync(done, 0, (size_t)Qb * 4, e->stream));
+            if (p.wide) CK(launch_coincide_count64(e->x64.as<double>(), zdev + b0 * d, e->n, d, Qb, c0, e->stream));
+            else CK(launch_coincide_count32(e->xb.as<float>(), e->zq.as<float>(), e->n, d, e->tiles, Qb, c0, e->stream));
+            e->stats.kernel_launches += 1;
+        }
         StateArgs s{e->pole.as<double>(), e->reflv.as<double>(), e->reflmode.as<int>(),
                     e->dmin.as<double>(), e->bestcnt.as<long long>(), (long long)e->n, Qb, d};
         CK(launch_state_init(s, e->stream));
@@ -491,6 +513,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 g.uop_mode = p.tcf ? 1 : 0;
                 g.u32r = p.tcf ? e->u32.as<float>() : nullptr;
                 g.NB = p.nb8;
+                g.done = done;
                 CK(launch_cap_generate(g, e->stream));
                 e->stats.kernel_launches++;
                 if (p.tcs) {  // six-product operand of the projection store from the FP64 directions
@@ -501,7 +524,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
             }
             if (cfg->notion == RRS_HALFSPACE) {
                 Timer t(e, 1);
-                if (int rc = contract_halfspace(e, p, Qb, zdev + b0 * d)) return rc;
+                if (int rc = contract_halfspace(e, p, Qb, zdev + b0 * d, done)) return rc;
                 e->stats.kernel_launches++;
                 e->stats.contract_launches++;
             } else {
@@ -528,6 +551,8 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 u.r = r;
                 u.refinement = l;
                 u.notion = cfg->notion;
+                u.done = done;
+                u.c0 = c0;
                 CK(launch_update(u, e->stream));
                 e->stats.kernel_launches++;
             }
@@ -615,7 +640,7 @@ int rrs_engine_destroy(rrs_engine* e) {
     for (DevBuf* b : {&e->xb, &e->xmax, &e->zq, &e->u64, &e->u32, &e->uop, &e->counts, &e->depths, &e->y, &e->pole,
                       &e->reflv, &e->reflmode, &e->dmin, &e->bestcnt, &e->tmp_in, &e->tmp_out0,
                       &e->tmp_out1, &e->tmp_out2, &e->tmp_out3, &e->center, &e->xcb, &e->xc64, &e->zq0,
-                      &e->shift, &e->fallbacks, &e->x64})
+                      &e->shift, &e->fallbacks, &e->x64, &e->done, &e->c0})
         b->release();
     for (auto ev : e->ev_pool) cudaEventDestroy(ev);
     if (e->own) cudaStreamDestroy(e->own);
@@ -843,7 +868,7 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
     if (p.tcs) CK(launch_pack_tc6_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (notion == RRS_HALFSPACE) {
         CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.mpad * 2 * 4, e->stream));
-        if (int rc = contract_halfspace(e, p, 1, e->tmp_in.as<double>())) return rc;
+        if (int rc = contract_halfspace(e, p, 1, e->tmp_in.as<double>(), nullptr)) return rc;
         std::vector<int> cnt((size_t)p.mpad * 2);
         CK(cudaMemcpyAsync(cnt.data(), e->counts.p, cnt.size() * 4, cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));

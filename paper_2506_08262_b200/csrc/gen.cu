@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(256) cap_generate_kernel(GenArgs a) {
     const int warp = threadIdx.x >> 5;
     const int64_t gdir = (int64_t)blockIdx.x * 8 + warp;  // over Qb * mpad
     if (gdir >= (int64_t)a.Qb * a.mpad) return;
+    if (a.done && a.done[gdir / a.mpad]) return;  // early exit: the query is finished
     double* g = gsm + (size_t)warp * 2 * a.d;  // d values + d scratch
     gen_direction_warp(a, gdir, g, g + a.d);
 }
@@ -378,6 +379,7 @@ __global__ void __launch_bounds__(GV_THREADS, RRS_GEN_BLOCKS_PER_SM) cap_generat
     const int64_t gdir0 = (int64_t)blockIdx.x * GV_DIRS;
     const int q = (int)(gdir0 / a.mpad);
     const int j0 = (int)(gdir0 % a.mpad);       // GV_DIRS | 128 | mpad: one query, one 128-block
+    if (a.done && a.done[q]) return;            // early exit: the query is finished (block-uniform)
     const int nval = a.m - j0 < GV_DIRS ? (a.m - j0 > 0 ? a.m - j0 : 0) : GV_DIRS;
     const uint32_t qg = (uint32_t)((uint64_t)(a.q0 + q) & 0xFFFFFFFFu);
     const uint32_t l = a.refinement;
@@ -617,6 +619,21 @@ __global__ void __launch_bounds__(256) update_kernel(UpdateArgs a) {
     __shared__ int s_improved;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int d = a.d;
+    if (a.done && a.done[q]) {
+        // early exit: no direction can beat the best count any more (it equals the
+        // rows coinciding with the query); the record repeats the state, exactly
+        // what the full run writes when the strict-< update does not fire
+        if (a.trace) {
+            double* rec = a.trace + ((size_t)q * a.r + a.refinement) * (2 + d);
+            const double* pole = a.pole + (size_t)q * d;
+            for (int c = tid; c < d; c += blockDim.x) rec[2 + c] = pole[c];
+            if (tid == 0) {
+                rec[0] = a.dmin[q];
+                rec[1] = a.eps;
+            }
+        }
+        return;
+    }
     double bval = INFINITY;
     long long bcnt = 0;
     int bidx = 0x7fffffff;
@@ -712,6 +729,9 @@ __global__ void __launch_bounds__(256) update_kernel(UpdateArgs a) {
     if (a.notion == 0) {
         int* cnt = a.counts + (size_t)q * a.mpad * 2;
         for (int j = tid; j < a.mpad * 2; j += blockDim.x) cnt[j] = 0;
+        // every direction's count is >= the rows coinciding with the query (they
+        // are ties on both sides), so a best count at that bound is final
+        if (a.done && tid == 0 && a.best_count[q] <= a.c0[q]) a.done[q] = 1;
     }
 }
 

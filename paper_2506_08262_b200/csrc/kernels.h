@@ -22,6 +22,7 @@ struct GenArgs {
     uint32_t refinement;
     double eps;
     int Qb, m, mpad, d;
+    const int* done;         // nullable [Qb]: early exit, skip these queries
 };
 
 struct StateArgs {
@@ -47,6 +48,8 @@ struct UpdateArgs {
     long long n;
     double eps;
     int Qb, m, mpad, d, r, refinement, notion;
+    int* done;               // nullable [Qb]: early exit (halfspace); set when best count <= c0
+    const long long* c0;     // [Qb] rows coinciding with the query (the count's lower bound)
 };
 
 struct FinalArgs {
@@ -75,6 +78,7 @@ struct ContractArgs {
     int m;                   // real directions per query
     int tiles_per_unit;
     int chunks;              // ceil(T / tiles_per_unit)
+    const int* done;         // nullable [Qb]: early exit, skip these queries (count mode)
 };
 
 // Tensor-core (FP16 hi/lo split) halfspace contraction, contract_tc.cu.
@@ -235,6 +239,7 @@ struct TcArgs {
     // filled by launch_contract_tc
     int groups, chunks, raw_stages, gb;
     int64_t tiles_per_chunk;
+    const int* done;            // nullable [Qb]: early exit, units of these queries are skipped
 };
 
 // Filter-and-refine halfspace contraction (contract_tcf.cu, d <= 64): one FP16
@@ -307,8 +312,15 @@ struct Contract64Args {
     float* y;                // [Qb][jcount][n], store mode
     int64_t n;
     int d, m, mpad, jbase, jcount, Qb;
+    const int* done;         // nullable [Qb]: early exit, skip these queries (count mode)
 };
 cudaError_t launch_contract64(const Contract64Args& a, bool store, cudaStream_t st);
+// early exit: rows coinciding with each query (FP32 equality on the blocked
+// data, or FP64 on the row-major copy for the d > 256 path)
+cudaError_t launch_coincide_count32(const float* xb, const float* zq, int64_t n, int d, int64_t tiles, int Qb,
+                                    long long* c0, cudaStream_t st);
+cudaError_t launch_coincide_count64(const double* x64, const double* z, int64_t n, int d, int Qb, long long* c0,
+                                    cudaStream_t st);
 // centred frame of the projection notions (center.cu)
 constexpr int64_t STORE64_N = 4096;  // below: FP64-accumulated store from an FP64 centred copy
 cudaError_t launch_center_sample(const double* x, int64_t n, int d, double* center, cudaStream_t st);

@@ -29,7 +29,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(L, s), s
     assert {name for name, _, _ in _lib.SIGNATURES} == set(syms)
-    assert L.rrs_abi_version() == 2
+    assert L.rrs_abi_version() == 3
 
 
 def test_library_is_sm100a_only():

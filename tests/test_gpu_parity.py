@@ -560,3 +560,36 @@ def test_wide_dimensions(b200, d):
     dg = b200.depth_batch_arrays(Z, data, cfg)[0]
     dr = oracle.depth_batch(Z, X, total_directions=600, refinements=3, shrink=0.9, notion="halfspace", seed=7)[0]
     assert np.array_equal(dg, dr), (dg, dr)
+
+
+@pytest.mark.parametrize("case", ["tensor_d50", "tensor_d80", "ffma_small_n", "wide_d300", "ffma_forced"])
+def test_early_exit_bitwise(b200, case):
+    """RrsConfig(early_exit=True): a query stops once its best count equals the
+    rows coinciding with it (the strict-< update, optimizer.py:202, can never
+    fire again).  Depth, argmin, min count and every trace record must be
+    bitwise those of the full run, for in-sample queries (bound 1, reached
+    early), duplicated rows (bound 2), off-sample and far queries (bound 0)."""
+    from paper_2506_08262_b200.synthetic import toeplitz_gaussian
+
+    n, d, path = {"tensor_d50": (20000, 50, "auto"), "tensor_d80": (8000, 80, "auto"),
+                  "ffma_small_n": (3000, 6, "auto"), "wide_d300": (3000, 300, "auto"),
+                  "ffma_forced": (6000, 12, "ffma")}[case]
+    X = toeplitz_gaussian(d, n, seed=9)
+    X[1] = X[0]  # a duplicated row: its count bound is 2
+    Z = np.vstack([X[:40], 0.3 * X[40:48], X[50:52] * 50.0])
+    data = b200.Dataset(X)
+    kw = dict(total_directions=3000, refinements=15, shrink=0.8, notion="halfspace", seed=3)
+    eng = b200.engine()
+    eng.set_contract_path(path)
+    try:
+        full = b200.depth_batch_arrays(Z, data, b200.RrsConfig(**kw), trace=True)
+        eng.enable_timing(True)
+        fast = b200.depth_batch_arrays(Z, data, b200.RrsConfig(early_exit=True, **kw), trace=True)
+        launches = eng.stats()["kernel_launches"]
+        eng.enable_timing(False)
+    finally:
+        eng.set_contract_path("auto")
+    for a, b in zip(full, fast):
+        assert np.array_equal(a, b)
+    assert full[3][0] >= 2 and full[3][1] >= 2  # the duplicated pair: bound 2
+    print(f"\n{case}: final counts {np.bincount(full[3])[:4]}, launches {launches}")
