@@ -96,7 +96,7 @@ class ClockSampler:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+                 "-lms", "50"], stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
@@ -245,7 +245,7 @@ def main():
     ap.add_argument("--early-exit", action="store_true",
                     help="RrsConfig(early_exit=True): exact early exit of finished halfspace queries "
                          "(outputs bitwise unchanged; not the default, which does the reference's full work)")
-    ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "tensor2", "filter"],
+    ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "filter"],
                     help="halfspace contraction kernel (auto: the library's choice)")
     args = ap.parse_args()
     wl = args.workload

@@ -153,8 +153,7 @@ int rrs_philox4x32_host(rrs_engine* e, const uint32_t* ctr, int64_t N, uint32_t 
 /* Halfspace contraction kernel: 0 = auto (tensor cores when d <= 256 and
  * n >= 4096), 1 = FP32 FFMA (contract.cu), 2 = tcgen05 FP16 hi/lo split with
  * FP32 accumulation (contract_tc.cu for d <= 64, contract_tcw.cu for
- * 64 < d <= 256), 3 = the d <= 64 kernel on SM pairs with cta_group::2 MMAs
- * (contract_tc2.cu; wider d takes contract_tcw.cu), 4 = filter and refine
+ * 64 < d <= 256), 4 = filter and refine
  * (contract_tcf.cu, d <= 64).  Any d > 256 (up to 1024) takes the FP64
  * contraction (contract64.cu) whatever the path. */
 int rrs_engine_set_contract_path(rrs_engine* e, int32_t path);

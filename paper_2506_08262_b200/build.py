@@ -25,7 +25,6 @@ SOURCES = {  # file -> extra flags
     "contract.cu": [],
     "contract_tc.cu": [],
     "contract_tcf.cu": [],
-    "contract_tc2.cu": [],
     "contract_tcw.cu": [],
     "contract_tcs.cu": [],
     "select.cu": [],

@@ -96,7 +96,7 @@ struct rrs_engine {
     DevBuf zq0, shift;  // projection notions: zero queries for the centred store, <u, m - z> per direction
     DevBuf done, c0;    // early exit (halfspace): finished flags, coinciding-row counts per query
     // 0 auto, 1 FFMA (contract.cu), 2 tensor cores (contract_tc.cu two-term split for d <= 64,
-    // contract_tcw.cu above), 3 2-SM split (contract_tc2.cu), 4 filter and refine (contract_tcf.cu, d <= 64)
+    // contract_tcw.cu above), 4 filter and refine (contract_tcf.cu, d <= 64); 3 (2-SM split) was removed
     int contract_path = 0;
     int select_path = 0;  // 0 auto (select v3 where it applies), 2 radix select v2
     DevBuf fallbacks;     // device counter of select-v3 rows that left their bracket
@@ -328,8 +328,6 @@ int contract_halfspace(rrs_engine* e, const Plan& p, int Qb, const double* zdev,
         t.done = done;
         if (e->d > TC_SLICE)
             CK(launch_contract_tcw(t, e->sms, e->stream));
-        else if (e->contract_path == 3)
-            CK(launch_contract_tc2(t, e->sms, e->stream));
         else
             CK(launch_contract_tc(t, e->sms, e->stream));
         e->stats.tensor_contract_launches++;
@@ -469,8 +467,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
         CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.Qb * p.mpad * 2 * 4, e->stream));
     const int d = e->d;
     // early exit (halfspace; not on the experimental 2-SM / filter kernels)
-    const bool early = cfg->notion == RRS_HALFSPACE && cfg->early_exit != 0 && !p.tcf &&
-                       !(p.tc && e->contract_path == 3 && e->d <= TC_SLICE);
+    const bool early = cfg->notion == RRS_HALFSPACE && cfg->early_exit != 0 && !p.tcf;
     int* done = nullptr;
     long long* c0 = nullptr;
     if (early) {
@@ -670,9 +667,10 @@ int rrs_engine_set_workspace_limit(rrs_engine* e, int64_t bytes) {
 
 int rrs_engine_set_contract_path(rrs_engine* e, int32_t path) {
     if (!e) return fail(RRS_ERR_INVALID, "engine is null");
-    if (path < 0 || path > 4)
+    if (path < 0 || path > 4 || path == 3)
         return fail(RRS_ERR_INVALID,
-                    "contract path must be 0 (auto), 1 (FFMA), 2 (tensor), 3 (2-SM split) or 4 (filter and refine)");
+                    "contract path must be 0 (auto), 1 (FFMA), 2 (tensor) or 4 (filter and refine); "
+                    "3 (the 2-SM split kernel) was removed");
     e->contract_path = path;
     return RRS_OK;
 }

@@ -336,7 +336,6 @@ cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st);
 cudaError_t launch_contract_tcf(TcfArgs a, int sms, cudaStream_t st);  // filter and refine, d <= 64
 cudaError_t launch_pack_tcf_operand(const double* u64, unsigned char* uop, float* u32r, int Qb, int m, int NB,
                                     int mpad, int d, cudaStream_t st);
-cudaError_t launch_contract_tc2(TcArgs a, int sms, cudaStream_t st);  // 2-SM (cta_group::2) variant
 cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st);  // 64 < d <= 256 (contract_tcw.cu)
 cudaError_t launch_contract_tcs(TcsArgs a, int sms, cudaStream_t st);  // projection store, d <= 64
 cudaError_t launch_pack_tc6_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,

@@ -17,7 +17,6 @@ eng = rrs.engine()
 cases = [
     # (n, d, notion, contract path, select path)
     (4100, 50, "halfspace", "tensor", "auto"),     # contract_tc + cap_generate_v2 + update
-    (4100, 50, "halfspace", "tensor2", "auto"),    # contract_tc2 (cta_group::2)
     (4100, 50, "halfspace", "filter", "auto"),     # contract_tcf
     (4100, 80, "halfspace", "tensor", "auto"),     # contract_tcw
     (1000, 5, "halfspace", "ffma", "auto"),        # contract_kernel<count>

@@ -18,7 +18,7 @@ TIE_REL = 1e-6
 DEPTH_RTOL = 1e-5
 
 
-PATHS = ["ffma", "tensor", "tensor2", "filter"]
+PATHS = ["ffma", "tensor", "filter"]
 
 
 class contract_path:
