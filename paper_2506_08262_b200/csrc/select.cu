@@ -914,15 +914,13 @@ __device__ __forceinline__ void s3_sort_sample(uint32_t v, Sel3Shared<NT>& sh) {
         for (int c = 0; c < C; ++c) {
             if (c == w) continue;
             const uint32_t* ch = sh.sdev + 32 * c;
-            const bool le = c < w;  // earlier chunk: its equal keys rank first
+            // count of t < vv: t <= v for an earlier chunk (its equal keys rank
+            // first), t < v for a later one; keys of finite floats are < 2^32 - 1
+            const uint32_t vv = v + (c < w ? 1u : 0u);
             uint32_t pos = 0;
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const uint32_t t = ch[pos + step - 1];
-                pos += (le ? t <= v : t < v) ? (uint32_t)step : 0u;
-            }
-            const uint32_t t = ch[pos];
-            rank += pos + ((le ? t <= v : t < v) ? 1u : 0u);
+            for (int step = 16; step > 0; step >>= 1) pos += ch[pos + step - 1] < vv ? (uint32_t)step : 0u;
+            rank += pos + (ch[pos] < vv ? 1u : 0u);
         }
         sh.sorted[rank] = v;
     }
@@ -999,7 +997,19 @@ __device__ bool s3_select(const float* __restrict__ row, int n, KF kf, uint32_t 
     if (overflow || R < c_lo || R >= c_lo + c_mid) return false;  // block-uniform
     // compact the slots into one contiguous array
     const uint32_t off = (woff + incl - v) & 0xFFFFu;
-    for (uint32_t i = 0; i < c; ++i) cand[off + i] = slots[(size_t)i * NT + tid];
+    {
+        const uint32_t* sp = slots + tid;
+        uint32_t* dp = cand + off;
+        uint32_t i = 0;
+        for (; i + 4 <= c; i += 4) {
+            const uint32_t k0 = sp[i * NT], k1 = sp[(i + 1) * NT], k2 = sp[(i + 2) * NT], k3 = sp[(i + 3) * NT];
+            dp[i] = k0;
+            dp[i + 1] = k1;
+            dp[i + 2] = k2;
+            dp[i + 3] = k3;
+        }
+        for (; i < c; ++i) dp[i] = sp[i * NT];
+    }
     __syncthreads();
     const auto each = [&](auto&& f) { s3_arr_each<NT>(cand, (int)c_mid, f); };
     uint32_t cl;

@@ -1,0 +1,16 @@
+# round-2 full validation: smoke, every GPU test, bench lines for every config,
+# reference arm, launch list + ncu of the headline kernel
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/r2
+O=gpurun_out/r2
+nproc > $O/host.txt; grep -m1 'model name' /proc/cpuinfo >> $O/host.txt
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv >> $O/host.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider -rA --durations=20 > $O/gpu_tests.log 2>&1; echo "tests rc=$?" >> $O/gpu_tests.log
+timeout 900 python bench.py > $O/bench_config4.json 2> $O/bench_config4.err
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_reference_config4.json 2> $O/bench_reference_config4.err
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --contract-path filter > $O/bench_config4_filter.json 2> $O/bench_config4_filter.err
+timeout 600 python bench.py --workload config1 --steps 400 --warmup 20 > $O/bench_config1.json 2> $O/bench_config1.err
+for w in config2 config3 config5 config5p; do timeout 900 python bench.py --workload $w --steps 3 --warmup 3 > $O/bench_$w.json 2> $O/bench_$w.err; done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_config4.csv python bench.py --steps 1 --warmup 1 --batch 256 --no-e2e --no-cpu-baseline > $O/launches_config4.log 2>&1
+echo done
