@@ -65,7 +65,7 @@ constexpr uint32_t W_ACC = 128;
 constexpr int W_SMEM_LIMIT = 227 * 1024;
 
 struct WSmem {
-    int P, D, CNT, ZS, NZ, EXCL, BARS, TADDR, RAW, total, raw_stages;
+    int P, D, CNT, ZS, NZ, EXCL, INV, BARS, TADDR, RAW, total, raw_stages;
     static constexpr int NBARS = 2 * W_P_STAGES + 2 + 2 + 3 + 2 * W_R_MAX;
     __host__ __device__ WSmem() {
         P = 0;
@@ -74,7 +74,8 @@ struct WSmem {
         ZS = CNT + W_MD * 4;                     // float [2][256] (+ [2] max |z|)
         NZ = ZS + 2 * W_MAXD * 4 + 16;           // uint32 [8][W_GROUPS][4] nonzero ballots (tile ring)
         EXCL = NZ + 8 * W_GROUPS * 4 * 4;        // (unused)
-        BARS = EXCL + 8 * 4 * 4;
+        INV = EXCL + 8 * 4 * 4;                  // float [8][128] per-point 1 / (s 2^15) (STORE mode)
+        BARS = INV + 8 * W_NP * 4;
         TADDR = BARS + NBARS * 8;
         RAW = (TADDR + 16 + 1023) & ~1023;       // [64][128] floats per stage
         const int room = W_SMEM_LIMIT - 1024 - RAW;
@@ -89,13 +90,14 @@ struct WUnit {
     int64_t t0, t1;
 };
 
+// units (chunk, query, block) over blocks [jb0, jb0 + jbn) (count mode: all NB)
 __device__ __forceinline__ WUnit w_unit(const TcArgs& a, int64_t u) {
     WUnit r;
-    const int64_t per_c = (int64_t)a.Qb * a.NB;
+    const int64_t per_c = (int64_t)a.Qb * a.jbn;
     const int64_t c = u / per_c;
     const int64_t rem = u - c * per_c;
-    r.q = (int)(rem / a.NB);
-    r.blk = (int)(rem - (int64_t)r.q * a.NB);
+    r.q = (int)(rem / a.jbn);
+    r.blk = a.jb0 + (int)(rem - (int64_t)r.q * a.jbn);
     r.t0 = c * a.tiles_per_chunk;
     r.t1 = r.t0 + a.tiles_per_chunk < a.tiles ? r.t0 + a.tiles_per_chunk : a.tiles;
     return r;
@@ -104,8 +106,8 @@ __device__ __forceinline__ WUnit w_unit(const TcArgs& a, int64_t u) {
 // first unit >= u of this CTA's stride whose query is still live (early exit)
 __device__ __forceinline__ int64_t w_next(const TcArgs& a, int64_t u, int64_t units) {
     if (a.done) {
-        const int64_t per_c = (int64_t)a.Qb * a.NB;
-        while (u < units && a.done[(u % per_c) / a.NB]) u += gridDim.x;
+        const int64_t per_c = (int64_t)a.Qb * a.jbn;
+        while (u < units && a.done[(u % per_c) / a.jbn]) u += gridDim.x;
     }
     return u;
 }
@@ -213,6 +215,7 @@ __device__ __forceinline__ void w_store_slice(unsigned char* P, const float2 (&a
 
 }  // namespace
 
+template <bool STORE>
 __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs a) {
     extern __shared__ __align__(1024) unsigned char w_raw[];
     unsigned char* sm = w_raw + ((1024u - (smem_u32(w_raw) & 1023u)) & 1023u);
@@ -227,6 +230,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
     uint32_t* sCnt = reinterpret_cast<uint32_t*>(sm + lay.CNT);
     float* sZ = reinterpret_cast<float*>(sm + lay.ZS);
     uint32_t* sNz = reinterpret_cast<uint32_t*>(sm + lay.NZ);
+    float* sInv = reinterpret_cast<float*>(sm + lay.INV);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + lay.BARS);
     uint64_t* pfull = &bars[0];
     uint64_t* pempty = &bars[W_P_STAGES];
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
     const int RS = lay.raw_stages;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t units = (int64_t)a.Qb * a.NB * a.chunks;
+    const int64_t units = (int64_t)a.Qb * a.jbn * a.chunks;
 
     for (int i = tid; i < W_P_STAGES * W_STAGE / 16; i += W_THREADS)
         reinterpret_cast<uint4*>(sP)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -404,7 +408,18 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
                     unsigned char* P = sP + st * W_STAGE + r * 16;
                     if (s < L.full) w_store_slice<true>(P, av, scale, h, TC_SLICE, 4, 0);
                     else w_store_slice<false>(P, av, scale, h, d - TC_SLICE * L.full, L.q16, L.rem);
-                    if (s == S - 1) {
+                    if (STORE && s == S - 1 && h == 0) {
+                        // exact power-of-two rescale of this point for the epilogue: y = acc 2^(E - 29)
+                        // (8-deep ring; the converter runs at most S_P + 2 tiles ahead of the epilogue)
+                        float inv = 0.0f;
+                        if (bnd > 0.0f) {
+                            int E = (int)((__float_as_uint(bnd) >> 23) & 0xFF) - 126;
+                            if (E < -100) E = -100;
+                            inv = ldexpf(1.0f, E - 29);
+                        }
+                        sInv[(gtile & 7u) * W_NP + r] = inv;
+                    }
+                    if (!STORE && s == S - 1) {
                         // counted points of the tile: valid rows with some a != 0 (coinciding
                         // rows x = z give y = +-0 and are ties on both sides); one ballot word
                         // per (warp's point group, coordinate group), read by the epilogue
@@ -420,6 +435,54 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
             // max |z| slot of this unit parity is reused two units later
             named_bar(2, W_CONV_THREADS);
             if (ct == 0) zmx[it & 1u] = 0.0f;
+        }
+    } else if (STORE) {
+        // ---------------------------------------------- epilogue: y' rows (STORE)
+        const int quarter = warp & 3;
+        const int half = (warp - W_EPI_WARP0) >> 2;
+        const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
+        const bool vec = (a.n & 3) == 0;
+        uint32_t gacc = 0, gtile = 0;
+        for (int64_t u = w_next(a, blockIdx.x, units); u < units; u = w_next(a, u + gridDim.x, units)) {
+            const WUnit w = w_unit(a, u);
+            const int jl = (w.blk - a.jb0) * W_MD + 32 * quarter + lane;  // row of the chunk
+            const bool live = w.blk * W_MD + 32 * quarter + lane < a.m;
+            float* yrow = a.y + ((size_t)w.q * a.jbn * W_MD + jl) * (size_t)a.n;
+            for (int64_t t = w.t0; t < w.t1; ++t, ++gtile, ++gacc) {
+                const uint32_t buf = dbl ? (gacc & 1u) : 0u;
+                const uint32_t ph = dbl ? ((gacc >> 1) & 1u) : (gacc & 1u);
+                mbar_wait(&tfull[buf], ph);
+                tc_fence_after();
+                const float* inv = sInv + (gtile & 7u) * W_NP + 64 * half;
+                const int64_t p0 = t * W_NP + 64 * half;
+                const uint32_t tb = tmem + lane_base + buf * W_ACC + (uint32_t)(half * 64);
+#pragma unroll
+                for (int part = 0; part < 2; ++part) {
+                    uint32_t y[32];
+                    tmem_ld32(tb + 32 * part, y);
+                    tmem_wait_ld();
+                    if (part == 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[buf]);
+                    }
+                    if (!live) continue;
+                    const int64_t pb = p0 + 32 * part;
+                    if (vec && pb + 32 <= a.n) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            *reinterpret_cast<float4*>(yrow + pb + 4 * k) =
+                                make_float4(__uint_as_float(y[4 * k]) * inv[32 * part + 4 * k],
+                                            __uint_as_float(y[4 * k + 1]) * inv[32 * part + 4 * k + 1],
+                                            __uint_as_float(y[4 * k + 2]) * inv[32 * part + 4 * k + 2],
+                                            __uint_as_float(y[4 * k + 3]) * inv[32 * part + 4 * k + 3]);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 32; ++k)
+                            if (pb + k < a.n) yrow[pb + k] = __uint_as_float(y[k]) * inv[32 * part + k];
+                    }
+                }
+            }
         }
     } else {
         // ------------------------------------------------------------ epilogue
@@ -485,14 +548,19 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(W_TMEM_COLS));
 }
 
-cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st) {
+template <bool STORE>
+static cudaError_t launch_tcw(TcArgs a, int sms, cudaStream_t st) {
     if (a.d <= TC_SLICE || a.d > W_MAXD || a.xmax == nullptr) return cudaErrorInvalidValue;
     const WSmem lay;
     if (lay.raw_stages < 2) return cudaErrorInvalidValue;
     a.gb = 1;
-    a.groups = a.NB;
+    if (!STORE) {
+        a.jb0 = 0;
+        a.jbn = a.NB;
+    }
+    a.groups = a.jbn;
     // chunks: >= 4 units per SM, and chunks short enough that a wave's tiles stay in L2
-    const int64_t base = (int64_t)a.Qb * a.NB;
+    const int64_t base = (int64_t)a.Qb * a.jbn;
     int64_t chunks = (4ll * sms + base - 1) / base;
     const int64_t l2_tiles = (int64_t)(48ll << 20) / ((int64_t)a.d * W_NP * 4);  // ~48 MB of rows per chunk
     const int64_t min_chunks = (a.tiles + l2_tiles - 1) / (l2_tiles > 0 ? l2_tiles : 1);
@@ -503,13 +571,17 @@ cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st) {
     a.chunks = (int)((a.tiles + a.tiles_per_chunk - 1) / a.tiles_per_chunk);
     a.raw_stages = lay.raw_stages;
     const size_t smem = (size_t)lay.total;
-    cudaError_t e = cudaFuncSetAttribute(contract_tcw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(contract_tcw_kernel<STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t units = base * a.chunks;
     if (units == 0) return cudaSuccess;
     const int grid = (int)(units < sms ? units : sms);
-    contract_tcw_kernel<<<grid, W_THREADS, smem, st>>>(a);
+    contract_tcw_kernel<STORE><<<grid, W_THREADS, smem, st>>>(a);
     return cudaGetLastError();
 }
+
+cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st) { return launch_tcw<false>(a, sms, st); }
+cudaError_t launch_contract_tcw_store(TcArgs a, int sms, cudaStream_t st) { return launch_tcw<true>(a, sms, st); }
 
 }  // namespace rrs

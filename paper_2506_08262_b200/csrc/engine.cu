@@ -86,7 +86,7 @@ struct rrs_engine {
     DevBuf xmax;  // [tiles * BM] max_l |x_il| (wide tensor path, 64 < d <= 256)
     // centred frame of the projection notions (center.cu): m, the FP32 blocked
     // copy of x - m, and for n < STORE64_N the FP64 row-major copy of x - m
-    DevBuf center, xcb, xc64;
+    DevBuf center, xcb, xc64, xcmax;  // xcmax: max_l |x_il - m_l| per row (wide tensor store)
     DevBuf x64;  // d > 256: FP64 row-major copy of the data (contract64.cu)
     int64_t n = 0;
     int d = 0;
@@ -170,6 +170,7 @@ struct Plan {
     bool tcs;    // tensor-core projection store (projection notions, d <= 50; contract_tcs.cu)
     bool store64;  // FP64-accumulated store (projection notions, n < STORE64_N, no tensor store; center.cu)
     bool wide;     // d > 256: FP64 contraction (contract64.cu) for counts and the store
+    bool tcws;     // projection store on the wide tensor kernel (contract_tcw.cu STORE, 64 < d <= 256)
     int nb8;     // 128-direction blocks per query (tensor path operand, tc_block_bytes(d) each)
     int jchunk;  // direction blocks per store launch (projection notions)
     int tpu, chunks;
@@ -190,6 +191,8 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     p.tcs = tcs_ok && (e->contract_path >= 2 || (e->contract_path == 0 && e->n >= 4096 && e->d >= 32));
     p.store64 = notion != RRS_HALFSPACE && !p.tcs && e->n < STORE64_N;
     p.wide = e->d > TC_MAX_D;
+    p.tcws = notion != RRS_HALFSPACE && !p.store64 && !p.wide && e->d > TC_SLICE && e->n >= 4096 &&
+             (e->contract_path == 0 || e->contract_path == 2);
     const int64_t d = e->d, n = e->n;
     int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * tcf_dp((int)d) * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 16 +
                     d * 40 + 64 +
@@ -241,7 +244,7 @@ int ensure_ws(rrs_engine* e, const Plan& p, int notion) {
     CK(e->dmin.ensure(Qb * 8));
     CK(e->bestcnt.ensure(Qb * 8));
     CK(e->uop.ensure(p.tcf   ? Qb * (size_t)p.nb8 * tcf_block_bytes(e->d)
-                     : p.tc  ? Qb * (size_t)p.nb8 * tc_block_bytes(e->d)
+                     : (p.tc || p.tcws) ? Qb * (size_t)p.nb8 * tc_block_bytes(e->d)
                      : p.tcs ? Qb * (size_t)p.nb8 * tc6_block_bytes(e->d)
                              : 16));
     if (notion == RRS_HALFSPACE) {
@@ -354,7 +357,25 @@ int univariate_from_store(rrs_engine* e, const Plan& p, int Qb, int notion, cons
         const int jbn = (p.MB - jb0) < p.jchunk ? (p.MB - jb0) : p.jchunk;
         {
             Timer t(e, 1);
-            if (p.wide && !p.store64) {
+            if (p.tcws) {
+                TcArgs t{};
+                t.xb = e->xcb.as<float>();
+                t.zq = e->zq0.as<float>();
+                t.uop = e->uop.as<unsigned char>();
+                t.n = e->n;
+                t.tiles = e->tiles;
+                t.d = e->d;
+                t.Qb = Qb;
+                t.NB = p.nb8;
+                t.m = p.m;
+                t.mpad = p.mpad;
+                t.xmax = e->xcmax.as<float>();
+                t.y = e->y.as<float>();
+                t.jb0 = jb0;
+                t.jbn = jbn;
+                CK(launch_contract_tcw_store(t, e->sms, e->stream));
+                e->stats.tensor_contract_launches++;
+            } else if (p.wide && !p.store64) {
                 Contract64Args c{};
                 c.x64 = e->x64.as<double>();
                 c.c = e->center.as<double>();  // centred frame, the same m for every query
@@ -497,7 +518,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 g.refl_mode = e->reflmode.as<int>();
                 g.refl_v = e->reflv.as<double>();
                 g.u64 = e->u64.as<double>();
-                g.u32 = (p.tc || p.tcs) ? nullptr : e->u32.as<float>();  // the tensor paths read uop only
+                g.u32 = (p.tc || p.tcs || p.tcws) ? nullptr : e->u32.as<float>();  // the tensor paths read uop only
                 g.seed = cfg->seed;
                 g.q0 = q0 + b0;
                 g.refinement = (uint32_t)l;
@@ -506,7 +527,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 g.m = m;
                 g.mpad = p.mpad;
                 g.d = d;
-                g.uop = p.tc ? e->uop.as<unsigned char>() : nullptr;
+                g.uop = (p.tc || p.tcws) ? e->uop.as<unsigned char>() : nullptr;
                 g.uop_mode = p.tcf ? 1 : 0;
                 g.u32r = p.tcf ? e->u32.as<float>() : nullptr;
                 g.NB = p.nb8;
@@ -637,7 +658,7 @@ int rrs_engine_destroy(rrs_engine* e) {
     for (DevBuf* b : {&e->xb, &e->xmax, &e->zq, &e->u64, &e->u32, &e->uop, &e->counts, &e->depths, &e->y, &e->pole,
                       &e->reflv, &e->reflmode, &e->dmin, &e->bestcnt, &e->tmp_in, &e->tmp_out0,
                       &e->tmp_out1, &e->tmp_out2, &e->tmp_out3, &e->center, &e->xcb, &e->xc64, &e->zq0,
-                      &e->shift, &e->fallbacks, &e->x64, &e->done, &e->c0})
+                      &e->shift, &e->fallbacks, &e->x64, &e->done, &e->c0, &e->xcmax})
         b->release();
     for (auto ev : e->ev_pool) cudaEventDestroy(ev);
     if (e->own) cudaStreamDestroy(e->own);
@@ -742,6 +763,10 @@ static int set_dataset_common(rrs_engine* e, const double* xdev, int64_t n, int3
     CK(launch_center_sample(xdev, n, d, e->center.as<double>(), e->stream));
     CK(e->xcb.ensure((size_t)tiles * d * BM * 4));
     CK(launch_block_centered(xdev, e->center.as<double>(), e->xcb.as<float>(), n, d, tiles, e->stream));
+    if (d > TC_SLICE && d <= TC_MAX_D) {
+        CK(e->xcmax.ensure((size_t)tiles * BM * 4));
+        CK(launch_row_absmax(e->xcb.as<float>(), e->xcmax.as<float>(), d, tiles, e->stream));
+    }
     if (n < STORE64_N) {
         CK(e->xc64.ensure((size_t)n * d * 8));
         CK(launch_center_copy64(xdev, e->center.as<double>(), e->xc64.as<double>(), n, d, e->stream));
@@ -864,6 +889,7 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
         CK(launch_pack_directions(e->u64.as<double>(), e->u32.as<float>(), 1, m, p.mpad, d, e->stream));
     if (p.tc && !p.tcf) CK(launch_pack_tc_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (p.tcs) CK(launch_pack_tc6_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
+    if (p.tcws) CK(launch_pack_tc_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (notion == RRS_HALFSPACE) {
         CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.mpad * 2 * 4, e->stream));
         if (int rc = contract_halfspace(e, p, 1, e->tmp_in.as<double>(), nullptr)) return rc;

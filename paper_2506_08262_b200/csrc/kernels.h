@@ -240,6 +240,10 @@ struct TcArgs {
     int groups, chunks, raw_stages, gb;
     int64_t tiles_per_chunk;
     const int* done;            // nullable [Qb]: early exit, units of these queries are skipped
+    // projection store on the wide kernel (contract_tcw.cu STORE mode): direction
+    // blocks [jb0, jb0 + jbn) of each query, rows y[q][(blk - jb0) * 128 + j][n]
+    float* y;
+    int jb0, jbn;
 };
 
 // Filter-and-refine halfspace contraction (contract_tcf.cu, d <= 64): one FP16
@@ -336,7 +340,8 @@ cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st);
 cudaError_t launch_contract_tcf(TcfArgs a, int sms, cudaStream_t st);  // filter and refine, d <= 64
 cudaError_t launch_pack_tcf_operand(const double* u64, unsigned char* uop, float* u32r, int Qb, int m, int NB,
                                     int mpad, int d, cudaStream_t st);
-cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st);  // 64 < d <= 256 (contract_tcw.cu)
+cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st);
+cudaError_t launch_contract_tcw_store(TcArgs a, int sms, cudaStream_t st);  // centred projection store, 64 < d <= 256  // 64 < d <= 256 (contract_tcw.cu)
 cudaError_t launch_contract_tcs(TcsArgs a, int sms, cudaStream_t st);  // projection store, d <= 64
 cudaError_t launch_pack_tc6_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,
                                     cudaStream_t st);

@@ -22,6 +22,7 @@ cases = [
     (1000, 5, "halfspace", "ffma", "auto"),        # contract_kernel<count>
     (1000, 300, "halfspace", "auto", "auto"),      # d > 256: contract64 count
     (5000, 300, "projection", "auto", "auto"),     # d > 256: contract64 store
+    (5000, 80, "asym_projection", "auto", "auto"),  # contract_tcw STORE (centred, 64 < d <= 256)
     (5000, 40, "projection", "tensor", "auto"),    # contract_tcs + select v3<256>
     (20000, 20, "asym_projection", "ffma", "auto"),  # contract_kernel<store> + select v3<512>
     (20000, 20, "projection", "ffma", "wide"),     # select v3<1024>
