@@ -26,7 +26,7 @@ constexpr int CENTER_S = 1024;
 
 // m_c = lower median of column c over min(n, 1024) rows at strided positions
 __global__ void __launch_bounds__(512) center_sample_kernel(const double* __restrict__ x, int64_t n, int d,
-                                                            double* __restrict__ center) {
+                                                            double* __restrict__ center, double* __restrict__ iqr) {
     __shared__ double s[CENTER_S];
     const int c = blockIdx.x;
     const int S = n >= CENTER_S ? CENTER_S : (int)n;
@@ -48,7 +48,10 @@ __global__ void __launch_bounds__(512) center_sample_kernel(const double* __rest
             __syncthreads();
         }
     }
-    if (threadIdx.x == 0) center[c] = s[(S - 1) / 2];
+    if (threadIdx.x == 0) {
+        center[c] = s[(S - 1) / 2];
+        if (iqr) iqr[c] = s[(3 * S) / 4 < S ? (3 * S) / 4 : S - 1] - s[S / 4];
+    }
 }
 
 // xb[t][c][i] = (float)(x[t·BM + i][c] - m_c), zero padding rows; a 32 x 32
@@ -145,8 +148,8 @@ cudaError_t launch_coincide_count32(const float* xb, const float* zq, int64_t n,
     return cudaGetLastError();
 }
 
-cudaError_t launch_center_sample(const double* x, int64_t n, int d, double* center, cudaStream_t st) {
-    center_sample_kernel<<<d, 512, 0, st>>>(x, n, d, center);
+cudaError_t launch_center_sample(const double* x, int64_t n, int d, double* center, double* iqr, cudaStream_t st) {
+    center_sample_kernel<<<d, 512, 0, st>>>(x, n, d, center, iqr);
     return cudaGetLastError();
 }
 

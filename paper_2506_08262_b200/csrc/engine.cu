@@ -87,6 +87,7 @@ struct rrs_engine {
     // centred frame of the projection notions (center.cu): m, the FP32 blocked
     // copy of x - m, and for n < STORE64_N the FP64 row-major copy of x - m
     DevBuf center, xcb, xc64, xcmax;  // xcmax: max_l |x_il - m_l| per row (wide tensor store)
+    double col_ratio = 1.0;           // max / min column IQR (> 0) of the centre sample (store gating)
     DevBuf x64;  // d > 256: FP64 row-major copy of the data (contract64.cu)
     int64_t n = 0;
     int d = 0;
@@ -185,14 +186,23 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     const bool tc_ok = notion == RRS_HALFSPACE && e->d <= 256;
     p.tc = tc_ok && (e->contract_path >= 2 || (e->contract_path == 0 && e->n >= 4096));
     p.tcf = p.tc && e->d <= TC_SLICE && e->contract_path == 4;
-    const bool tcs_ok = notion != RRS_HALFSPACE && tc6_layout(e->d).ns <= 19;
-    // auto: the store is HBM-write bound at small d (y is n*m*4 bytes per query and
-    // refinement whatever computes it), the tensor store pays from d ~ 32 (config 3)
-    p.tcs = tcs_ok && (e->contract_path >= 2 || (e->contract_path == 0 && e->n >= 4096 && e->d >= 32));
-    p.store64 = notion != RRS_HALFSPACE && !p.tcs && e->n < STORE64_N;
+    // projection store (centred frame): the 2-term FP16 split on the tensor cores for
+    // n >= 4096 -- contract_tc.cu STORE for d <= 64 (up to 8 direction blocks share a
+    // converted point tile), contract_tcw.cu STORE above; the three-way split
+    // (contract_tcs.cu) only when forced (path 5); FP64 below n = 4096
+    // the FP16-split stores scale each point by a power of two from its largest
+    // coordinate, so a column whose spread is tiny next to another's is resolved
+    // only to 2^-22 (2-term) / 2^-33 (3-term) of the large one; auto takes them
+    // for scale-homogeneous data only (column IQR ratio, measured at set_dataset)
+    const bool proj = notion != RRS_HALFSPACE;
+    const bool forced = e->contract_path == 2;
+    const bool autop = e->contract_path == 0;
+    p.tcs = proj && tc6_layout(e->d).ns <= 19 &&
+            (forced || (autop && e->n >= 4096 && e->d >= 32 && e->col_ratio <= 4096.0));
+    p.store64 = proj && !p.tcs && e->n < STORE64_N;
     p.wide = e->d > TC_MAX_D;
-    p.tcws = notion != RRS_HALFSPACE && !p.store64 && !p.wide && e->d > TC_SLICE && e->n >= 4096 &&
-             (e->contract_path == 0 || e->contract_path == 2);
+    p.tcws = proj && !p.store64 && !p.wide && e->d > TC_SLICE &&
+             (forced || (autop && e->n >= 4096 && e->col_ratio <= 8.0));
     const int64_t d = e->d, n = e->n;
     int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * tcf_dp((int)d) * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 16 +
                     d * 40 + 64 +
@@ -518,7 +528,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 g.refl_mode = e->reflmode.as<int>();
                 g.refl_v = e->reflv.as<double>();
                 g.u64 = e->u64.as<double>();
-                g.u32 = (p.tc || p.tcs || p.tcws) ? nullptr : e->u32.as<float>();  // the tensor paths read uop only
+                g.u32 = (p.tc || p.tcs || p.tcws) ? nullptr : e->u32.as<float>();  // tensor paths: uop only
                 g.seed = cfg->seed;
                 g.q0 = q0 + b0;
                 g.refinement = (uint32_t)l;
@@ -760,7 +770,20 @@ static int set_dataset_common(rrs_engine* e, const double* xdev, int64_t n, int3
     CK(e->xb.ensure((size_t)tiles * d * BM * 4));
     CK(launch_block_dataset(xdev, e->xb.as<float>(), n, d, tiles, e->stream));
     CK(e->center.ensure((size_t)d * 8));
-    CK(launch_center_sample(xdev, n, d, e->center.as<double>(), e->stream));
+    CK(e->tmp_out1.ensure((size_t)d * 8));
+    CK(launch_center_sample(xdev, n, d, e->center.as<double>(), e->tmp_out1.as<double>(), e->stream));
+    {
+        std::vector<double> iqr((size_t)d);
+        CK(cudaMemcpyAsync(iqr.data(), e->tmp_out1.p, (size_t)d * 8, cudaMemcpyDeviceToHost, e->stream));
+        CK(cudaStreamSynchronize(e->stream));
+        double lo = 0.0, hi = 0.0;
+        for (double v : iqr)
+            if (v > 0.0) {
+                lo = (lo == 0.0 || v < lo) ? v : lo;
+                hi = v > hi ? v : hi;
+            }
+        e->col_ratio = lo > 0.0 ? hi / lo : 1.0;
+    }
     CK(e->xcb.ensure((size_t)tiles * d * BM * 4));
     CK(launch_block_centered(xdev, e->center.as<double>(), e->xcb.as<float>(), n, d, tiles, e->stream));
     if (d > TC_SLICE && d <= TC_MAX_D) {
@@ -889,7 +912,8 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
         CK(launch_pack_directions(e->u64.as<double>(), e->u32.as<float>(), 1, m, p.mpad, d, e->stream));
     if (p.tc && !p.tcf) CK(launch_pack_tc_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (p.tcs) CK(launch_pack_tc6_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
-    if (p.tcws) CK(launch_pack_tc_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
+    if (p.tcws)
+        CK(launch_pack_tc_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (notion == RRS_HALFSPACE) {
         CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.mpad * 2 * 4, e->stream));
         if (int rc = contract_halfspace(e, p, 1, e->tmp_in.as<double>(), nullptr)) return rc;

@@ -327,7 +327,9 @@ cudaError_t launch_coincide_count64(const double* x64, const double* z, int64_t 
                                     cudaStream_t st);
 // centred frame of the projection notions (center.cu)
 constexpr int64_t STORE64_N = 4096;  // below: FP64-accumulated store from an FP64 centred copy
-cudaError_t launch_center_sample(const double* x, int64_t n, int d, double* center, cudaStream_t st);
+// centre m_c (lower median of a strided 1024-row sample) and the column's
+// interquartile range on that sample (iqr may be null)
+cudaError_t launch_center_sample(const double* x, int64_t n, int d, double* center, double* iqr, cudaStream_t st);
 cudaError_t launch_block_centered(const double* x, const double* center, float* xb, int64_t n, int d, int64_t tiles,
                                   cudaStream_t st);
 cudaError_t launch_center_copy64(const double* x, const double* center, double* xc, int64_t n, int d,

@@ -439,7 +439,8 @@ def test_dataset_validation_on_device(b200):
 
 @pytest.mark.parametrize("notion", ["projection", "asym_projection"])
 @pytest.mark.parametrize("shape", [(10_000, 20, "gaussian"), (50_000, 50, "cauchy"), (53_248, 7, "cauchy"),
-                                   (4_097, 33, "gaussian"), (60_001, 48, "cauchy")])
+                                   (4_097, 33, "gaussian"), (60_001, 48, "cauchy"), (30_000, 90, "cauchy"),
+                                   (20_000, 256, "gaussian")])
 def test_tensor_store_projection_depths(b200, notion, shape):
     """The tensor-core projection store (contract_tcs.cu, three-way FP16
     split, six products): per-direction D_P / D_AP against the FP64 oracle to
@@ -593,3 +594,24 @@ def test_early_exit_bitwise(b200, case):
         assert np.array_equal(a, b)
     assert full[3][0] >= 2 and full[3][1] >= 2  # the duplicated pair: bound 2
     print(f"\n{case}: final counts {np.bincount(full[3])[:4]}, launches {launches}")
+
+
+@pytest.mark.parametrize("d", [40, 80])
+def test_heterogeneous_columns_projection(b200, d):
+    """Columns on scales 1e-3 .. 1e3 and axis-aligned directions: the FP16-split
+    tensor stores resolve a point only relative to its largest coordinate, so
+    auto must take the FFMA store here (column IQR ratio gate) and every
+    per-direction depth must stay within DEPTH_RTOL of the FP64 oracle."""
+    from oracle import oracle
+    from paper_2506_08262_b200.synthetic import toeplitz_gaussian
+
+    n = 6000
+    X = toeplitz_gaussian(d, n, seed=8) * np.logspace(-3, 3, d)[None, :]
+    rng = np.random.default_rng(d)
+    U = np.vstack([np.eye(d)[:4], -np.eye(d)[d - 2:], rng.standard_normal((12, d))])
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    data = b200.Dataset(X)
+    for notion in ("projection", "asym_projection"):
+        for z in (X[4], np.median(X, axis=0)):
+            got = b200.evaluate_directions(z, data, U, notion, b200.ParallelConfig())
+            np.testing.assert_allclose(got, oracle.evaluate_directions(z, X, U, notion), rtol=DEPTH_RTOL, atol=0)
