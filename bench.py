@@ -245,7 +245,7 @@ def main():
     ap.add_argument("--early-exit", action="store_true",
                     help="RrsConfig(early_exit=True): exact early exit of finished halfspace queries "
                          "(outputs bitwise unchanged; not the default, which does the reference's full work)")
-    ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "filter"],
+    ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "filter", "tensor3"],
                     help="halfspace contraction kernel (auto: the library's choice)")
     args = ap.parse_args()
     wl = args.workload

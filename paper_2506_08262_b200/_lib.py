@@ -227,7 +227,7 @@ class Engine:
         kernel; tensor = the two-term FP16 split (contract_tc.cu, d <= 64) / wide
         split (d > 64), tensor2 = its 2-SM cta_group::2 variant, filter = filter
         and refine, contract_tcf.cu, d <= 64)."""
-        code = {"auto": 0, "ffma": 1, "tensor": 2, "filter": 4}[path]
+        code = {"auto": 0, "ffma": 1, "tensor": 2, "filter": 4, "tensor3": 5}[path]
         _raise(load_library().rrs_engine_set_contract_path(self._h, code))
 
     def set_select_path(self, path: str):

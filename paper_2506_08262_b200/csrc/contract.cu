@@ -57,7 +57,11 @@ __global__ void __launch_bounds__(CT_THREADS, 2) contract_kernel(const ContractA
     uint64_t* bars = reinterpret_cast<uint64_t*>(zs + MAX_D);
 
     const int tid = threadIdx.x;
-    const int tx = tid & 15, ty = tid >> 4;
+    // tx: direction quads, ty: point quads.  Count mode: a warp holds 16 tx x 2 ty
+    // (the column sums fold lanes l and l ^ 16).  Store mode: 2 tx x 16 ty, so one
+    // float4 store instruction writes 2 rows x 256 contiguous bytes of y instead
+    // of 16 rows x 32 bytes (the store is bound by the y write traffic)
+    const int tx = STORE ? (tid >> 4) : (tid & 15), ty = STORE ? (tid & 15) : (tid >> 4);
 
     // ---- unit decode
     const int per_q = a.jbn * a.chunks;

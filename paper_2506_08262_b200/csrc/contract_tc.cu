@@ -79,10 +79,10 @@ constexpr int TC_SMEM_LIMIT = 227 * 1024;
 
 // Shared-memory layout (bytes from a 1024-aligned base), runtime in ns and d.
 struct TcSmem {
-    int P, D, CNT, ZS, SMX, EXCL, ZROWS, BARS, TADDR, RAW, total;
-    int stage_bytes, raw_stages;
+    int P, D, CNT, ZS, SMX, EXCL, ZROWS, INV, STG, BARS, TADDR, RAW, total;
+    int stage_bytes, raw_stages, raw_rows;
     static constexpr int NBARS = 2 * P_STAGES + 2 + 2 + 3 + 2 * R_MAX_STAGES;
-    __host__ __device__ TcSmem(int ns, int d) {
+    __host__ __device__ TcSmem(int ns, int d, bool store) {
         stage_bytes = ns * 4096;                   // one packed tile / direction block
         P = 0;                                     // P_STAGES point operands
         D = P + P_STAGES * stage_bytes;            // direction staging (one block)
@@ -91,14 +91,16 @@ struct TcSmem {
         SMX = ZS + 2 * TC_MAXD * 4;                // float [2][2][128] partial |a| maxima
         EXCL = SMX + 2 * 2 * TC_NP * 4;            // uint32 [8][4] excluded-point masks per tile
         ZROWS = EXCL + 8 * 4 * 4;                  // uint32 [4] coinciding rows per unit slot
-        BARS = ZROWS + 16;                         // mbarriers
+        INV = ZROWS + 16;                          // float [8][128] per-point 1 / (s 2^15) (STORE mode)
+        STG = INV + (store ? 8 * TC_NP * 4 : 0);   // float [8 warps][32][33] store transpose tiles (STORE)
+        BARS = STG + (store ? TC_EPI_WARPS * 32 * 33 * 4 : 0);  // mbarriers
         TADDR = BARS + NBARS * 8;
         RAW = (TADDR + 16 + 1023) & ~1023;         // raw FP32 tiles: 64 rows of 128 (rows >= d stay 0)
         const int room = TC_SMEM_LIMIT - 1024 - RAW;
-        raw_stages = room / (TC_MAXD * TC_NP * 4);
+        raw_rows = (d + 7) & ~7;                   // rows past d stay zero (whole 8-coordinate chunks)
+        raw_stages = room / (raw_rows * TC_NP * 4);
         if (raw_stages > R_MAX_STAGES) raw_stages = R_MAX_STAGES;
-        total = RAW + raw_stages * TC_MAXD * TC_NP * 4 + 1024;
-        (void)d;
+        total = RAW + raw_stages * raw_rows * TC_NP * 4 + 1024;
     }
 };
 
@@ -110,6 +112,8 @@ struct TcUnit {
 // first unit >= u of this CTA's stride whose query is still live (early exit:
 // done[] is written by the previous update kernel and read-only here, so every
 // warp role walks the same unit sequence)
+// units over the direction blocks [jb0, jb0 + jbn) of each query (count mode:
+// all NB); grp counts gb-block groups from jb0
 __device__ __forceinline__ int64_t tc_next(const TcArgs& a, int64_t u, int64_t units) {
     if (a.done) {
         const int64_t per_q = (int64_t)a.groups * a.chunks;
@@ -125,7 +129,7 @@ __device__ __forceinline__ TcUnit tc_unit(const TcArgs& a, int64_t u) {
     const int64_t rem = u - (int64_t)r.q * per_q;
     r.grp = (int)(rem / a.chunks);
     const int64_t c = rem - (int64_t)r.grp * a.chunks;
-    r.nbg = a.NB - r.grp * a.gb < a.gb ? a.NB - r.grp * a.gb : a.gb;
+    r.nbg = a.jbn - r.grp * a.gb < a.gb ? a.jbn - r.grp * a.gb : a.gb;
     r.t0 = c * a.tiles_per_chunk;
     r.t1 = r.t0 + a.tiles_per_chunk < a.tiles ? r.t0 + a.tiles_per_chunk : a.tiles;
     return r;
@@ -167,13 +171,14 @@ __device__ __forceinline__ void mma_issue(const TcArgs& a, int64_t units, unsign
     }
 }
 
+template <bool STORE>
 __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs a) {
     extern __shared__ __align__(1024) unsigned char tc_raw[];
     // 1024-align by pointer arithmetic on the __shared__ array (keeps the address space)
     unsigned char* sm = tc_raw + ((1024u - (smem_u32(tc_raw) & 1023u)) & 1023u);
     const int d = a.d;
     const TcLayout L = tc_layout(d);
-    const TcSmem lay(L.ns, d);
+    const TcSmem lay(L.ns, d, STORE);
     const int stage_bytes = lay.stage_bytes;
     unsigned char* sP = sm + lay.P;
     unsigned char* sD = sm + lay.D;
@@ -181,6 +186,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     float* sZ = reinterpret_cast<float*>(sm + lay.ZS);
     float* sMx = reinterpret_cast<float*>(sm + lay.SMX);
     uint32_t* sExcl = reinterpret_cast<uint32_t*>(sm + lay.EXCL);
+    float* sInv = reinterpret_cast<float*>(sm + lay.INV);
+    float* sStg = reinterpret_cast<float*>(sm + lay.STG);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + lay.BARS);
     uint64_t* pfull = &bars[0];                   // [P_STAGES] point tile converted (converter warps)
     uint64_t* pempty = &bars[P_STAGES];           // [P_STAGES] MMAs reading it completed
@@ -203,7 +210,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
     // are never written again, so they stay 0 (A is 0 there too)
     for (int i = tid; i < P_STAGES * stage_bytes / 16; i += TC_THREADS)
         reinterpret_cast<uint4*>(sP)[i] = make_uint4(0u, 0u, 0u, 0u);
-    for (int i = tid; i < RS * TC_MAXD * TC_NP; i += TC_THREADS) sRaw[i] = 0.0f;  // rows >= d stay 0
+    const int RR = lay.raw_rows;
+    for (int i = tid; i < RS * RR * TC_NP; i += TC_THREADS) sRaw[i] = 0.0f;  // rows >= d stay 0
     for (int c = tid; c < TC_GB_MAX * TC_MD; c += TC_THREADS) sCnt[c] = 0u;
     if (tid == 0) {
         for (int s = 0; s < P_STAGES; ++s) {
@@ -243,7 +251,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
         uint32_t gph = 0;
         for (int64_t u = tc_next(a, blockIdx.x, units); u < units; u = tc_next(a, u + gridDim.x, units)) {
             const TcUnit w = tc_unit(a, u);
-            const unsigned char* src = a.uop + ((size_t)w.q * a.NB + (size_t)w.grp * a.gb) * stage_bytes;
+            const unsigned char* src = a.uop + ((size_t)w.q * a.NB + (size_t)(a.jb0 + w.grp * a.gb)) * stage_bytes;
             for (int b = 0; b < w.nbg; ++b, ++gph) {
                 if (gph > 0) mbar_wait_sleep(dempty, (gph - 1) & 1u);
                 expect_tx_elect(dfull, (uint32_t)stage_bytes);
@@ -275,7 +283,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
             for (int64_t t = w.t0; t < w.t1; ++t, ++g) {
                 if (g >= (uint32_t)RS) mbar_wait_sleep(&rempty[rs], rph ^ 1u);
                 expect_tx_elect(&rfull[rs], raw_bytes);
-                tma_load_elect(sRaw + (size_t)rs * TC_MAXD * TC_NP, a.xb + (size_t)t * d * TC_NP, raw_bytes, &rfull[rs]);
+                tma_load_elect(sRaw + (size_t)rs * RR * TC_NP, a.xb + (size_t)t * d * TC_NP, raw_bytes, &rfull[rs]);
                 __syncwarp();
                 if (++rs == (uint32_t)RS) {
                     rs = 0;
@@ -301,7 +309,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                 mbar_wait(&rfull[rs], rph);
                 // staged tile [64][128] (rows >= d are 0, zs too): lane-consecutive points,
                 // conflict-free, immediate offsets; chunks past d are skipped (warp-uniform)
-                const float* X = sRaw + (size_t)rs * TC_MAXD * TC_NP + 32 * h * TC_NP + r;
+                const float* X = sRaw + (size_t)rs * RR * TC_NP + 32 * h * TC_NP + r;
                 const float* zh = zs + 32 * h;
                 float2 av[16];  // coordinate pairs, packed FP32x2 arithmetic (FADD2 / FMUL2)
                 float mx = 0.0f;
@@ -346,6 +354,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                     int E = (int)((__float_as_uint(mx) >> 23) & 0xFF) - 126;  // mx < 2^E
                     if (E < -100) E = -100;
                     scale = __uint_as_float((uint32_t)(127 + 14 - E) << 23);  // 2^(14-E)
+                    // STORE: exact rescale y = acc 2^(E - 29) for the epilogue (8-deep ring;
+                    // the converter runs at most P_STAGES + 2 tiles ahead of it)
+                    if (STORE && h == 0) sInv[(gtile & 7u) * TC_NP + r] = ldexpf(1.0f, E - 29);
+                } else if (STORE && h == 0) {
+                    sInv[(gtile & 7u) * TC_NP + r] = 0.0f;
                 }
                 if (gtile >= P_STAGES) mbar_wait(&pempty[s], ((gtile / P_STAGES) - 1) & 1u);
                 // packed K layout (kernels.h tc_layout), canonical K-major:
@@ -396,6 +409,67 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                 fence_proxy_async();  // generic-proxy smem writes -> tensor-core reads
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&pfull[s]);
+            }
+        }
+    } else if (STORE) {
+        // ---------------------------------------------- epilogue: y' rows (STORE)
+        const int quarter = warp & 3;
+        const int half = (warp - TC_EPI_WARP0) >> 2;
+        const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
+        const bool vec = (a.n & 3) == 0;
+        float* stg = sStg + (warp - TC_EPI_WARP0) * 32 * 33;
+        uint32_t gacc = 0, gtile = 0;
+        for (int64_t u = tc_next(a, blockIdx.x, units); u < units; u = tc_next(a, u + gridDim.x, units)) {
+            const TcUnit w = tc_unit(a, u);
+            for (int64_t t = w.t0; t < w.t1; ++t, ++gtile) {
+                const float* inv = sInv + (gtile & 7u) * TC_NP + 64 * half;
+                const int64_t p0 = t * TC_NP + 64 * half;
+                for (int b = 0; b < w.nbg; ++b) {
+                    const uint32_t buf = gacc & 1u;
+                    mbar_wait(&tfull[buf], (gacc >> 1) & 1u);
+                    ++gacc;
+                    tc_fence_after();
+                    const uint32_t tb = tmem + lane_base + buf * ACC_COLS + (uint32_t)(half * 64);
+                    uint32_t y0[32], y1[32];
+                    tmem_ld32(tb, y0);
+                    tmem_ld32(tb + 32, y1);
+                    tmem_wait_ld();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[buf]);
+                    const int blk = a.jb0 + w.grp * a.gb + b;  // absolute direction block
+                    const int row0 = blk * TC_MD + 32 * quarter;  // the warp's first direction
+                    const int rows_live = min(32, a.m - row0);
+                    float* ybase = a.y + ((size_t)w.q * a.jbn * TC_MD + (size_t)(blk - a.jb0) * TC_MD + 32 * quarter) *
+                                             (size_t)a.n;
+#pragma unroll
+                    for (int part = 0; part < 2; ++part) {
+                        const uint32_t* yv = part ? y1 : y0;
+                        const int64_t pb = p0 + 32 * part;
+                        if (vec && pb + 32 <= a.n) {
+                            // transpose through the warp's tile: each store writes 4 rows x 128 B
+#pragma unroll
+                            for (int k = 0; k < 32; ++k) stg[lane * 33 + k] = __uint_as_float(yv[k]) * inv[32 * part + k];
+                            __syncwarp();
+                            const int c4 = 4 * (lane & 7);
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                const int rr = (lane >> 3) + 4 * k;
+                                if (rr < rows_live) {
+                                    const float* sv = stg + rr * 33 + c4;
+                                    *reinterpret_cast<float4*>(ybase + (size_t)rr * a.n + pb + c4) =
+                                        make_float4(sv[0], sv[1], sv[2], sv[3]);
+                                }
+                            }
+                            __syncwarp();
+                        } else if (lane < rows_live) {
+                            float* yrow = ybase + (size_t)lane * a.n;
+#pragma unroll
+                            for (int k = 0; k < 32; ++k)
+                                if (pb + k < a.n) yrow[pb + k] = __uint_as_float(yv[k]) * inv[32 * part + k];
+                        }
+                    }
+                }
             }
         }
     } else {
@@ -486,7 +560,7 @@ void plan_contract_tc(TcArgs& a, int sms) {
     int gb = (int)(256 / (8 * L.ns));  // direction blocks that fit the 256 A columns of TMEM
     if (gb > TC_GB_MAX) gb = TC_GB_MAX;
     a.gb = gb;
-    a.groups = (a.NB + gb - 1) / gb;
+    a.groups = (a.jbn + gb - 1) / gb;
     // split the point tiles into chunks so that every SM gets >= RRS_TC_UNITS_PER_SM units
     const int64_t base = (int64_t)a.Qb * a.groups;
     int64_t chunks = ((int64_t)RRS_TC_UNITS_PER_SM * sms + base - 1) / base;
@@ -496,21 +570,33 @@ void plan_contract_tc(TcArgs& a, int sms) {
     a.chunks = (int)((a.tiles + a.tiles_per_chunk - 1) / a.tiles_per_chunk);
 }
 
-cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st) {
+template <bool STORE>
+static cudaError_t launch_tc(TcArgs a, int sms, cudaStream_t st) {
     if (a.d > TC_MAXD || a.d < 1 || tc_layout(a.d).ns > TC_MAXNS) return cudaErrorInvalidValue;
+    if (!STORE) {
+        a.jb0 = 0;
+        a.jbn = a.NB;
+    }
     plan_contract_tc(a, sms);
-    const TcSmem lay(tc_layout(a.d).ns, a.d);
+    const TcSmem lay(tc_layout(a.d).ns, a.d, STORE);
     a.raw_stages = lay.raw_stages;
     if (a.raw_stages < 2) return cudaErrorInvalidValue;
     const size_t smem = (size_t)lay.total;
     cudaError_t e =
-        cudaFuncSetAttribute(contract_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(contract_tc_kernel<STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t units = (int64_t)a.Qb * a.groups * a.chunks;
     if (units == 0) return cudaSuccess;
     const int grid = (int)(units < sms ? units : sms);
-    contract_tc_kernel<<<grid, TC_THREADS, smem, st>>>(a);
+    contract_tc_kernel<STORE><<<grid, TC_THREADS, smem, st>>>(a);
     return cudaGetLastError();
 }
+
+bool contract_tc_store_fits(int d) {
+    return d >= 1 && d <= TC_MAXD && TcSmem(tc_layout(d).ns, d, true).raw_stages >= 2;
+}
+
+cudaError_t launch_contract_tc(TcArgs a, int sms, cudaStream_t st) { return launch_tc<false>(a, sms, st); }
+cudaError_t launch_contract_tc_store(TcArgs a, int sms, cudaStream_t st) { return launch_tc<true>(a, sms, st); }
 
 }  // namespace rrs

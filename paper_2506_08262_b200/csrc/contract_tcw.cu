@@ -65,9 +65,9 @@ constexpr uint32_t W_ACC = 128;
 constexpr int W_SMEM_LIMIT = 227 * 1024;
 
 struct WSmem {
-    int P, D, CNT, ZS, NZ, EXCL, INV, BARS, TADDR, RAW, total, raw_stages;
+    int P, D, CNT, ZS, NZ, EXCL, INV, STG, BARS, TADDR, RAW, total, raw_stages;
     static constexpr int NBARS = 2 * W_P_STAGES + 2 + 2 + 3 + 2 * W_R_MAX;
-    __host__ __device__ WSmem() {
+    __host__ __device__ explicit WSmem(bool store) {
         P = 0;
         D = P + W_P_STAGES * W_STAGE;
         CNT = D + W_DSTEPS * 4096;               // uint32 [128]
@@ -75,7 +75,8 @@ struct WSmem {
         NZ = ZS + 2 * W_MAXD * 4 + 16;           // uint32 [8][W_GROUPS][4] nonzero ballots (tile ring)
         EXCL = NZ + 8 * W_GROUPS * 4 * 4;        // (unused)
         INV = EXCL + 8 * 4 * 4;                  // float [8][128] per-point 1 / (s 2^15) (STORE mode)
-        BARS = INV + 8 * W_NP * 4;
+        STG = INV + 8 * W_NP * 4;                // float [8 warps][32][33] store transpose tiles (STORE mode)
+        BARS = STG + (store ? W_EPI_WARPS * 32 * 33 * 4 : 0);
         TADDR = BARS + NBARS * 8;
         RAW = (TADDR + 16 + 1023) & ~1023;       // [64][128] floats per stage
         const int room = W_SMEM_LIMIT - 1024 - RAW;
@@ -224,13 +225,14 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
     const int S = L.full + 1;                 // slices
     const bool dbl = 8 * L.ns <= 256;         // two accumulator buffers fit beside A
     const uint32_t a_base = dbl ? 2 * W_ACC : W_ACC;
-    const WSmem lay;
+    const WSmem lay(STORE);
     unsigned char* sP = sm + lay.P;
     unsigned char* sD = sm + lay.D;
     uint32_t* sCnt = reinterpret_cast<uint32_t*>(sm + lay.CNT);
     float* sZ = reinterpret_cast<float*>(sm + lay.ZS);
     uint32_t* sNz = reinterpret_cast<uint32_t*>(sm + lay.NZ);
     float* sInv = reinterpret_cast<float*>(sm + lay.INV);
+    float* sStg = reinterpret_cast<float*>(sm + lay.STG);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + lay.BARS);
     uint64_t* pfull = &bars[0];
     uint64_t* pempty = &bars[W_P_STAGES];
@@ -442,12 +444,16 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
         const int half = (warp - W_EPI_WARP0) >> 2;
         const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
         const bool vec = (a.n & 3) == 0;
+        float* stg = sStg + (warp - W_EPI_WARP0) * 32 * 33;
         uint32_t gacc = 0, gtile = 0;
         for (int64_t u = w_next(a, blockIdx.x, units); u < units; u = w_next(a, u + gridDim.x, units)) {
             const WUnit w = w_unit(a, u);
             const int jl = (w.blk - a.jb0) * W_MD + 32 * quarter + lane;  // row of the chunk
             const bool live = w.blk * W_MD + 32 * quarter + lane < a.m;
             float* yrow = a.y + ((size_t)w.q * a.jbn * W_MD + jl) * (size_t)a.n;
+            // the warp's 32 rows: consecutive, the first at y0; rows_live of them < m
+            float* y0 = a.y + ((size_t)w.q * a.jbn * W_MD + (size_t)(w.blk - a.jb0) * W_MD + 32 * quarter) * (size_t)a.n;
+            const int rows_live = min(32, a.m - (w.blk * W_MD + 32 * quarter));
             for (int64_t t = w.t0; t < w.t1; ++t, ++gtile, ++gacc) {
                 const uint32_t buf = dbl ? (gacc & 1u) : 0u;
                 const uint32_t ph = dbl ? ((gacc >> 1) & 1u) : (gacc & 1u);
@@ -466,17 +472,24 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&tempty[buf]);
                     }
-                    if (!live) continue;
                     const int64_t pb = p0 + 32 * part;
                     if (vec && pb + 32 <= a.n) {
+                        // transpose through the warp's tile: each store writes 4 rows x 128 B
 #pragma unroll
-                        for (int k = 0; k < 8; ++k)
-                            *reinterpret_cast<float4*>(yrow + pb + 4 * k) =
-                                make_float4(__uint_as_float(y[4 * k]) * inv[32 * part + 4 * k],
-                                            __uint_as_float(y[4 * k + 1]) * inv[32 * part + 4 * k + 1],
-                                            __uint_as_float(y[4 * k + 2]) * inv[32 * part + 4 * k + 2],
-                                            __uint_as_float(y[4 * k + 3]) * inv[32 * part + 4 * k + 3]);
-                    } else {
+                        for (int k = 0; k < 32; ++k) stg[lane * 33 + k] = __uint_as_float(y[k]) * inv[32 * part + k];
+                        __syncwarp();
+                        const int c4 = 4 * (lane & 7);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int rr = (lane >> 3) + 4 * k;
+                            if (rr < rows_live) {
+                                const float* sv = stg + rr * 33 + c4;
+                                *reinterpret_cast<float4*>(y0 + (size_t)rr * a.n + pb + c4) =
+                                    make_float4(sv[0], sv[1], sv[2], sv[3]);
+                            }
+                        }
+                        __syncwarp();
+                    } else if (live) {
 #pragma unroll
                         for (int k = 0; k < 32; ++k)
                             if (pb + k < a.n) yrow[pb + k] = __uint_as_float(y[k]) * inv[32 * part + k];
@@ -551,7 +564,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
 template <bool STORE>
 static cudaError_t launch_tcw(TcArgs a, int sms, cudaStream_t st) {
     if (a.d <= TC_SLICE || a.d > W_MAXD || a.xmax == nullptr) return cudaErrorInvalidValue;
-    const WSmem lay;
+    const WSmem lay(STORE);
     if (lay.raw_stages < 2) return cudaErrorInvalidValue;
     a.gb = 1;
     if (!STORE) {

@@ -172,6 +172,7 @@ struct Plan {
     bool store64;  // FP64-accumulated store (projection notions, n < STORE64_N, no tensor store; center.cu)
     bool wide;     // d > 256: FP64 contraction (contract64.cu) for counts and the store
     bool tcws;     // projection store on the wide tensor kernel (contract_tcw.cu STORE, 64 < d <= 256)
+    bool tcst;     // projection store on the d <= 64 tensor kernel (contract_tc.cu STORE)
     int nb8;     // 128-direction blocks per query (tensor path operand, tc_block_bytes(d) each)
     int jchunk;  // direction blocks per store launch (projection notions)
     int tpu, chunks;
@@ -194,15 +195,22 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     // coordinate, so a column whose spread is tiny next to another's is resolved
     // only to 2^-22 (2-term) / 2^-33 (3-term) of the large one; auto takes them
     // for scale-homogeneous data only (column IQR ratio, measured at set_dataset)
+    // 2-term split stores (contract_tc / contract_tcw STORE) for n >= 4096; the
+    // 3-term split (contract_tcs) for 32 <= d <= 50 when the columns are too
+    // heterogeneous for 22 bits, for forced tensor stores on small n, or forced
+    // (path 5); FP64 below n = 4096 otherwise; FFMA for the rest
     const bool proj = notion != RRS_HALFSPACE;
     const bool forced = e->contract_path == 2;
     const bool autop = e->contract_path == 0;
-    p.tcs = proj && tc6_layout(e->d).ns <= 19 &&
-            (forced || (autop && e->n >= 4096 && e->d >= 32 && e->col_ratio <= 4096.0));
-    p.store64 = proj && !p.tcs && e->n < STORE64_N;
+    const bool big = e->n >= 4096;
     p.wide = e->d > TC_MAX_D;
-    p.tcws = proj && !p.store64 && !p.wide && e->d > TC_SLICE &&
-             (forced || (autop && e->n >= 4096 && e->col_ratio <= 8.0));
+    const bool split2 = proj && big && (forced || (autop && e->col_ratio <= 8.0));
+    p.tcst = split2 && e->d <= TC_SLICE && contract_tc_store_fits(e->d);
+    p.tcws = split2 && e->d > TC_SLICE && !p.wide;
+    p.tcs = proj && !p.tcst && tc6_layout(e->d).ns <= 19 &&
+            (e->contract_path == 5 || (forced && !big) ||
+             (autop && big && e->d >= 32 && e->col_ratio <= 4096.0));
+    p.store64 = proj && !p.tcs && !p.tcst && !p.tcws && e->n < STORE64_N;
     const int64_t d = e->d, n = e->n;
     int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * tcf_dp((int)d) * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 16 +
                     d * 40 + 64 +
@@ -254,7 +262,7 @@ int ensure_ws(rrs_engine* e, const Plan& p, int notion) {
     CK(e->dmin.ensure(Qb * 8));
     CK(e->bestcnt.ensure(Qb * 8));
     CK(e->uop.ensure(p.tcf   ? Qb * (size_t)p.nb8 * tcf_block_bytes(e->d)
-                     : (p.tc || p.tcws) ? Qb * (size_t)p.nb8 * tc_block_bytes(e->d)
+                     : (p.tc || p.tcws || p.tcst) ? Qb * (size_t)p.nb8 * tc_block_bytes(e->d)
                      : p.tcs ? Qb * (size_t)p.nb8 * tc6_block_bytes(e->d)
                              : 16));
     if (notion == RRS_HALFSPACE) {
@@ -367,7 +375,7 @@ int univariate_from_store(rrs_engine* e, const Plan& p, int Qb, int notion, cons
         const int jbn = (p.MB - jb0) < p.jchunk ? (p.MB - jb0) : p.jchunk;
         {
             Timer t(e, 1);
-            if (p.tcws) {
+            if (p.tcws || p.tcst) {
                 TcArgs t{};
                 t.xb = e->xcb.as<float>();
                 t.zq = e->zq0.as<float>();
@@ -383,7 +391,8 @@ int univariate_from_store(rrs_engine* e, const Plan& p, int Qb, int notion, cons
                 t.y = e->y.as<float>();
                 t.jb0 = jb0;
                 t.jbn = jbn;
-                CK(launch_contract_tcw_store(t, e->sms, e->stream));
+                if (p.tcst) CK(launch_contract_tc_store(t, e->sms, e->stream));
+                else CK(launch_contract_tcw_store(t, e->sms, e->stream));
                 e->stats.tensor_contract_launches++;
             } else if (p.wide && !p.store64) {
                 Contract64Args c{};
@@ -528,7 +537,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 g.refl_mode = e->reflmode.as<int>();
                 g.refl_v = e->reflv.as<double>();
                 g.u64 = e->u64.as<double>();
-                g.u32 = (p.tc || p.tcs || p.tcws) ? nullptr : e->u32.as<float>();  // tensor paths: uop only
+                g.u32 = (p.tc || p.tcs || p.tcws || p.tcst) ? nullptr : e->u32.as<float>();  // tensor: uop only
                 g.seed = cfg->seed;
                 g.q0 = q0 + b0;
                 g.refinement = (uint32_t)l;
@@ -537,7 +546,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
                 g.m = m;
                 g.mpad = p.mpad;
                 g.d = d;
-                g.uop = (p.tc || p.tcws) ? e->uop.as<unsigned char>() : nullptr;
+                g.uop = (p.tc || p.tcws || p.tcst) ? e->uop.as<unsigned char>() : nullptr;
                 g.uop_mode = p.tcf ? 1 : 0;
                 g.u32r = p.tcf ? e->u32.as<float>() : nullptr;
                 g.NB = p.nb8;
@@ -698,10 +707,10 @@ int rrs_engine_set_workspace_limit(rrs_engine* e, int64_t bytes) {
 
 int rrs_engine_set_contract_path(rrs_engine* e, int32_t path) {
     if (!e) return fail(RRS_ERR_INVALID, "engine is null");
-    if (path < 0 || path > 4 || path == 3)
+    if (path < 0 || path > 5 || path == 3)
         return fail(RRS_ERR_INVALID,
-                    "contract path must be 0 (auto), 1 (FFMA), 2 (tensor) or 4 (filter and refine); "
-                    "3 (the 2-SM split kernel) was removed");
+                    "contract path must be 0 (auto), 1 (FFMA), 2 (tensor), 4 (filter and refine) or 5 (three-term "
+                    "tensor projection store); 3 (the 2-SM split kernel) was removed");
     e->contract_path = path;
     return RRS_OK;
 }
@@ -912,7 +921,7 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
         CK(launch_pack_directions(e->u64.as<double>(), e->u32.as<float>(), 1, m, p.mpad, d, e->stream));
     if (p.tc && !p.tcf) CK(launch_pack_tc_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (p.tcs) CK(launch_pack_tc6_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
-    if (p.tcws)
+    if (p.tcws || p.tcst)
         CK(launch_pack_tc_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (notion == RRS_HALFSPACE) {
         CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.mpad * 2 * 4, e->stream));

@@ -343,7 +343,9 @@ cudaError_t launch_contract_tcf(TcfArgs a, int sms, cudaStream_t st);  // filter
 cudaError_t launch_pack_tcf_operand(const double* u64, unsigned char* uop, float* u32r, int Qb, int m, int NB,
                                     int mpad, int d, cudaStream_t st);
 cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st);
-cudaError_t launch_contract_tcw_store(TcArgs a, int sms, cudaStream_t st);  // centred projection store, 64 < d <= 256  // 64 < d <= 256 (contract_tcw.cu)
+cudaError_t launch_contract_tcw_store(TcArgs a, int sms, cudaStream_t st);  // centred projection store, 64 < d <= 256
+cudaError_t launch_contract_tc_store(TcArgs a, int sms, cudaStream_t st);   // centred projection store, d <= 64
+bool contract_tc_store_fits(int d);  // its shared-memory layout leaves >= 2 raw-tile stages  // 64 < d <= 256 (contract_tcw.cu)
 cudaError_t launch_contract_tcs(TcsArgs a, int sms, cudaStream_t st);  // projection store, d <= 64
 cudaError_t launch_pack_tc6_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,
                                     cudaStream_t st);
