@@ -1207,6 +1207,225 @@ static cudaError_t launch_sel3(const SelectArgs& a, dim3 grid, cudaStream_t st) 
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------- K3 v5 --
+// Sample-bracket select for rows past shared memory (n > 53248, config 5p:
+// n = 1M).  v2 streams a 4 MB row ~8 times (key rewrite, radix passes, the MAD
+// rewrite); here an order statistic costs two streaming passes: pass A counts
+// the keys below the sample bracket and histograms the keys inside it (1024
+// offset bins, one red.shared each, ~20 % of the keys), pass B gathers the
+// keys of the bin holding the target rank (a few hundred) into shared memory,
+// where v3's candidate select finishes.  A bin above S5_CAP keys (ties) is
+// refined by another histogram pass restricted to it; a missed bracket
+// restarts from the full key range.  Same keys / midpoints as v2: bitwise
+// equal depths.
+constexpr int S5_NT = 1024;
+constexpr int S5_CAP = 8192;
+
+// one pass over the row: keys < base counted, keys in [base, base + span]
+// histogrammed by (key - base) >> shift; returns (below, inside) totals
+template <typename KF>
+__device__ void s5_hist_pass(const float* __restrict__ row, int64_t n, KF kf, uint32_t base, uint32_t span, int shift,
+                             Sel3Shared<S5_NT>& sh, uint32_t& below, uint32_t& inside) {
+    const int tid = threadIdx.x;
+    __syncthreads();  // previous readers of hist are done
+    for (int i = tid; i < S3_BINS; i += S5_NT) sh.hist[i] = 0u;
+    __syncthreads();
+    const uint32_t hbase = smem_u32(sh.hist);
+    uint32_t b = 0, in = 0;
+    s3_row_each<S5_NT>(row, (int)n, [&](float y) {
+        const uint32_t key = kf(y);
+        const uint32_t off = key - base;
+        b += key < base ? 1u : 0u;
+        const uint32_t addr = hbase + ((off >> shift) << 2);
+        asm volatile("{\n.reg .pred p;\nsetp.le.u32 p, %0, %1;\n@p red.shared.add.u32 [%2], 1;\n}\n" ::"r"(off), "r"(span),
+                     "r"(addr)
+                     : "memory");
+        in += off <= span ? 1u : 0u;
+    });
+    below = s3_reduce_add<S5_NT>(b, sh);
+    inside = s3_reduce_add<S5_NT>(in, sh);
+}
+
+// the bin of sh.hist holding rank t (0-based, among the histogrammed keys):
+// bin index, keys in lower bins, keys in the bin
+__device__ void s5_find_bin(uint32_t t, Sel3Shared<S5_NT>& sh, uint32_t& bin, uint32_t& below, uint32_t& cnt) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t h = sh.hist[tid];  // S3_BINS == S5_NT: one bin per thread
+    uint32_t incl = h;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) sh.wsum[warp] = incl;
+    __syncthreads();
+    uint32_t run = incl - h;
+    for (int w = 0; w < warp; ++w) run += sh.wsum[w];
+    if (run <= t && t < run + h) {
+        sh.s_bin = (uint32_t)tid;
+        sh.s_below = run;
+        sh.s_cnt = h;
+    }
+    __syncthreads();
+    bin = sh.s_bin;
+    below = sh.s_below;
+    cnt = sh.s_cnt;
+    __syncthreads();
+}
+
+// keys at ranks R (and R + 1) of the n keys kf(y) of a global row; c_le = keys <= key(R)
+template <typename KF>
+__device__ void s5_rank(const float* __restrict__ row, int64_t n, KF kf, uint32_t R, bool need_next,
+                        const uint32_t* sorted, uint32_t* cand, Sel3Shared<S5_NT>& sh, uint32_t& kR, uint32_t& kN,
+                        uint32_t& c_le, unsigned* fallbacks) {
+    uint32_t lo, hi;
+    s3_bracket<Sel3Cfg<S5_NT>::S>(sorted, R, need_next ? R + 1 : R, (uint32_t)n, lo, hi);
+    uint32_t base = lo, span = hi - lo, wbelow = 0, wcnt = 0;
+    for (int round = 0;; ++round) {
+        const int bits = span ? 32 - __clz(span) : 0;
+        const int shift = bits > S3_BITS ? bits - S3_BITS : 0;
+        uint32_t below, inside;
+        s5_hist_pass(row, n, kf, base, span, shift, sh, below, inside);
+        if (R < below || R >= below + inside) {
+            // the sample bracket missed: restart from the whole key range
+            if (fallbacks && threadIdx.x == 0) atomicAdd(fallbacks, 1u);
+            base = 0u;
+            span = 0xFFFFFFFFu;
+            continue;
+        }
+        uint32_t bin, bbelow, bcnt;
+        s5_find_bin(R - below, sh, bin, bbelow, bcnt);
+        const uint32_t start = bin << shift;
+        base += start;
+        span = min(span - start, (shift ? (1u << shift) : 1u) - 1u);
+        wbelow = below + bbelow;
+        wcnt = bcnt;
+        if (wcnt <= (uint32_t)S5_CAP || span == 0u) break;
+    }
+    if (span == 0u) {  // one key value
+        kR = base;
+        c_le = wbelow + wcnt;
+    } else {
+        // gather the window's keys (pass B)
+        if (threadIdx.x == 0) sh.s_ovf = 0u;
+        __syncthreads();
+        s3_row_each<S5_NT>(row, (int)n, [&](float y) {
+            const uint32_t key = kf(y);
+            if (key - base <= span) cand[atomicAdd(&sh.s_ovf, 1u)] = key;
+        });
+        __syncthreads();
+        const auto each = [&](auto&& f) { s3_arr_each<S5_NT>(cand, (int)wcnt, f); };
+        uint32_t cl;
+        kR = s3_kth<S5_NT>(each, R - wbelow, base, base + span, wcnt, sh, cl);
+        c_le = wbelow + cl;
+    }
+    kN = kR;
+    if (need_next && c_le < R + 2) {
+        uint32_t best = 0xFFFFFFFFu;
+        if (span != 0u && R + 1 < wbelow + wcnt) {
+            s3_arr_each<S5_NT>(cand, (int)wcnt, [&](uint32_t k2) { best = min(best, k2 > kR ? k2 : 0xFFFFFFFFu); });
+        } else {
+            s3_row_each<S5_NT>(row, (int)n, [&](float y) {
+                const uint32_t k2 = kf(y);
+                best = min(best, k2 > kR ? k2 : 0xFFFFFFFFu);
+            });
+        }
+        kN = s3_reduce_min<S5_NT>(best, sh);
+    }
+}
+
+__global__ void __launch_bounds__(S5_NT) select_v5_kernel(const SelectArgs a) {
+    extern __shared__ __align__(16) unsigned char sel5_raw[];
+    Sel3Shared<S5_NT>& sh = *reinterpret_cast<Sel3Shared<S5_NT>*>(sel5_raw);
+    uint32_t* cand = reinterpret_cast<uint32_t*>(sel5_raw + ((sizeof(Sel3Shared<S5_NT>) + 15) & ~size_t(15)));
+    const int jj = blockIdx.x, q = blockIdx.y;
+    const int j = a.j0 + jj;
+    if (j >= a.m) return;
+    const int tid = threadIdx.x;
+    const int64_t n = a.n;
+    const float* row = a.y + ((size_t)q * a.jcount + jj) * a.n;
+    constexpr int S = Sel3Cfg<S5_NT>::S;
+    uint32_t sv = 0u;
+    if (tid < S) sv = fkey(__ldg(row + (((int64_t)(2 * tid + 1) * n) / (2 * S))));
+    s3_sort_sample<S5_NT>(sv, sh);
+
+    const uint32_t k = (uint32_t)((n - 1) >> 1);
+    const bool even = (n & 1) == 0;
+    uint32_t kR, kN, c_le;
+    s5_rank(row, n, S3KeyY{}, k, even, sh.sorted, cand, sh, kR, kN, c_le, a.fallbacks);
+    const double lov = (double)kfloat(kR);
+    const double med = even ? (lov + (double)kfloat(kN)) / 2.0 : lov;
+    const double medz = med + (a.shift ? a.shift[(size_t)q * a.m + j] : 0.0);
+    double depth;
+    if (a.notion == 1) {
+        // the sample's deviations: two monotone runs, merge-ranked (as in v3)
+        uint32_t dk = 0u, le = 0u;
+        if (tid < S) {
+            const double yv = (double)kfloat(sh.sorted[tid]);
+            dk = fkey((float)fabs(yv - med));
+            le = yv <= med ? 1u : 0u;
+        }
+        __syncthreads();
+        if (tid < S) sh.sdev[tid] = dk;
+        const uint32_t nl = s3_reduce_add<S5_NT>(le, sh);
+        if (tid < S) {
+            uint32_t rank;
+            if ((uint32_t)tid < nl) {
+                uint32_t lo_i = nl, hi_i = S;
+                while (lo_i < hi_i) {
+                    const uint32_t mid = (lo_i + hi_i) >> 1;
+                    if (sh.sdev[mid] < dk) lo_i = mid + 1;
+                    else hi_i = mid;
+                }
+                rank = (nl - 1 - tid) + (lo_i - nl);
+            } else {
+                uint32_t lo_i = 0, hi_i = nl;
+                while (lo_i < hi_i) {
+                    const uint32_t mid = (lo_i + hi_i) >> 1;
+                    if (sh.sdev[mid] <= dk) hi_i = mid;
+                    else lo_i = mid + 1;
+                }
+                rank = (tid - nl) + (nl - lo_i);
+            }
+            sh.sorted[rank] = dk;
+        }
+        __syncthreads();
+        uint32_t mR, mN, mc;
+        s5_rank(row, n, S3KeyAbsDev{med}, k, even, sh.sorted, cand, sh, mR, mN, mc, a.fallbacks);
+        const double mlo = (double)kfloat(mR);
+        const double mad = even ? (mlo + (double)kfloat(mN)) / 2.0 : mlo;
+        const double dev = fabs(medz);
+        if (mad == 0.0) depth = (dev == 0.0) ? 1.0 : 0.0;
+        else depth = 1.0 / (1.0 + dev / mad);
+    } else {
+        const double dev = -medz;
+        const uint32_t npos = (uint32_t)n - c_le;
+        if (dev <= 0.0) {
+            depth = 1.0;
+        } else if (npos == 0u) {
+            depth = 0.0;
+        } else {
+            const uint32_t A = c_le + ((npos - 1u) >> 1);
+            const bool pe = (npos & 1u) == 0u;
+            uint32_t aR, aN, ac;
+            s5_rank(row, n, S3KeyY{}, A, pe, sh.sorted, cand, sh, aR, aN, ac, a.fallbacks);
+            const double ta = (double)(float)((double)kfloat(aR) - med);
+            const double madp = pe ? (ta + (double)(float)((double)kfloat(aN) - med)) / 2.0 : ta;
+            depth = 1.0 / (1.0 + dev / madp);
+        }
+    }
+    if (tid == 0) a.depths[(size_t)q * a.m + j] = depth;
+}
+
+static cudaError_t launch_sel5(const SelectArgs& a, dim3 grid, cudaStream_t st) {
+    const size_t smem = ((sizeof(Sel3Shared<S5_NT>) + 15) & ~size_t(15)) + (size_t)S5_CAP * 4;
+    cudaError_t e = cudaFuncSetAttribute(select_v5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    select_v5_kernel<<<grid, S5_NT, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
 template <int NT, bool GLB>
 static cudaError_t launch_sel2(const SelectArgs& a, dim3 grid, cudaStream_t st) {
     const size_t smem = ((sizeof(Sel2Shared<NT>) + 15) & ~size_t(15)) + (GLB ? (size_t)SEL2G_CAP * 4 : (size_t)a.n * 4);
@@ -1231,6 +1450,9 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
         if (a.n <= SEL2_WIDER_N) return launch_sel2<512, false>(a, grid, st);
         return launch_sel2<1024, false>(a, grid, st);
     }
+    // rows past shared memory: the two-pass sample-bracket select (v5) unless
+    // the radix select is asked for (variant 2)
+    if (a.variant != 2 && a.n < ((int64_t)1 << 31)) return launch_sel5(a, grid, st);
 #ifndef RRS_SEL_LEGACY_GLOBAL
     // (16-byte key loads: rows must start aligned, i.e. n % 4 == 0)
     if ((a.n & 3) == 0 && a.n < ((int64_t)1 << 31)) return launch_sel2<1024, true>(a, grid, st);
