@@ -1219,12 +1219,12 @@ static cudaError_t launch_sel3(const SelectArgs& a, dim3 grid, cudaStream_t st) 
 // refined by another histogram pass restricted to it; a missed bracket
 // restarts from the full key range.  Same keys / midpoints as v2: bitwise
 // equal depths.
-constexpr int S5_NT = 1024;
-constexpr int S5_CAP = 8192;
+constexpr int S5_CAP = 8192;                   // gathered keys (global rows)
+
 
 // one pass over the row: keys < base counted, keys in [base, base + span]
 // histogrammed by (key - base) >> shift; returns (below, inside) totals
-template <typename KF>
+template <int S5_NT, typename KF>
 __device__ void s5_hist_pass(const float* __restrict__ row, int64_t n, KF kf, uint32_t base, uint32_t span, int shift,
                              Sel3Shared<S5_NT>& sh, uint32_t& below, uint32_t& inside) {
     const int tid = threadIdx.x;
@@ -1249,10 +1249,17 @@ __device__ void s5_hist_pass(const float* __restrict__ row, int64_t n, KF kf, ui
 
 // the bin of sh.hist holding rank t (0-based, among the histogrammed keys):
 // bin index, keys in lower bins, keys in the bin
+template <int S5_NT>
 __device__ void s5_find_bin(uint32_t t, Sel3Shared<S5_NT>& sh, uint32_t& bin, uint32_t& below, uint32_t& cnt) {
+    constexpr int PER = S3_BINS / S5_NT;  // consecutive bins per thread
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t h = sh.hist[tid];  // S3_BINS == S5_NT: one bin per thread
-    uint32_t incl = h;
+    uint32_t hv[PER], local = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        hv[i] = sh.hist[tid * PER + i];
+        local += hv[i];
+    }
+    uint32_t incl = local;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
         const uint32_t o = __shfl_up_sync(0xffffffffu, incl, off);
@@ -1260,12 +1267,18 @@ __device__ void s5_find_bin(uint32_t t, Sel3Shared<S5_NT>& sh, uint32_t& bin, ui
     }
     if (lane == 31) sh.wsum[warp] = incl;
     __syncthreads();
-    uint32_t run = incl - h;
+    uint32_t run = incl - local;
     for (int w = 0; w < warp; ++w) run += sh.wsum[w];
-    if (run <= t && t < run + h) {
-        sh.s_bin = (uint32_t)tid;
-        sh.s_below = run;
-        sh.s_cnt = h;
+    if (run <= t && t < run + local) {
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            if (run <= t && t < run + hv[i]) {
+                sh.s_bin = (uint32_t)(tid * PER + i);
+                sh.s_below = run;
+                sh.s_cnt = hv[i];
+            }
+            run += hv[i];
+        }
     }
     __syncthreads();
     bin = sh.s_bin;
@@ -1275,7 +1288,7 @@ __device__ void s5_find_bin(uint32_t t, Sel3Shared<S5_NT>& sh, uint32_t& bin, ui
 }
 
 // keys at ranks R (and R + 1) of the n keys kf(y) of a global row; c_le = keys <= key(R)
-template <typename KF>
+template <int S5_NT, int CAP, typename KF>
 __device__ void s5_rank(const float* __restrict__ row, int64_t n, KF kf, uint32_t R, bool need_next,
                         const uint32_t* sorted, uint32_t* cand, Sel3Shared<S5_NT>& sh, uint32_t& kR, uint32_t& kN,
                         uint32_t& c_le, unsigned* fallbacks) {
@@ -1286,7 +1299,7 @@ __device__ void s5_rank(const float* __restrict__ row, int64_t n, KF kf, uint32_
         const int bits = span ? 32 - __clz(span) : 0;
         const int shift = bits > S3_BITS ? bits - S3_BITS : 0;
         uint32_t below, inside;
-        s5_hist_pass(row, n, kf, base, span, shift, sh, below, inside);
+        s5_hist_pass<S5_NT>(row, n, kf, base, span, shift, sh, below, inside);
         if (R < below || R >= below + inside) {
             // the sample bracket missed: restart from the whole key range
             if (fallbacks && threadIdx.x == 0) atomicAdd(fallbacks, 1u);
@@ -1295,13 +1308,13 @@ __device__ void s5_rank(const float* __restrict__ row, int64_t n, KF kf, uint32_
             continue;
         }
         uint32_t bin, bbelow, bcnt;
-        s5_find_bin(R - below, sh, bin, bbelow, bcnt);
+        s5_find_bin<S5_NT>(R - below, sh, bin, bbelow, bcnt);
         const uint32_t start = bin << shift;
         base += start;
         span = min(span - start, (shift ? (1u << shift) : 1u) - 1u);
         wbelow = below + bbelow;
         wcnt = bcnt;
-        if (wcnt <= (uint32_t)S5_CAP || span == 0u) break;
+        if (wcnt <= (uint32_t)CAP || span == 0u) break;
     }
     if (span == 0u) {  // one key value
         kR = base;
@@ -1335,6 +1348,7 @@ __device__ void s5_rank(const float* __restrict__ row, int64_t n, KF kf, uint32_
     }
 }
 
+template <int S5_NT, int CAP>
 __global__ void __launch_bounds__(S5_NT) select_v5_kernel(const SelectArgs a) {
     extern __shared__ __align__(16) unsigned char sel5_raw[];
     Sel3Shared<S5_NT>& sh = *reinterpret_cast<Sel3Shared<S5_NT>*>(sel5_raw);
@@ -1353,7 +1367,7 @@ __global__ void __launch_bounds__(S5_NT) select_v5_kernel(const SelectArgs a) {
     const uint32_t k = (uint32_t)((n - 1) >> 1);
     const bool even = (n & 1) == 0;
     uint32_t kR, kN, c_le;
-    s5_rank(row, n, S3KeyY{}, k, even, sh.sorted, cand, sh, kR, kN, c_le, a.fallbacks);
+    s5_rank<S5_NT, CAP>(row, n, S3KeyY{}, k, even, sh.sorted, cand, sh, kR, kN, c_le, a.fallbacks);
     const double lov = (double)kfloat(kR);
     const double med = even ? (lov + (double)kfloat(kN)) / 2.0 : lov;
     const double medz = med + (a.shift ? a.shift[(size_t)q * a.m + j] : 0.0);
@@ -1392,7 +1406,7 @@ __global__ void __launch_bounds__(S5_NT) select_v5_kernel(const SelectArgs a) {
         }
         __syncthreads();
         uint32_t mR, mN, mc;
-        s5_rank(row, n, S3KeyAbsDev{med}, k, even, sh.sorted, cand, sh, mR, mN, mc, a.fallbacks);
+        s5_rank<S5_NT, CAP>(row, n, S3KeyAbsDev{med}, k, even, sh.sorted, cand, sh, mR, mN, mc, a.fallbacks);
         const double mlo = (double)kfloat(mR);
         const double mad = even ? (mlo + (double)kfloat(mN)) / 2.0 : mlo;
         const double dev = fabs(medz);
@@ -1409,7 +1423,7 @@ __global__ void __launch_bounds__(S5_NT) select_v5_kernel(const SelectArgs a) {
             const uint32_t A = c_le + ((npos - 1u) >> 1);
             const bool pe = (npos & 1u) == 0u;
             uint32_t aR, aN, ac;
-            s5_rank(row, n, S3KeyY{}, A, pe, sh.sorted, cand, sh, aR, aN, ac, a.fallbacks);
+            s5_rank<S5_NT, CAP>(row, n, S3KeyY{}, A, pe, sh.sorted, cand, sh, aR, aN, ac, a.fallbacks);
             const double ta = (double)(float)((double)kfloat(aR) - med);
             const double madp = pe ? (ta + (double)(float)((double)kfloat(aN) - med)) / 2.0 : ta;
             depth = 1.0 / (1.0 + dev / madp);
@@ -1418,11 +1432,13 @@ __global__ void __launch_bounds__(S5_NT) select_v5_kernel(const SelectArgs a) {
     if (tid == 0) a.depths[(size_t)q * a.m + j] = depth;
 }
 
+template <int S5_NT, int CAP>
 static cudaError_t launch_sel5(const SelectArgs& a, dim3 grid, cudaStream_t st) {
-    const size_t smem = ((sizeof(Sel3Shared<S5_NT>) + 15) & ~size_t(15)) + (size_t)S5_CAP * 4;
-    cudaError_t e = cudaFuncSetAttribute(select_v5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = ((sizeof(Sel3Shared<S5_NT>) + 15) & ~size_t(15)) + (size_t)CAP * 4;
+    cudaError_t e =
+        cudaFuncSetAttribute(select_v5_kernel<S5_NT, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    select_v5_kernel<<<grid, S5_NT, smem, st>>>(a);
+    select_v5_kernel<S5_NT, CAP><<<grid, S5_NT, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -1452,7 +1468,7 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
     }
     // rows past shared memory: the two-pass sample-bracket select (v5) unless
     // the radix select is asked for (variant 2)
-    if (a.variant != 2 && a.n < ((int64_t)1 << 31)) return launch_sel5(a, grid, st);
+    if (a.variant != 2 && a.n < ((int64_t)1 << 31)) return launch_sel5<1024, S5_CAP>(a, grid, st);
 #ifndef RRS_SEL_LEGACY_GLOBAL
     // (16-byte key loads: rows must start aligned, i.e. n % 4 == 0)
     if ((a.n & 3) == 0 && a.n < ((int64_t)1 << 31)) return launch_sel2<1024, true>(a, grid, st);
