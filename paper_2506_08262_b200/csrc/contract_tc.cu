@@ -386,6 +386,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                         *reinterpret_cast<uint4*>(P + (main_chunks + cc) * (TC_NP * 16)) =
                             make_uint4(lw[0], lw[1], lw[2], lw[3]);
                         *reinterpret_cast<uint4*>(P + (2 * main_chunks + cc) * (TC_NP * 16)) = hv;
+                    } else if (L.rem <= 2) {
+                        // remainder of one or two coordinates (d = 50: 48, 49): its products sit
+                        // at K positions 48 Q + p rem + i, all inside one 16-byte chunk
+                        // [hi0 hi1 lo0 lo1 hi0 hi1 0 0] (rem 2) / [hi lo hi 0 ...] (rem 1)
+                        const uint32_t h0 = hw[0], l0 = lw[0];
+                        const uint4 rv = L.rem == 2 ? make_uint4(h0, l0, h0, 0u)
+                                                    : make_uint4((h0 & 0xFFFFu) | (l0 << 16), h0 & 0xFFFFu, 0u, 0u);
+                        *reinterpret_cast<uint4*>(P + (6 * L.q16) * (TC_NP * 16)) = rv;
                     } else {
                         // remainder coordinates 16 Q + i: scattered into the tail K steps
                         // (a rolled loop: at most two such chunks, d % 16 values)

@@ -195,6 +195,13 @@ __device__ __forceinline__ void w_store_slice(unsigned char* P, const float2 (&a
             *reinterpret_cast<uint4*>(P + cc * (W_NP * 16)) = hv;
             *reinterpret_cast<uint4*>(P + (mc + cc) * (W_NP * 16)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
             *reinterpret_cast<uint4*>(P + (2 * mc + cc) * (W_NP * 16)) = hv;
+        } else if (rem == 8 && 8 * cc == 16 * q16) {
+            // a remainder of exactly 8 coordinates (d = 200's last slice): product p
+            // fills the whole chunk 6 q16 + p -- three 16-byte stores, no scatter
+            const uint4 hv = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(P + (6 * q16) * (W_NP * 16)) = hv;
+            *reinterpret_cast<uint4*>(P + (6 * q16 + 1) * (W_NP * 16)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            *reinterpret_cast<uint4*>(P + (6 * q16 + 2) * (W_NP * 16)) = hv;
         } else {
 #pragma unroll 1
             for (int e = 0; e < 8; ++e) {
