@@ -530,7 +530,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                             m0 = __funnelshift_l(y0[j], m0, 1);
                             m1 = __funnelshift_l(y1[j], m1, 1);
                         }
-                        cnt[b] += __popc(m0 & keep0) + __popc(m1 & keep1);
+                        // static register indices (a dynamic cnt[b] lands in local memory)
+                        const uint32_t v = (uint32_t)(__popc(m0 & keep0) + __popc(m1 & keep1));
+#pragma unroll
+                        for (int i = 0; i < TC_GB_MAX; ++i) cnt[i] += i == b ? v : 0u;
                     }
                 }
             }
