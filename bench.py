@@ -245,6 +245,8 @@ def main():
     ap.add_argument("--early-exit", action="store_true",
                     help="RrsConfig(early_exit=True): exact early exit of finished halfspace queries "
                          "(outputs bitwise unchanged; not the default, which does the reference's full work)")
+    ap.add_argument("--workspace-mb", type=int, default=0,
+                    help="engine workspace cap (query batching / projection chunking), MiB; 0 = default")
     ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "filter", "tensor3"],
                     help="halfspace contraction kernel (auto: the library's choice)")
     args = ap.parse_args()
@@ -280,6 +282,8 @@ def main():
     eng = rrs.engine(local)
     eng.set_contract_path(args.contract_path)
     eng.set_select_path(args.select_path)
+    if args.workspace_mb:
+        eng.set_workspace_limit(args.workspace_mb << 20)
     stream = torch.cuda.Stream()  # one non-default stream shared by torch and the engine
     torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
