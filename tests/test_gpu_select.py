@@ -145,3 +145,29 @@ def test_far_queries_tier2(b200, notion, n, d):
         got = b200.evaluate_directions(z, data, U, notion, cfg)
         ref = oracle.evaluate_directions(z, X, U, notion)
         np.testing.assert_allclose(got, ref, rtol=DEPTH_RTOL, atol=0)
+
+
+def test_select_randomized_bitwise(b200):
+    """40 random rows (n anywhere in 2048 .. 130000, odd / unaligned lengths,
+    mixtures of Gaussian, Cauchy, rounded values with heavy ties and constant
+    blocks): the sample-bracket selects (v3 / v5) give the radix select's
+    depths bit for bit."""
+    rng = np.random.default_rng(2024)
+    U = np.array([[1.0, 0.0], [0.0, 1.0], [0.8, -0.6]])
+    for trial in range(40):
+        n = int(rng.integers(2048, 130_000))
+        kind = trial % 4
+        if kind == 0:
+            col = rng.standard_normal(n)
+        elif kind == 1:
+            col = rng.standard_cauchy(n)
+        elif kind == 2:
+            col = np.round(rng.standard_normal(n) * 3.0)  # ~20 distinct values
+        else:
+            col = rng.standard_normal(n)
+            col[rng.random(n) < 0.3] = 1.5  # a 30 % tie block
+        X = np.stack([col, 1e-2 * rng.standard_normal(n)], axis=1)
+        z = np.array([rng.standard_normal() * 2.0, 0.0])
+        for notion in NOTIONS:
+            auto, radix, _ = _depths(b200, X, z, U, notion)
+            assert np.array_equal(auto, radix), (trial, n, kind, notion, auto, radix)
