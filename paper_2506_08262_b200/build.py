@@ -57,14 +57,20 @@ def build(verbose: bool = False, force: bool = False) -> str:
     headers.append(os.path.join(os.path.dirname(HERE), "include", "rrs_b200.h"))
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-Xptxas", "-v" if verbose else "-O3"]
-    objs = []
+    objs, jobs = [], []
     for src, extra in SOURCES.items():
         path = os.path.join(CSRC, src)
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [path, *headers]):
-            cmd = [*common, *extra, "-c", path, "-o", obj]
-            subprocess.run(cmd, check=True, capture_output=not verbose)
+            jobs.append([*common, *extra, "-c", path, "-o", obj])
+    # the translation units are independent: compile them in parallel
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1) or 1) as pool:
+        for r in list(pool.map(lambda cmd: subprocess.run(cmd, capture_output=not verbose), jobs)):
+            if r.returncode != 0:
+                raise subprocess.CalledProcessError(r.returncode, r.args, r.stdout, r.stderr)
     if force or _stale(LIB, objs):
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"]
         subprocess.run(cmd, check=True, capture_output=not verbose)
