@@ -9,7 +9,8 @@
 // sides (#<= = n - #>0, #>= = n - #<0).
 //
 // Operands ("two-term FP16 split", FP32-class accuracy; packed along K as in
-// kernels.h tc_layout: d = 50 takes 10 K steps of 16 instead of 3 x 4):
+// kernels.h tc_layout: each FP16 term stored once, d = 50 takes 7 stored K
+// steps of 16 and 10 MMAs instead of 3 x 4):
 //   a_il = x_il - z_l (FP32, as in contract.cu), scaled per point by the power
 //          of two s_i = 2^(14 - E_i) with max_l |a_il| < 2^E_i (never changes a
 //          sign); a*s = ah + al, ah = fp16(a*s), al = fp16(a*s - ah): 22 bits;
@@ -25,18 +26,18 @@
 // this kernel runs N = 128 MMAs at the full 64-clock rate.
 //
 // Layout (M = 128 DIRECTIONS on TMEM lanes, N = 128 POINTS, K = 16 per MMA,
-// ns = tc_layout(d).ns K steps per (tile, block)):
+// ns = tc_layout(d).ns stored K steps per tile / block, 3 Q + R MMAs):
 //   TMEM columns [0,128) and [128,256): two FP32 accumulator buffers;
 //   TMEM columns [256 + 8 ns b, 256 + 8 ns (b + 1)): direction block b of the
 //   current unit (8 columns = 16 K values per step), resident for the whole
 //   unit (TS MMA: A from TMEM, B from shared memory); gb = 256 / (8 ns) blocks
-//   (3 at d = 50).
+//   (4 at d = 50), so each converted point tile feeds 4 blocks.
 // Work unit = (query, group of gb direction blocks, chunk of 128-point tiles);
 // persistent CTAs (one per SM) stride over units.
 //   warp 0      producer: TMA of the unit's direction blocks (ns * 4 KB each, one
 //               at a time) into a staging area (cp.async.bulk + mbarrier);
 //   warp 1      TMEM allocator + tcgen05 issuer: staging -> TMEM (tcgen05.cp)
-//               once per unit, then per tile and block ns MMAs;
+//               once per unit, then per tile and block 3 Q + R MMAs;
 //   warp 2      producer: TMA of each raw FP32 point tile (d*512 bytes, the
 //               tile-blocked dataset) into a 2-4 stage ring;
 //   warps 3-10  converters: one (point, half of K) per thread: x - z from the
@@ -66,7 +67,7 @@ constexpr int TC_EPI_WARPS = 8;                  // 4 lane quarters x 2 column h
 constexpr int TC_EPI_THREADS = TC_EPI_WARPS * 32;
 constexpr int TC_THREADS = (TC_EPI_WARP0 + TC_EPI_WARPS) * 32;  // 608
 constexpr int TC_MAXD = 64;                      // coordinates handled per point (2 x 32)
-constexpr int TC_MAXNS = 12;                     // K steps at d = 64
+constexpr int TC_MAXNS = 9;                      // stored K steps, d <= 64 (d = 63: 2 * 3 + 3)
 constexpr int TC_MD = 128;                       // directions per block (MMA M)
 constexpr int TC_NP = 128;                       // points per tile (MMA N)
 constexpr int TC_GB_MAX = 8;                     // direction blocks resident per unit (max)
@@ -135,11 +136,12 @@ __device__ __forceinline__ TcUnit tc_unit(const TcArgs& a, int64_t u) {
     return r;
 }
 
-template <int NS>
+template <int Q, int R>
 __device__ __forceinline__ void mma_issue(const TcArgs& a, int64_t units, unsigned char* sP, unsigned char* sD,
                                           uint64_t* pfull, uint64_t* pempty, uint64_t* dfull, uint64_t* dempty,
                                           uint64_t* tfull, uint64_t* tempty, uint64_t* udone) {
     constexpr uint32_t tmem = 0u;
+    constexpr int NS = 2 * Q + R;
     constexpr uint32_t stage_bytes = NS * 4096;
     // F32 accumulate, FP16 A and B, K-major both, N = 128, M = 128
     const uint32_t idesc = (1u << 4) | ((uint32_t)(TC_NP >> 3) << 17) | ((uint32_t)(TC_MD >> 4) << 24);
@@ -162,8 +164,8 @@ __device__ __forceinline__ void mma_issue(const TcArgs& a, int64_t units, unsign
                 const uint32_t buf = gacc & 1u;
                 if (gacc >= 2) mbar_wait(&tempty[buf], ((gacc >> 1) - 1) & 1u);
                 tc_fence_after();
-                mma_tile_block<NS>(tmem + buf * ACC_COLS, tmem + A_TMEM + 8u * NS * b, bd, idesc,
-                                   smem_u32(&tfull[buf]));
+                mma_split_block<Q, R>(tmem + buf * ACC_COLS, tmem + A_TMEM + 8u * NS * b, bd, idesc,
+                                      smem_u32(&tfull[buf]));
             }
             mma_commit_elect(&pempty[s]);  // point stage free once this tile's MMAs are done
         }
@@ -261,20 +263,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
         }
     } else if (warp == 1) {
         // -------------------------------------------------------- MMA issuer
-        switch (L.ns) {
-            case 1: mma_issue<1>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
-            case 2: mma_issue<2>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
-            case 3: mma_issue<3>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
-            case 4: mma_issue<4>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
-            case 5: mma_issue<5>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
-            case 6: mma_issue<6>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
-            case 7: mma_issue<7>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
-            case 8: mma_issue<8>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
-            case 9: mma_issue<9>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
-            case 10: mma_issue<10>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
-            case 11: mma_issue<11>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
-            default: mma_issue<12>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone); break;
+#define RRS_TC_ISSUE(Q, R) mma_issue<Q, R>(a, units, sP, sD, pfull, pempty, dfull, dempty, tfull, tempty, udone)
+        switch (4 * L.q16 + L.rsteps) {
+            case 1: RRS_TC_ISSUE(0, 1); break;
+            case 2: RRS_TC_ISSUE(0, 2); break;
+            case 3: RRS_TC_ISSUE(0, 3); break;
+            case 4: RRS_TC_ISSUE(1, 0); break;
+            case 5: RRS_TC_ISSUE(1, 1); break;
+            case 6: RRS_TC_ISSUE(1, 2); break;
+            case 7: RRS_TC_ISSUE(1, 3); break;
+            case 8: RRS_TC_ISSUE(2, 0); break;
+            case 9: RRS_TC_ISSUE(2, 1); break;
+            case 10: RRS_TC_ISSUE(2, 2); break;
+            case 11: RRS_TC_ISSUE(2, 3); break;
+            case 12: RRS_TC_ISSUE(3, 0); break;
+            case 13: RRS_TC_ISSUE(3, 1); break;
+            case 14: RRS_TC_ISSUE(3, 2); break;
+            case 15: RRS_TC_ISSUE(3, 3); break;
+            default: RRS_TC_ISSUE(4, 0); break;
         }
+#undef RRS_TC_ISSUE
     } else if (warp == 2) {
         // -------------------------------------- producer: raw FP32 point tiles
         uint32_t g = 0, rs = 0, rph = 0;  // ring slot and its phase, advanced incrementally
@@ -380,20 +388,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                         lw[e] = pack_half2(res.x, res.y);
                     }
                     if (cc < main_chunks) {
-                        // aligned part: products 0 (hi), 1 (lo), 2 (hi) of coordinates 8 cc .. 8 cc + 7
-                        const uint4 hv = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-                        *reinterpret_cast<uint4*>(P + cc * (TC_NP * 16)) = hv;
+                        // aligned part: the hi and the lo terms of coordinates 8 cc .. 8 cc + 7
+                        *reinterpret_cast<uint4*>(P + cc * (TC_NP * 16)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
                         *reinterpret_cast<uint4*>(P + (main_chunks + cc) * (TC_NP * 16)) =
                             make_uint4(lw[0], lw[1], lw[2], lw[3]);
-                        *reinterpret_cast<uint4*>(P + (2 * main_chunks + cc) * (TC_NP * 16)) = hv;
                     } else if (L.rem <= 2) {
                         // remainder of one or two coordinates (d = 50: 48, 49): its products sit
-                        // at K positions 48 Q + p rem + i, all inside one 16-byte chunk
+                        // at K positions 32 Q + p rem + i, all inside one 16-byte chunk
                         // [hi0 hi1 lo0 lo1 hi0 hi1 0 0] (rem 2) / [hi lo hi 0 ...] (rem 1)
                         const uint32_t h0 = hw[0], l0 = lw[0];
                         const uint4 rv = L.rem == 2 ? make_uint4(h0, l0, h0, 0u)
                                                     : make_uint4((h0 & 0xFFFFu) | (l0 << 16), h0 & 0xFFFFu, 0u, 0u);
-                        *reinterpret_cast<uint4*>(P + (6 * L.q16) * (TC_NP * 16)) = rv;
+                        *reinterpret_cast<uint4*>(P + (4 * L.q16) * (TC_NP * 16)) = rv;
                     } else {
                         // remainder coordinates 16 Q + i: scattered into the tail K steps
                         // (a rolled loop: at most two such chunks, d % 16 values)
@@ -406,7 +412,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) contract_tc_kernel(const TcArgs
                             const uint32_t lv = wi == 0 ? lw[0] : wi == 1 ? lw[1] : wi == 2 ? lw[2] : lw[3];
                             const uint16_t hb = (uint16_t)((e & 1) ? (hv >> 16) : (hv & 0xFFFFu));
                             const uint16_t lb = (uint16_t)((e & 1) ? (lv >> 16) : (lv & 0xFFFFu));
-                            int kk = 32 * L.q16 + cd;  // 48 Q + (cd - 16 Q): product 0
+                            int kk = 16 * L.q16 + cd;  // 32 Q + (cd - 16 Q): product 0
 #pragma unroll
                             for (int pr = 0; pr < 3; ++pr, kk += L.rem)
                                 *reinterpret_cast<uint16_t*>(P + (kk >> 3) * (TC_NP * 16) + (kk & 7) * 2) =

@@ -1,6 +1,7 @@
 // contract_tcw.cu -- K2 on the tensor cores for 64 < d <= 256 ("wide"): the
 // FP16 hi/lo split contraction of contract_tc.cu with the coordinates taken in
-// slices of 64 (kernels.h tc_layout: full slices of 12 K steps + a last slice).
+// slices of 64 (kernels.h tc_layout: full slices of 8 stored K steps / 12 MMAs
+// + a last slice).
 //
 // Same arithmetic and result contract as contract_tc.cu (see there): a_il =
 // x_il - z_l in FP32, a power-of-two scale per point, a*s = ah + al (FP16),
@@ -13,13 +14,13 @@
 // (2^-25 of the scaled unit, i.e. ~2^-39 of the bound).
 //
 // Layout (M = 128 directions on TMEM lanes, N = 128 points, K = 16 per MMA):
-//   one direction block per unit (its A operand: 8 ns TMEM columns, 304 at
-//   d = 200, resident for the unit, loaded slice by slice through a 48 KB
-//   staging area); FP32 accumulator: two buffers of 128 columns when
-//   8 ns <= 256 (d <= 128), else one (the MMAs of the next tile wait for the
-//   epilogue to drain it);
+//   one direction block per unit (its A operand: 8 ns TMEM columns, 208 at
+//   d = 200, resident for the unit, loaded through a staging area); FP32
+//   accumulator: two buffers of 128 columns when 8 ns <= 256 (every d <= 256
+//   but 251..255), else one (the MMAs of the next tile wait for the epilogue
+//   to drain it);
 //   per (tile, slice): the raw FP32 rows [64 s, 64 s + 64) of the tile (TMA),
-//   converted into one 48 KB point-operand stage (2 stages), ns_s MMAs
+//   converted into one 32 KB point-operand stage (2 stages), 3 Q + R MMAs
 //   accumulating into the tile's accumulator.
 // Work units = (chunk of point tiles, query, direction block) with the chunk
 // slowest-varying: the CTAs running at the same time read the same tiles, so
@@ -55,7 +56,7 @@ constexpr int W_MD = 128;
 constexpr int W_NP = 128;
 constexpr int W_P_STAGES = 2;
 constexpr int W_R_MAX = 4;
-constexpr int W_STAGE = TC_SLICE_NS * 4096;  // one slice of a tile: 48 KB
+constexpr int W_STAGE = TC_SLICE_NS * 4096;  // one slice of a tile: 32 KB
 #ifndef RRS_TCW_DSTEPS
 #define RRS_TCW_DSTEPS 4
 #endif
@@ -121,17 +122,19 @@ __device__ __forceinline__ int slice_ns(const TcLayout& L, int s) {
     return s < L.full ? TC_SLICE_NS : L.ns - TC_SLICE_NS * L.full;
 }
 
-// ns MMAs (K = 16 each) of one slice into the accumulator; the first one
+// The nm MMAs (K = 16 each) of one slice with q aligned groups into the
+// accumulator, A / B K steps paired by kernels.h tc_mma_steps; the first one
 // overwrites it when `first` (the tile's first slice), the rest accumulate.
-__device__ __forceinline__ void mma_slice(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, int ns, bool first) {
-    for (int i = 0; i < ns; ++i) {
-        const uint32_t en = (first && i == 0) ? 0u : 1u;
-        asm volatile(
-            "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
-            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(acc),
-            "r"(aT + 8u * (uint32_t)i), "l"(bd + 256ull * (uint64_t)i), "r"(idesc), "r"(en)
-            : "memory");
+__device__ __forceinline__ void mma_slice(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, int q, int nm,
+                                          bool first) {
+    if (elect_one()) {
+        for (int i = 0; i < nm; ++i) {
+            int sa, sb;
+            tc_mma_steps(q, i, sa, sb);
+            umma_f16(acc, aT + 8u * (uint32_t)sa, bd + 256ull * (uint64_t)sb, idesc, (first && i == 0) ? 0u : 1u);
+        }
     }
+    __syncwarp();
 }
 
 // One converter thread's W_CPT coordinates [W_CPT h, W_CPT h + W_CPT) of a slice
@@ -190,18 +193,17 @@ __device__ __forceinline__ void w_store_slice(unsigned char* P, const float2 (&a
             lw[e] = pack_half2(res.x, res.y);
         }
         if (FULL || cc < main_chunks) {
+            // aligned: the hi and the lo terms of 8 coordinates (kernels.h tc_layout)
             const int mc = FULL ? 8 : main_chunks;
-            const uint4 hv = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-            *reinterpret_cast<uint4*>(P + cc * (W_NP * 16)) = hv;
+            *reinterpret_cast<uint4*>(P + cc * (W_NP * 16)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
             *reinterpret_cast<uint4*>(P + (mc + cc) * (W_NP * 16)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-            *reinterpret_cast<uint4*>(P + (2 * mc + cc) * (W_NP * 16)) = hv;
         } else if (rem == 8 && 8 * cc == 16 * q16) {
             // a remainder of exactly 8 coordinates (d = 200's last slice): product p
-            // fills the whole chunk 6 q16 + p -- three 16-byte stores, no scatter
+            // fills the whole chunk 4 q16 + p -- three 16-byte stores, no scatter
             const uint4 hv = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-            *reinterpret_cast<uint4*>(P + (6 * q16) * (W_NP * 16)) = hv;
-            *reinterpret_cast<uint4*>(P + (6 * q16 + 1) * (W_NP * 16)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-            *reinterpret_cast<uint4*>(P + (6 * q16 + 2) * (W_NP * 16)) = hv;
+            *reinterpret_cast<uint4*>(P + (4 * q16) * (W_NP * 16)) = hv;
+            *reinterpret_cast<uint4*>(P + (4 * q16 + 1) * (W_NP * 16)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            *reinterpret_cast<uint4*>(P + (4 * q16 + 2) * (W_NP * 16)) = hv;
         } else {
 #pragma unroll 1
             for (int e = 0; e < 8; ++e) {
@@ -212,7 +214,7 @@ __device__ __forceinline__ void w_store_slice(unsigned char* P, const float2 (&a
                 const uint32_t lv = wi == 0 ? lw[0] : wi == 1 ? lw[1] : wi == 2 ? lw[2] : lw[3];
                 const uint16_t hb = (uint16_t)((e & 1) ? (hv >> 16) : (hv & 0xFFFFu));
                 const uint16_t lb = (uint16_t)((e & 1) ? (lv >> 16) : (lv & 0xFFFFu));
-                int kk = 32 * q16 + cd;
+                int kk = 16 * q16 + cd;  // 32 q16 + (cd - 16 q16): product 0
 #pragma unroll
                 for (int pr = 0; pr < 3; ++pr, kk += rem)
                     *reinterpret_cast<uint16_t*>(P + (kk >> 3) * (W_NP * 16) + (kk & 7) * 2) = pr == 1 ? lb : hb;
@@ -335,7 +337,8 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
                     mbar_wait(&pfull[st], (gs / W_P_STAGES) & 1u);
                     tc_fence_after();
                     mma_slice(tmem + buf * W_ACC, tmem + a_base + 8u * TC_SLICE_NS * s,
-                              umma_desc(smem_u32(sP) + st * W_STAGE, 2048, 128), idesc, slice_ns(L, s), s == 0);
+                              umma_desc(smem_u32(sP) + st * W_STAGE, 2048, 128), idesc, s < L.full ? 4 : L.q16,
+                              s < L.full ? TC_SLICE_MMA : 3 * L.q16 + L.rsteps, s == 0);
                     mma_commit_elect(&pempty[st]);
                 }
                 mma_commit_elect(&tfull[buf]);

@@ -157,8 +157,9 @@ __device__ __forceinline__ __half tcf_value(const double* row, int d, int kk, bo
 
 // Tensor-path direction operand (contract_tc.cu): u * 2^15 = hi + lo, both
 // FP16 (hi = fp16(u 2^15), lo = fp16(u 2^15 - hi), |u| <= 1), placed at the
-// three K positions of the packed split-product layout (kernels.h, tc_layout):
-// hi for products 0 and 1, lo for product 2.
+// K positions of the packed split-product layout (kernels.h, tc_layout): hi
+// and lo once each for an aligned coordinate, hi, hi, lo (products 0..2) for a
+// remainder coordinate.
 // oprow points at (block, direction) = block base + (j & 127) * 16.
 __device__ __forceinline__ void tc_split(double u, __half& h, __half& l) {
     const double v = u * 32768.0;
@@ -168,10 +169,10 @@ __device__ __forceinline__ void tc_split(double u, __half& h, __half& l) {
 __device__ __forceinline__ void put_tc_operand(unsigned char* oprow, const TcLayout& L, int c, double u) {
     __half h, l;
     tc_split(u, h, l);
-#pragma unroll
-    for (int p = 0; p < 3; ++p) {
-        const int kk = tc_pos(L, p, c);
-        *reinterpret_cast<__half*>(oprow + (kk >> 3) * 2048 + (kk & 7) * 2) = (p == 2) ? l : h;
+    const int ne = tc_entries(L, c);
+    for (int e = 0; e < ne; ++e) {
+        const int kk = tc_pos(L, e, c);
+        *reinterpret_cast<__half*>(oprow + (kk >> 3) * 2048 + (kk & 7) * 2) = tc_a_lo(L, e, c) ? l : h;
     }
 }
 
@@ -508,26 +509,26 @@ __global__ void __launch_bounds__(GV_THREADS, RRS_GEN_BLOCKS_PER_SM) cap_generat
             uint32_t w[4] = {0u, 0u, 0u, 0u};
             if (jj < nval) {
                 const double* row = val + jj * d;
-                int p, c0;
-                if (tc_chunk_run(L, cc, p, c0)) {
-                    // aligned part: one product p of 8 consecutive coordinates c0 .. c0 + 7
+                bool lo;
+                int c0;
+                if (tc_chunk_run(L, cc, lo, c0)) {
+                    // aligned part: the hi or lo terms of 8 consecutive coordinates c0 .. c0 + 7
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         __half h0, l0, h1, l1;
                         tc_split(row[c0 + 2 * e], h0, l0);
                         tc_split(row[c0 + 2 * e + 1], h1, l1);
-                        w[e] = (uint32_t)__half_as_ushort(p == 2 ? l0 : h0) |
-                               ((uint32_t)__half_as_ushort(p == 2 ? l1 : h1) << 16);
+                        w[e] = (uint32_t)__half_as_ushort(lo ? l0 : h0) | ((uint32_t)__half_as_ushort(lo ? l1 : h1) << 16);
                     }
                 } else {
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        int p, c;
-                        tc_elem(L, cc * 8 + e, p, c);
+                        int en, c;
+                        tc_elem(L, cc * 8 + e, en, c);
                         if (c >= 0) {
                             __half h, l;
                             tc_split(row[c], h, l);
-                            w[e >> 1] |= (uint32_t)__half_as_ushort(p == 2 ? l : h) << (16 * (e & 1));
+                            w[e >> 1] |= (uint32_t)__half_as_ushort(tc_a_lo(L, en, c) ? l : h) << (16 * (e & 1));
                         }
                     }
                 }
@@ -571,12 +572,12 @@ __global__ void pack_tc_operand_kernel(const double* __restrict__ u64, unsigned 
     int64_t r = idx / K;
     int j = (int)(r % (NB * 128));
     int q = (int)(r / (NB * 128));
-    int p, c;
-    tc_elem(L, kk, p, c);
+    int e, c;
+    tc_elem(L, kk, e, c);
     __half h = __double2half(0.0), l = h;
     if (c >= 0 && j < m) tc_split(u64[((size_t)q * m + j) * d + c], h, l);
     *reinterpret_cast<__half*>(uop + ((size_t)q * NB + (j >> 7)) * tc_block_bytes(d) + (size_t)(kk >> 3) * 2048 +
-                               (size_t)(j & 127) * 16 + (kk & 7) * 2) = (p == 2) ? l : h;
+                               (size_t)(j & 127) * 16 + (kk & 7) * 2) = (c >= 0 && tc_a_lo(L, e, c)) ? l : h;
 }
 
 cudaError_t launch_pack_tc_operand(const double* u64, unsigned char* uop, int Qb, int m, int NB, int d,

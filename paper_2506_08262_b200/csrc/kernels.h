@@ -82,94 +82,112 @@ struct ContractArgs {
 };
 
 // Tensor-core (FP16 hi/lo split) halfspace contraction, contract_tc.cu.
-// Packed K layout of the split products, shared by the direction operand (A,
-// written by gen.cu) and the point operand (B, written by the kernels):
-//   d = 16 Q + r.  K steps s < 3Q (16 elements each): product p = s / Q of the
-//   coordinates 16 (s % Q) .. +15;  K steps 3Q .. 3Q + R - 1, R = ceil(3r/16):
-//   element e = kk - 48 Q < 3 r is product e / r of coordinate 16 Q + e % r,
-//   the rest zero.  Products: p = 0 hi*hi, 1 hi*lo, 2 lo*hi (A value: lo for
-//   p = 2 else hi; B value: lo for p = 1 else hi), so
-//   sum_kk A[kk] B[kk] = sum_c (uh bh + uh bl + ul bh)  over ns = 3Q + R steps
-//   (d = 50: 10 MMAs instead of 3 x ceil(50/16) = 12).
-// d > 64 (contract_tcw.cu): coordinates in slices of 64; slice s < full is a
-// full slice (12 K steps: Q = 4, r = 0) at K steps [12 s, 12 s + 12), the last
-// slice (64 full .. d - 1, width 1..64) follows with its own Q / r.  For
-// d <= 64 (full = 0) this is the single-slice layout above.
+// Packed K layout of the split products.  Per 64-coordinate slice of width
+// 16 Q + r (d <= 64: the only slice), both operands store each FP16 term once:
+//   K steps [0, Q)      hi terms of coordinates 16 g .. 16 g + 15 (A: uh, B: bh)
+//   K steps [Q, 2Q)     lo terms of the same coordinates          (A: ul, B: bl)
+//   K steps [2Q, 2Q+R)  the r remainder coordinates, R = ceil(3 r / 16): element
+//                       e = kk - 32 Q < 3 r holds product e / r of coordinate
+//                       16 Q + e % r (products hi*hi, hi*lo, lo*hi: A values
+//                       h, h, l; B values h, l, h), the rest zero.
+// The MMAs of a slice pair the chunks explicitly: for g < Q the three products
+// (A g, B g) = uh bh, (A g, B Q+g) = uh bl, (A Q+g, B g) = ul bh, then
+// (A 2Q+i, B 2Q+i) for i < R, so
+//   sum = sum_c (uh bh + uh bl + ul bh)   in 3 Q + R MMAs of K = 16
+// from 2 Q + R stored K steps (d = 50: 10 MMAs over 7 steps; the A operand of a
+// direction block takes 56 TMEM columns instead of 80).
+// d > 64 (contract_tcw.cu): slices s < full are full (Q = 4, r = 0: 8 stored
+// steps, 12 MMAs) at K steps [8 s, 8 s + 8); the last slice (width 1..64)
+// follows with its own Q / r.
 // Storage: canonical K-major, no swizzle: [kk / 8][row 128][8 fp16] per
 // 128-row block, i.e. ns * 4096 bytes per block.
 struct TcLayout {
-    int q16, rem, ns;  // q16 / rem of the last slice (of d itself when d <= 64); ns: all slices
+    int q16, rem, ns;  // q16 / rem of the last slice (of d itself when d <= 64); ns: stored K steps, all slices
     int full;          // full 64-coordinate slices before the last one
+    int rsteps;        // R: remainder K steps of the last slice
+    int nmma;          // MMAs per (point tile, direction block): 12 full + 3 q16 + R
 };
 constexpr int TC_SLICE = 64;
-constexpr int TC_SLICE_NS = 12;
+constexpr int TC_SLICE_NS = 8;    // stored K steps of a full slice
+constexpr int TC_SLICE_MMA = 12;  // its MMAs
 __host__ __device__ inline TcLayout tc_layout(int d) {
     TcLayout L;
     L.full = d > 0 ? (d - 1) / TC_SLICE : 0;
     const int dl = d - TC_SLICE * L.full;
     L.q16 = dl / 16;
     L.rem = dl % 16;
-    L.ns = TC_SLICE_NS * L.full + 3 * L.q16 + (3 * L.rem + 15) / 16;
+    L.rsteps = (3 * L.rem + 15) / 16;
+    L.ns = TC_SLICE_NS * L.full + 2 * L.q16 + L.rsteps;
+    L.nmma = TC_SLICE_MMA * L.full + 3 * L.q16 + L.rsteps;
     return L;
 }
 __host__ __device__ inline int tc_block_bytes(int d) { return tc_layout(d).ns * 4096; }
-// K position of product p of coordinate c
-__host__ __device__ inline int tc_pos(const TcLayout& L, int p, int c) {
-    const int s = c / TC_SLICE;
-    if (s < L.full) {
-        const int cl = c - TC_SLICE * s;
-        return 16 * TC_SLICE_NS * s + 16 * (4 * p + cl / 16) + cl % 16;
-    }
-    const int base = 16 * TC_SLICE_NS * L.full;
-    const int cl = c - TC_SLICE * L.full;
-    return base + (cl < 16 * L.q16 ? 16 * (p * L.q16 + cl / 16) + cl % 16 : 48 * L.q16 + p * L.rem + (cl - 16 * L.q16));
+// slice of coordinate c and its (base K position, Q, r, local coordinate)
+__host__ __device__ inline void tc_slice_of(const TcLayout& L, int c, int& base, int& q, int& r, int& cl) {
+    const int s = c / TC_SLICE < L.full ? c / TC_SLICE : L.full;
+    base = 16 * TC_SLICE_NS * s;
+    cl = c - TC_SLICE * s;
+    q = s < L.full ? 4 : L.q16;
+    r = s < L.full ? 0 : L.rem;
 }
-// inverse: product p and coordinate c of K position kk (c = -1: zero padding)
-__host__ __device__ inline void tc_elem(const TcLayout& L, int kk, int& p, int& c) {
-    const int s = kk / (16 * TC_SLICE_NS);
-    if (s < L.full) {
-        const int kl = kk - 16 * TC_SLICE_NS * s;
-        const int st = kl / 16;
-        p = st / 4;
-        c = TC_SLICE * s + 16 * (st % 4) + kl % 16;
-        return;
-    }
-    const int kl = kk - 16 * TC_SLICE_NS * L.full;
-    const int c0 = TC_SLICE * L.full;
-    if (kl < 48 * L.q16) {
-        const int st = kl / 16;
-        p = st / L.q16;
-        c = c0 + 16 * (st % L.q16) + kl % 16;
+// stored terms of coordinate c: 2 in the aligned part (hi, lo), 3 in the remainder (products 0..2)
+__host__ __device__ inline int tc_entries(const TcLayout& L, int c) {
+    int base, q, r, cl;
+    tc_slice_of(L, c, base, q, r, cl);
+    return cl < 16 * q ? 2 : 3;
+}
+// K position of entry e of coordinate c
+__host__ __device__ inline int tc_pos(const TcLayout& L, int e, int c) {
+    int base, q, r, cl;
+    tc_slice_of(L, c, base, q, r, cl);
+    return base + (cl < 16 * q ? 16 * q * e + cl : 32 * q + e * r + (cl - 16 * q));
+}
+// whether entry e of coordinate c holds the lo term in A (the direction operand)
+// / in B (the point operand)
+__host__ __device__ inline bool tc_a_lo(const TcLayout& L, int e, int c) { return tc_entries(L, c) == 2 ? e == 1 : e == 2; }
+__host__ __device__ inline bool tc_b_lo(const TcLayout&, int e, int) { return e == 1; }
+// inverse: entry e and coordinate c of K position kk (c = -1: zero padding)
+__host__ __device__ inline void tc_elem(const TcLayout& L, int kk, int& e, int& c) {
+    const int s = kk / (16 * TC_SLICE_NS) < L.full ? kk / (16 * TC_SLICE_NS) : L.full;
+    const int kl = kk - 16 * TC_SLICE_NS * s;
+    const int c0 = TC_SLICE * s;
+    const int q = s < L.full ? 4 : L.q16, r = s < L.full ? 0 : L.rem;
+    if (kl < 32 * q) {
+        e = kl / (16 * q);
+        c = c0 + kl - 16 * q * e;
     } else {
-        const int e = kl - 48 * L.q16;
-        if (L.rem == 0 || e >= 3 * L.rem) {
-            p = 0;
+        const int x = kl - 32 * q;
+        if (r == 0 || x >= 3 * r) {
+            e = 0;
             c = -1;
         } else {
-            p = e / L.rem;
-            c = c0 + 16 * L.q16 + e % L.rem;
+            e = x / r;
+            c = c0 + 16 * q + x % r;
         }
     }
 }
-// 16-byte chunk cc (K positions 8 cc .. 8 cc + 7): true when it holds product p
-// of the 8 consecutive coordinates c0 .. c0 + 7 (the aligned parts of slices)
-__host__ __device__ inline bool tc_chunk_run(const TcLayout& L, int cc, int& p, int& c0) {
-    const int kk = 8 * cc;
-    const int s = kk / (16 * TC_SLICE_NS);
-    int kl, q, cbase;
-    if (s < L.full) {
-        kl = kk - 16 * TC_SLICE_NS * s;
-        q = 4;
-        cbase = TC_SLICE * s;
+// MMA i of a slice with q aligned groups (i < 3 q + R): its slice-local A and B
+// K steps -- (g, g), (g, q + g), (q + g, g) for g = i / 3, then (2q + j, 2q + j)
+__host__ __device__ inline void tc_mma_steps(int q, int i, int& sa, int& sb) {
+    if (i < 3 * q) {
+        const int g = i / 3, k = i - 3 * g;
+        sa = k == 2 ? q + g : g;
+        sb = k == 1 ? q + g : g;
     } else {
-        kl = kk - 16 * TC_SLICE_NS * L.full;
-        q = L.q16;
-        cbase = TC_SLICE * L.full;
-        if (kl >= 48 * q) return false;
+        sa = sb = 2 * q + (i - 3 * q);
     }
-    const int st = kl / 16;
-    p = st / q;
-    c0 = cbase + 16 * (st - p * q) + (kl % 16);
+}
+// 16-byte chunk cc (K positions 8 cc .. 8 cc + 7): true when it holds the hi
+// (lo = false) or lo terms of the 8 consecutive coordinates c0 .. c0 + 7 (the
+// aligned parts of the slices)
+__host__ __device__ inline bool tc_chunk_run(const TcLayout& L, int cc, bool& lo, int& c0) {
+    const int kk = 8 * cc;
+    const int s = kk / (16 * TC_SLICE_NS) < L.full ? kk / (16 * TC_SLICE_NS) : L.full;
+    const int kl = kk - 16 * TC_SLICE_NS * s;
+    const int q = s < L.full ? 4 : L.q16;
+    if (kl >= 32 * q) return false;
+    lo = kl >= 16 * q;
+    c0 = TC_SLICE * s + kl - (lo ? 16 * q : 0);
     return true;
 }
 

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "kernels.h"
 
 #include <cuda_fp16.h>
 
@@ -250,6 +251,41 @@ __device__ __forceinline__ void mma_tile_block<12>(uint32_t acc, uint32_t aT, ui
                  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+88], b11, %3, 1;\n"
                  "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
                  ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
+}
+
+// One MMA (K = 16): D (+)= A[aT] x B[bd]; `acc` nonzero accumulates into D.
+__device__ __forceinline__ void umma_f16(uint32_t d, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+                 "r"(aT), "l"(bd), "r"(idesc), "r"(acc)
+                 : "memory");
+}
+
+__device__ __forceinline__ bool elect_one() {
+    uint32_t r;
+    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\nselp.u32 %0, 1, 0, e;\n}\n" : "=r"(r));
+    return r != 0u;
+}
+
+// One (point tile, direction block) product in the split-product layout
+// (kernels.h tc_layout, one slice of Q aligned groups and R remainder steps):
+// 3 Q + R MMAs pairing A and B K steps by tc_mma_steps, the first overwriting
+// the accumulator, then the commit to `bar`; one elected thread issues all.
+//   aT: the block's A columns (K step i at +8 i); bd: descriptor of the tile's
+//   K step 0 (K step i at +256 i in descriptor units of 16 bytes)
+template <int Q, int R>
+__device__ __forceinline__ void mma_split_block(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    if (elect_one()) {
+#pragma unroll
+        for (int i = 0; i < 3 * Q + R; ++i) {
+            int sa, sb;
+            tc_mma_steps(Q, i, sa, sb);
+            umma_f16(acc, aT + 8u * (uint32_t)sa, bd + 256ull * (uint64_t)sb, idesc, i > 0 ? 1u : 0u);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                     : "memory");
+    }
+    __syncwarp();
 }
 
 // A direction block in the staging area (canonical K-major [kk/8][128][16 B]) ->
