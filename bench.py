@@ -256,7 +256,7 @@ def main():
                          "(outputs bitwise unchanged; not the default, which does the reference's full work)")
     ap.add_argument("--workspace-mb", type=int, default=0,
                     help="engine workspace cap (query batching / projection chunking), MiB; 0 = default")
-    ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "filter", "tensor3"],
+    ap.add_argument("--contract-path", default="auto", choices=["auto", "ffma", "tensor", "filter", "tensor3", "convert"],
                     help="halfspace contraction kernel (auto: the library's choice)")
     args = ap.parse_args()
     wl = args.workload
@@ -396,10 +396,11 @@ def main():
         # tcgen05 FP16-split path: executed tensor work = ns K-steps of M128 x N128 x K16 per
         # (128-point tile, 128-direction block); peak = measured dense bf16 (same rate as fp16)
         if notion == "halfspace":
-            full = (d - 1) // 64  # kernels.h tc_layout: 64-coordinate slices (d > 64: contract_tcw.cu)
+            full = (d - 1) // 64  # kernels.h tc_layout: 64-coordinate slices (d > 64: contract_tcp.cu)
             dl = d - 64 * full
-            L_ns = 12 * full + 3 * (dl // 16) + (3 * (dl % 16) + 15) // 16
-            kname, nprod = ("contract_tc_kernel" if d <= 64 else "contract_tcw_kernel"), 3
+            L_ns = 12 * full + 3 * (dl // 16) + (3 * (dl % 16) + 15) // 16  # MMAs per tile and block
+            wide = "contract_tcw_kernel" if args.contract_path == "convert" else "contract_tcp_kernel"
+            kname, nprod = ("contract_tc_kernel" if d <= 64 else wide), 3
         else:  # projection store, kernels.h Tc6Layout (contract_tcs.cu)
             L_ns = 6 * (d // 16) + (6 * (d % 16) + 15) // 16
             kname, nprod = "contract_tcs_kernel", 6

@@ -223,11 +223,13 @@ class Engine:
         _raise(load_library().rrs_engine_set_workspace_limit(self._h, int(nbytes)))
 
     def set_contract_path(self, path: str):
-        """'auto' | 'ffma' | 'tensor' | 'filter' (halfspace contraction
-        kernel; tensor = the two-term FP16 split (contract_tc.cu, d <= 64) / wide
-        split (d > 64), tensor2 = its 2-SM cta_group::2 variant, filter = filter
-        and refine, contract_tcf.cu, d <= 64)."""
-        code = {"auto": 0, "ffma": 1, "tensor": 2, "filter": 4, "tensor3": 5}[path]
+        """'auto' | 'ffma' | 'tensor' | 'filter' | 'tensor3' | 'convert'
+        (contraction kernel; tensor = the two-term FP16 split: contract_tc.cu
+        for d <= 64, the pre-split contract_tcp.cu for 64 < d <= 256; convert =
+        the same split with in-kernel converters above d = 64, contract_tcw.cu;
+        filter = filter and refine, contract_tcf.cu, d <= 64; tensor3 = the
+        three-term projection store, contract_tcs.cu)."""
+        code = {"auto": 0, "ffma": 1, "tensor": 2, "filter": 4, "tensor3": 5, "convert": 6}[path]
         _raise(load_library().rrs_engine_set_contract_path(self._h, code))
 
     def set_select_path(self, path: str):

@@ -26,6 +26,7 @@ SOURCES = {  # file -> extra flags
     "contract_tc.cu": [],
     "contract_tcf.cu": [],
     "contract_tcw.cu": [],
+    "contract_tcp.cu": [],
     "contract_tcs.cu": [],
     "select.cu": [],
     "center.cu": [],

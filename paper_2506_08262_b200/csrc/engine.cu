@@ -89,6 +89,12 @@ struct rrs_engine {
     DevBuf center, xcb, xc64, xcmax;  // xcmax: max_l |x_il - m_l| per row (wide tensor store)
     double col_ratio = 1.0;           // max / min column IQR (> 0) of the centre sample (store gating)
     DevBuf x64;  // d > 256: FP64 row-major copy of the data (contract64.cu)
+    // pre-split point operands of the converter-free wide tensor kernel
+    // (contract_tcp.cu, 64 < d <= 256), built on first use per dataset:
+    // [0] x (halfspace counts), [1] x - m (centred projection store)
+    DevBuf xps[2], pinv[2];
+    bool xps_ok[2] = {false, false};
+    DevBuf coin, coin_n, zero_d;  // coinciding-row lists per query; d zeros (halfspace shift centre)
     int64_t n = 0;
     int d = 0;
     int64_t tiles = 0;
@@ -97,7 +103,9 @@ struct rrs_engine {
     DevBuf zq0, shift;  // projection notions: zero queries for the centred store, <u, m - z> per direction
     DevBuf done, c0;    // early exit (halfspace): finished flags, coinciding-row counts per query
     // 0 auto, 1 FFMA (contract.cu), 2 tensor cores (contract_tc.cu two-term split for d <= 64,
-    // contract_tcw.cu above), 4 filter and refine (contract_tcf.cu, d <= 64); 3 (2-SM split) was removed
+    // contract_tcp.cu above), 4 filter and refine (contract_tcf.cu, d <= 64), 5 three-term tensor
+    // projection store, 6 tensor with the in-kernel converters above d = 64 (contract_tcw.cu);
+    // 3 (2-SM split) was removed
     int contract_path = 0;
     int select_path = 0;  // 0 auto (select v3 where it applies), 2 radix select v2
     DevBuf fallbacks;     // device counter of select-v3 rows that left their bracket
@@ -173,6 +181,7 @@ struct Plan {
     bool wide;     // d > 256: FP64 contraction (contract64.cu) for counts and the store
     bool tcws;     // projection store on the wide tensor kernel (contract_tcw.cu STORE, 64 < d <= 256)
     bool tcst;     // projection store on the d <= 64 tensor kernel (contract_tc.cu STORE)
+    bool tcp;      // 64 < d <= 256 on the pre-split kernel (contract_tcp.cu) instead of contract_tcw.cu
     int nb8;     // 128-direction blocks per query (tensor path operand, tc_block_bytes(d) each)
     int jchunk;  // direction blocks per store launch (projection notions)
     int tpu, chunks;
@@ -201,7 +210,7 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
     // (path 5); FP64 below n = 4096 otherwise; FFMA for the rest
     const bool proj = notion != RRS_HALFSPACE;
     const bool forced = e->contract_path == 2;
-    const bool autop = e->contract_path == 0;
+    const bool autop = e->contract_path == 0 || e->contract_path == 6;
     const bool big = e->n >= 4096;
     p.wide = e->d > TC_MAX_D;
     const bool split2 = proj && big && (forced || (autop && e->col_ratio <= 8.0));
@@ -211,6 +220,9 @@ Plan make_plan(const rrs_engine* e, int64_t Q, int m, int notion) {
             (e->contract_path == 5 || (forced && !big) ||
              (autop && big && e->d >= 32 && e->col_ratio <= 4096.0));
     p.store64 = proj && !p.tcs && !p.tcst && !p.tcws && e->n < STORE64_N;
+    // above d = 64 both the counts and the store run on the pre-split kernel
+    // (contract_tcp.cu) unless the in-kernel converters are forced (path 6)
+    p.tcp = (p.tc || p.tcws) && e->d > TC_SLICE && e->contract_path != 6;
     const int64_t d = e->d, n = e->n;
     int64_t per_q = (int64_t)m * d * 8 + (int64_t)p.mpad * tcf_dp((int)d) * 4 + (int64_t)p.mpad * 8 + (int64_t)m * 16 +
                     d * 40 + 64 +
@@ -268,6 +280,14 @@ int ensure_ws(rrs_engine* e, const Plan& p, int notion) {
     if (notion == RRS_HALFSPACE) {
         CK(e->counts.ensure(Qb * p.mpad * 2 * 4));
         CK(e->depths.ensure(8));
+        if (p.tcp) {
+            CK(e->shift.ensure(Qb * p.m * 8));
+            CK(e->coin.ensure(Qb * TCP_COIN_MAX * 4));
+            CK(e->coin_n.ensure(Qb * 4));
+            CK(e->c0.ensure(Qb * 8));
+            CK(e->zero_d.ensure(d * 8));  // (ensure keeps headroom: clear all d entries every time)
+            CK(cudaMemsetAsync(e->zero_d.p, 0, d * 8, e->stream));
+        }
     } else {
         CK(e->counts.ensure(8));
         CK(e->depths.ensure(Qb * p.m * 8));
@@ -299,7 +319,20 @@ ContractArgs contract_args(rrs_engine* e, const Plan& p, int Qb, int jb0, int jb
     return c;
 }
 
-int contract_halfspace(rrs_engine* e, const Plan& p, int Qb, const double* zdev, const int* done) {
+// pre-split point operand k (0: x for the counts, 1: x - m for the centred store),
+// built once per dataset from the tile-blocked FP32 copy and its row maxima
+int ensure_presplit(rrs_engine* e, int k) {
+    if (e->xps_ok[k]) return RRS_OK;
+    CK(e->xps[k].ensure((size_t)e->tiles * tc_block_bytes(e->d)));
+    CK(e->pinv[k].ensure((size_t)e->tiles * BM * 4));
+    CK(launch_presplit(k ? e->xcb.as<float>() : e->xb.as<float>(), k ? e->xcmax.as<float>() : e->xmax.as<float>(),
+                       e->n, e->d, e->tiles, e->xps[k].as<unsigned char>(), e->pinv[k].as<float>(), e->stream));
+    e->stats.kernel_launches++;
+    e->xps_ok[k] = true;
+    return RRS_OK;
+}
+
+int contract_halfspace(rrs_engine* e, const Plan& p, int Qb, const double* zdev, const int* done, bool use_tcp) {
     if (p.wide) {
         Contract64Args c{};
         c.x64 = e->x64.as<double>();
@@ -347,10 +380,23 @@ int contract_halfspace(rrs_engine* e, const Plan& p, int Qb, const double* zdev,
         t.mpad = p.mpad;
         t.xmax = e->xmax.as<float>();
         t.done = done;
-        if (e->d > TC_SLICE)
+        if (e->d > TC_SLICE && use_tcp) {
+            // y = acc inv_i + <u_j, 0 - z>: the per-direction shift, then the pre-split kernel
+            CK(launch_direction_shift(e->u64.as<double>(), e->zero_d.as<double>(), zdev, e->shift.as<double>(), Qb,
+                                      p.m, e->d, e->stream));
+            e->stats.kernel_launches++;
+            if (int rc = ensure_presplit(e, 0)) return rc;
+            t.xps = e->xps[0].as<unsigned char>();
+            t.pinv = e->pinv[0].as<float>();
+            t.dshift = e->shift.as<double>();
+            t.coin = e->coin.as<int>();
+            t.coin_n = e->coin_n.as<int>();
+            CK(launch_contract_tcp(t, e->sms, e->stream));
+        } else if (e->d > TC_SLICE) {
             CK(launch_contract_tcw(t, e->sms, e->stream));
-        else
+        } else {
             CK(launch_contract_tc(t, e->sms, e->stream));
+        }
         e->stats.tensor_contract_launches++;
     } else {
         ContractArgs c = contract_args(e, p, Qb, 0, p.MB);
@@ -391,8 +437,16 @@ int univariate_from_store(rrs_engine* e, const Plan& p, int Qb, int notion, cons
                 t.y = e->y.as<float>();
                 t.jb0 = jb0;
                 t.jbn = jbn;
-                if (p.tcst) CK(launch_contract_tc_store(t, e->sms, e->stream));
-                else CK(launch_contract_tcw_store(t, e->sms, e->stream));
+                if (p.tcst) {
+                    CK(launch_contract_tc_store(t, e->sms, e->stream));
+                } else if (p.tcp) {
+                    if (int rc = ensure_presplit(e, 1)) return rc;
+                    t.xps = e->xps[1].as<unsigned char>();
+                    t.pinv = e->pinv[1].as<float>();
+                    CK(launch_contract_tcp_store(t, e->sms, e->stream));
+                } else {
+                    CK(launch_contract_tcw_store(t, e->sms, e->stream));
+                }
                 e->stats.tensor_contract_launches++;
             } else if (p.wide && !p.store64) {
                 Contract64Args c{};
@@ -508,6 +562,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
     const int d = e->d;
     // early exit (halfspace; not on the experimental 2-SM / filter kernels)
     const bool early = cfg->notion == RRS_HALFSPACE && cfg->early_exit != 0 && !p.tcf;
+    const bool tcp_counts = cfg->notion == RRS_HALFSPACE && p.tc && p.tcp;
     int* done = nullptr;
     long long* c0 = nullptr;
     if (early) {
@@ -516,13 +571,32 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
         done = e->done.as<int>();
         c0 = e->c0.as<long long>();
     }
+    std::vector<int> coin_n_host;
     for (int64_t b0 = 0; b0 < Q; b0 += p.Qb) {
         const int Qb = (int)((Q - b0) < p.Qb ? (Q - b0) : p.Qb);
         CK(launch_queries_to_f32(zdev + b0 * d, e->zq.as<float>(), (int64_t)Qb * d, e->stream));
+        // the pre-split kernel excludes the rows coinciding with each query by index; a
+        // query with more than TCP_COIN_MAX of them sends its batch to the converter kernel
+        bool use_tcp = false;
+        if (tcp_counts) {
+            CK(launch_coincide_list32(e->xb.as<float>(), e->zq.as<float>(), e->n, d, e->tiles, Qb,
+                                      e->c0.as<long long>(), e->coin.as<int>(), e->coin_n.as<int>(), e->stream));
+            e->stats.kernel_launches += 1;
+            coin_n_host.resize((size_t)Qb);
+            CK(cudaMemcpyAsync(coin_n_host.data(), e->coin_n.p, (size_t)Qb * 4, cudaMemcpyDeviceToHost, e->stream));
+            CK(cudaStreamSynchronize(e->stream));
+            use_tcp = true;
+            for (int v : coin_n_host) use_tcp = use_tcp && v <= TCP_COIN_MAX;
+        }
         if (early) {
             CK(cudaMemsetAsync(done, 0, (size_t)Qb * 4, e->stream));
-            if (p.wide) CK(launch_coincide_count64(e->x64.as<double>(), zdev + b0 * d, e->n, d, Qb, c0, e->stream));
-            else CK(launch_coincide_count32(e->xb.as<float>(), e->zq.as<float>(), e->n, d, e->tiles, Qb, c0, e->stream));
+            if (tcp_counts) {
+                // c0 came with the lists (the same FP32 equality as launch_coincide_count32)
+            } else if (p.wide) {
+                CK(launch_coincide_count64(e->x64.as<double>(), zdev + b0 * d, e->n, d, Qb, c0, e->stream));
+            } else {
+                CK(launch_coincide_count32(e->xb.as<float>(), e->zq.as<float>(), e->n, d, e->tiles, Qb, c0, e->stream));
+            }
             e->stats.kernel_launches += 1;
         }
         StateArgs s{e->pole.as<double>(), e->reflv.as<double>(), e->reflmode.as<int>(),
@@ -561,7 +635,7 @@ int run_batches(rrs_engine* e, const double* zdev, int64_t Q, int64_t q0, const 
             }
             if (cfg->notion == RRS_HALFSPACE) {
                 Timer t(e, 1);
-                if (int rc = contract_halfspace(e, p, Qb, zdev + b0 * d, done)) return rc;
+                if (int rc = contract_halfspace(e, p, Qb, zdev + b0 * d, done, use_tcp)) return rc;
                 e->stats.kernel_launches++;
                 e->stats.contract_launches++;
             } else {
@@ -677,7 +751,8 @@ int rrs_engine_destroy(rrs_engine* e) {
     for (DevBuf* b : {&e->xb, &e->xmax, &e->zq, &e->u64, &e->u32, &e->uop, &e->counts, &e->depths, &e->y, &e->pole,
                       &e->reflv, &e->reflmode, &e->dmin, &e->bestcnt, &e->tmp_in, &e->tmp_out0,
                       &e->tmp_out1, &e->tmp_out2, &e->tmp_out3, &e->center, &e->xcb, &e->xc64, &e->zq0,
-                      &e->shift, &e->fallbacks, &e->x64, &e->done, &e->c0, &e->xcmax})
+                      &e->shift, &e->fallbacks, &e->x64, &e->done, &e->c0, &e->xcmax, &e->xps[0], &e->xps[1],
+                      &e->pinv[0], &e->pinv[1], &e->coin, &e->coin_n, &e->zero_d})
         b->release();
     for (auto ev : e->ev_pool) cudaEventDestroy(ev);
     if (e->own) cudaStreamDestroy(e->own);
@@ -707,10 +782,11 @@ int rrs_engine_set_workspace_limit(rrs_engine* e, int64_t bytes) {
 
 int rrs_engine_set_contract_path(rrs_engine* e, int32_t path) {
     if (!e) return fail(RRS_ERR_INVALID, "engine is null");
-    if (path < 0 || path > 5 || path == 3)
+    if (path < 0 || path > 6 || path == 3)
         return fail(RRS_ERR_INVALID,
-                    "contract path must be 0 (auto), 1 (FFMA), 2 (tensor), 4 (filter and refine) or 5 (three-term "
-                    "tensor projection store); 3 (the 2-SM split kernel) was removed");
+                    "contract path must be 0 (auto), 1 (FFMA), 2 (tensor), 4 (filter and refine), 5 (three-term "
+                    "tensor projection store) or 6 (tensor with in-kernel converters above d = 64); 3 (the 2-SM "
+                    "split kernel) was removed");
     e->contract_path = path;
     return RRS_OK;
 }
@@ -814,6 +890,7 @@ static int set_dataset_common(rrs_engine* e, const double* xdev, int64_t n, int3
     e->n = n;
     e->d = d;
     e->tiles = tiles;
+    e->xps_ok[0] = e->xps_ok[1] = false;
     return RRS_OK;
 }
 
@@ -925,7 +1002,16 @@ int rrs_evaluate_directions_host(rrs_engine* e, const double* z, const double* U
         CK(launch_pack_tc_operand(e->u64.as<double>(), e->uop.as<unsigned char>(), 1, m, p.nb8, d, e->stream));
     if (notion == RRS_HALFSPACE) {
         CK(cudaMemsetAsync(e->counts.p, 0, (size_t)p.mpad * 2 * 4, e->stream));
-        if (int rc = contract_halfspace(e, p, 1, e->tmp_in.as<double>(), nullptr)) return rc;
+        bool use_tcp = false;
+        if (p.tc && p.tcp) {
+            CK(launch_coincide_list32(e->xb.as<float>(), e->zq.as<float>(), e->n, d, e->tiles, 1,
+                                      e->c0.as<long long>(), e->coin.as<int>(), e->coin_n.as<int>(), e->stream));
+            int cn = 0;
+            CK(cudaMemcpyAsync(&cn, e->coin_n.p, 4, cudaMemcpyDeviceToHost, e->stream));
+            CK(cudaStreamSynchronize(e->stream));
+            use_tcp = cn <= TCP_COIN_MAX;
+        }
+        if (int rc = contract_halfspace(e, p, 1, e->tmp_in.as<double>(), nullptr, use_tcp)) return rc;
         std::vector<int> cnt((size_t)p.mpad * 2);
         CK(cudaMemcpyAsync(cnt.data(), e->counts.p, cnt.size() * 4, cudaMemcpyDeviceToHost, e->stream));
         CK(cudaStreamSynchronize(e->stream));

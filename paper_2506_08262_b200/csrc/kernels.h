@@ -262,7 +262,17 @@ struct TcArgs {
     // blocks [jb0, jb0 + jbn) of each query, rows y[q][(blk - jb0) * 128 + j][n]
     float* y;
     int jb0, jbn;
+    // pre-split point operand (contract_tcp.cu): [T][ns][128][8 fp16] B operand of
+    // every tile in the tc_layout, per-point 1 / (s_i 2^15); count mode adds the
+    // per-direction shift (FP64 [Qb][m], y = acc inv_i + shift_j) and excludes the
+    // rows coinciding with the query (coin[q][0 .. coin_n[q]), coin_n <= TCP_COIN_MAX)
+    const unsigned char* xps;
+    const float* pinv;
+    const double* dshift;
+    const int* coin;
+    const int* coin_n;
 };
+constexpr int TCP_COIN_MAX = 64;  // coinciding rows listed per query (more: the converter kernel)
 
 // Filter-and-refine halfspace contraction (contract_tcf.cu, d <= 64): one FP16
 // product per coordinate, K = d + 1.  Direction operand A (written by gen.cu):
@@ -361,6 +371,15 @@ cudaError_t launch_contract_tcf(TcfArgs a, int sms, cudaStream_t st);  // filter
 cudaError_t launch_pack_tcf_operand(const double* u64, unsigned char* uop, float* u32r, int Qb, int m, int NB,
                                     int mpad, int d, cudaStream_t st);
 cudaError_t launch_contract_tcw(TcArgs a, int sms, cudaStream_t st);
+// converter-free wide tensor kernel (contract_tcp.cu, 64 < d <= 256): counts / centred store
+cudaError_t launch_contract_tcp(TcArgs a, int sms, cudaStream_t st);
+cudaError_t launch_contract_tcp_store(TcArgs a, int sms, cudaStream_t st);
+// pre-split point operand from a tile-blocked FP32 copy and its per-row max |x|
+cudaError_t launch_presplit(const float* xb, const float* rowmax, int64_t n, int d, int64_t tiles,
+                            unsigned char* xps, float* pinv, cudaStream_t st);
+// rows FP32-equal to each query: count (c0, int64) and the first TCP_COIN_MAX indices
+cudaError_t launch_coincide_list32(const float* xb, const float* zq, int64_t n, int d, int64_t tiles, int Qb,
+                                   long long* c0, int* coin, int* coin_n, cudaStream_t st);
 cudaError_t launch_contract_tcw_store(TcArgs a, int sms, cudaStream_t st);  // centred projection store, 64 < d <= 256
 cudaError_t launch_contract_tc_store(TcArgs a, int sms, cudaStream_t st);   // centred projection store, d <= 64
 bool contract_tc_store_fits(int d);  // its shared-memory layout leaves >= 2 raw-tile stages  // 64 < d <= 256 (contract_tcw.cu)
