@@ -200,17 +200,11 @@ __global__ void __launch_bounds__(P_THREADS, 1) contract_tcp_kernel(const TcArgs
                     const uint32_t st = gs % P_STAGES;
                     mbar_wait(&pfull[st], (gs / P_STAGES) & 1u);
                     tc_fence_after();
-                    const int q = s < L.full ? 4 : L.q16;
-                    const int nm = s < L.full ? TC_SLICE_MMA : 3 * L.q16 + L.rsteps;
                     const uint32_t aT = tmem + a_base + 8u * TC_SLICE_NS * s;
                     const uint64_t bd = umma_desc(smem_u32(sP) + st * P_STAGE, 2048, 128);
                     if (elect_one()) {
-                        for (int i = 0; i < nm; ++i) {
-                            int sa, sb;
-                            tc_mma_steps(q, i, sa, sb);
-                            umma_f16(tmem + buf * P_ACC, aT + 8u * (uint32_t)sa, bd + 256ull * (uint64_t)sb, idesc,
-                                     (s == 0 && i == 0) ? 0u : 1u);
-                        }
+                        if (s < L.full) mma_split_seq<4, 0>(tmem + buf * P_ACC, aT, bd, idesc, s == 0 ? 0u : 1u);
+                        else mma_split_seq_rt(L.q16, L.rsteps, tmem + buf * P_ACC, aT, bd, idesc, s == 0 ? 0u : 1u);
                     }
                     __syncwarp();
                     mma_commit_elect(&pempty[st]);

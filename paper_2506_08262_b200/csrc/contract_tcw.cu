@@ -128,11 +128,8 @@ __device__ __forceinline__ int slice_ns(const TcLayout& L, int s) {
 __device__ __forceinline__ void mma_slice(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, int q, int nm,
                                           bool first) {
     if (elect_one()) {
-        for (int i = 0; i < nm; ++i) {
-            int sa, sb;
-            tc_mma_steps(q, i, sa, sb);
-            umma_f16(acc, aT + 8u * (uint32_t)sa, bd + 256ull * (uint64_t)sb, idesc, (first && i == 0) ? 0u : 1u);
-        }
+        if (nm == TC_SLICE_MMA) mma_split_seq<4, 0>(acc, aT, bd, idesc, first ? 0u : 1u);
+        else mma_split_seq_rt(q, nm - 3 * q, acc, aT, bd, idesc, first ? 0u : 1u);
     }
     __syncwarp();
 }

@@ -267,21 +267,51 @@ __device__ __forceinline__ bool elect_one() {
     return r != 0u;
 }
 
-// One (point tile, direction block) product in the split-product layout
-// (kernels.h tc_layout, one slice of Q aligned groups and R remainder steps):
-// 3 Q + R MMAs pairing A and B K steps by tc_mma_steps, the first overwriting
-// the accumulator, then the commit to `bar`; one elected thread issues all.
-//   aT: the block's A columns (K step i at +8 i); bd: descriptor of the tile's
-//   K step 0 (K step i at +256 i in descriptor units of 16 bytes)
+// The 3 Q + R MMAs of one slice in the split-product layout (kernels.h
+// tc_layout: Q aligned groups, R remainder steps), A / B K steps paired by
+// tc_mma_steps; the first accumulates iff acc0.  Issued by the calling thread
+// (the caller elects), fully unrolled so every operand offset is an immediate.
+//   aT: the slice's A columns (K step i at +8 i); bd: descriptor of the slice's
+//   B K step 0 (K step i at +256 i in descriptor units of 16 bytes)
+template <int Q, int R>
+__device__ __forceinline__ void mma_split_seq(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t acc0) {
+#pragma unroll
+    for (int i = 0; i < 3 * Q + R; ++i) {
+        int sa, sb;
+        tc_mma_steps(Q, i, sa, sb);
+        umma_f16(acc, aT + 8u * (uint32_t)sa, bd + 256ull * (uint64_t)sb, idesc, i == 0 ? acc0 : 1u);
+    }
+}
+
+// runtime (Q, R) -> the unrolled sequence (Q <= 4, R <= 3; Q = 4 has R = 0)
+__device__ __forceinline__ void mma_split_seq_rt(int q, int r, uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc,
+                                                 uint32_t acc0) {
+    switch (4 * q + r) {
+        case 1: mma_split_seq<0, 1>(acc, aT, bd, idesc, acc0); break;
+        case 2: mma_split_seq<0, 2>(acc, aT, bd, idesc, acc0); break;
+        case 3: mma_split_seq<0, 3>(acc, aT, bd, idesc, acc0); break;
+        case 4: mma_split_seq<1, 0>(acc, aT, bd, idesc, acc0); break;
+        case 5: mma_split_seq<1, 1>(acc, aT, bd, idesc, acc0); break;
+        case 6: mma_split_seq<1, 2>(acc, aT, bd, idesc, acc0); break;
+        case 7: mma_split_seq<1, 3>(acc, aT, bd, idesc, acc0); break;
+        case 8: mma_split_seq<2, 0>(acc, aT, bd, idesc, acc0); break;
+        case 9: mma_split_seq<2, 1>(acc, aT, bd, idesc, acc0); break;
+        case 10: mma_split_seq<2, 2>(acc, aT, bd, idesc, acc0); break;
+        case 11: mma_split_seq<2, 3>(acc, aT, bd, idesc, acc0); break;
+        case 12: mma_split_seq<3, 0>(acc, aT, bd, idesc, acc0); break;
+        case 13: mma_split_seq<3, 1>(acc, aT, bd, idesc, acc0); break;
+        case 14: mma_split_seq<3, 2>(acc, aT, bd, idesc, acc0); break;
+        case 15: mma_split_seq<3, 3>(acc, aT, bd, idesc, acc0); break;
+        default: mma_split_seq<4, 0>(acc, aT, bd, idesc, acc0); break;
+    }
+}
+
+// One (point tile, direction block) product of a single slice (d <= 64), then
+// the commit to `bar`; one elected thread issues all.
 template <int Q, int R>
 __device__ __forceinline__ void mma_split_block(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
     if (elect_one()) {
-#pragma unroll
-        for (int i = 0; i < 3 * Q + R; ++i) {
-            int sa, sb;
-            tc_mma_steps(Q, i, sa, sb);
-            umma_f16(acc, aT + 8u * (uint32_t)sa, bd + 256ull * (uint64_t)sb, idesc, i > 0 ? 1u : 0u);
-        }
+        mma_split_seq<Q, R>(acc, aT, bd, idesc, 0u);
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                      : "memory");
     }
