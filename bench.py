@@ -69,6 +69,19 @@ def measured_peaks() -> dict:
     return {}
 
 
+def store_split2(X) -> bool:
+    """Whether the engine's auto plan takes the two-term split store for d <= 64
+    (engine.cu make_plan: column IQR ratio <= 8 over the centre sample of
+    center_sample_kernel: min(n, 1024) rows at strided positions)."""
+    n = X.shape[0]
+    S = min(n, 1024)
+    rows = ((2 * np.arange(S) + 1) * n) // (2 * S)
+    s = np.sort(X[rows], axis=0)
+    iqr = s[min((3 * S) // 4, S - 1)] - s[S // 4]
+    iqr = iqr[iqr > 0]
+    return iqr.size == 0 or float(iqr.max() / iqr.min()) <= 8.0
+
+
 def profile_traffic(workload: str):
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
@@ -401,7 +414,13 @@ def main():
             L_ns = 12 * full + 3 * (dl // 16) + (3 * (dl % 16) + 15) // 16  # MMAs per tile and block
             wide = "contract_tcw_kernel" if args.contract_path == "convert" else "contract_tcp_kernel"
             kname, nprod = ("contract_tc_kernel" if d <= 64 else wide), 3
-        else:  # projection store, kernels.h Tc6Layout (contract_tcs.cu)
+        elif d > 64 or store_split2(X):  # two-term split store (contract_tc / contract_tcp STORE)
+            full = (d - 1) // 64
+            dl = d - 64 * full
+            L_ns = 12 * full + 3 * (dl // 16) + (3 * (dl % 16) + 15) // 16
+            wide = "contract_tcw_kernel<STORE>" if args.contract_path == "convert" else "contract_tcp_kernel<STORE>"
+            kname, nprod = ("contract_tc_kernel<STORE>" if d <= 64 else wide), 3
+        else:  # projection store, kernels.h Tc6Layout (contract_tcs.cu): column-heterogeneous data
             L_ns = 6 * (d // 16) + (6 * (d % 16) + 15) // 16
             kname, nprod = "contract_tcs_kernel", 6
         tiles, blocks = -(-n // 128), -(-m // 128)
@@ -438,7 +457,9 @@ def main():
                     "kernel": ("select_v2_kernel<256|512|1024, smem>" if args.select_path == "radix"
                                else "select_v3_kernel<256>" if n <= 16384
                                else "select_v3_kernel<512|1024>") if 2048 <= n <= 53248
-                    else "select_v2_kernel<1024, global>" if n % 4 == 0 else "select_kernel",
+                    else ("select_v5_kernel<1024, 8192>" if args.select_path != "radix" else
+                          "select_v2_kernel<1024, global>") if n > 53248 and n % 4 == 0
+                    else "select_v2_kernel<smem>" if n < 2048 else "select_kernel",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "nominal 8 TB/s",
                     "achieved_is": "algorithmic bytes (the stored projections, 4 n per direction) / select time",
                     "kernel_share_of_step": select_ms / ms if ms else None,

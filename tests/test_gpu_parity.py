@@ -325,11 +325,11 @@ def test_tensor_layout_dims(b200, d):
 
 @pytest.mark.parametrize("d", [65, 72, 100, 128, 129, 150, 200, 256])
 def test_tensor_wide_dims(b200, d):
-    """The wide tensor path (contract_tcw.cu, 64 < d <= 256: 64-coordinate
-    slices, bound-based per-point scale, one or two accumulator buffers)
-    against FP64 within the tie zone and against the FFMA kernel, with a
-    near-duplicate query, an in-sample query (self tie) and heterogeneous
-    coordinate scales; n not a multiple of the tile, m not of the block."""
+    """The wide tensor path (64 < d <= 256: the pre-split contract_tcp.cu by
+    default, 64-coordinate slices, one or two accumulator buffers) against FP64
+    within the tie zone and against the FFMA kernel, with a near-duplicate
+    query, an in-sample query (self tie) and heterogeneous coordinate scales;
+    n not a multiple of the tile, m not of the block."""
     rng = np.random.default_rng(300 + d)
     X = rng.standard_normal((4096 + 77, d)) * rng.uniform(0.1, 10.0, size=d)
     U = rng.standard_normal((200, d))
@@ -348,6 +348,50 @@ def test_tensor_wide_dims(b200, d):
         assert np.all(np.abs(cle - fle) <= T) and np.all(np.abs(cge - fge) <= T), d
 
 
+@pytest.mark.parametrize("d", [80, 200])
+def test_presplit_vs_converter(b200, d):
+    """The pre-split wide kernel (contract_tcp.cu: query applied in the epilogue
+    as y = acc inv_i + <u, -z>, coinciding rows excluded by index) against FP64
+    and against the converter kernel (contract_path 'convert', contract_tcw.cu)
+    on the cases the index exclusion and the epilogue shift must get right:
+    a query with 3 duplicated rows, one with more duplicates than the list
+    holds (TCP_COIN_MAX = 64: the batch goes to the converter kernel), a far
+    query, an all-zero query against data containing zero rows, and data far
+    from the origin."""
+    rng = np.random.default_rng(500 + d)
+    n = 5000 + 33
+    base = rng.standard_normal((n, d))
+    cases = []
+    X = base.copy()
+    X[10:13] = X[7]  # X[7] occurs 4 times
+    cases.append((X, X[7]))
+    X = base.copy()
+    X[100:170] = X[99]  # 71 copies: past the coinciding-row list
+    cases.append((X, X[99]))
+    cases.append((base, base[3] + 1e3))
+    X = base.copy()
+    X[20:25] = 0.0
+    cases.append((X, np.zeros(d)))
+    X = base + 500.0
+    cases.append((X, X[11]))
+    U = rng.standard_normal((300, d))
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    for X, z in cases:
+        data = b200.Dataset(X)
+        with contract_path(b200, "tensor"):
+            _, cle, cge = b200.evaluate_directions_counts(z, data, U)
+        with contract_path(b200, "convert"):
+            _, vle, vge = b200.evaluate_directions_counts(z, data, U)
+        y = X @ U.T - (U @ z)[None, :]
+        xn = np.linalg.norm(X, axis=1)
+        T = (np.abs(y) < TIE_REL * np.maximum(xn, np.linalg.norm(z))[:, None]).sum(axis=0)
+        exact = np.all(X == z[None, :], axis=1).sum()  # rows coinciding with z: ties on both sides
+        rle, rge = (y <= 0).sum(axis=0), (y >= 0).sum(axis=0)
+        assert np.all(cle >= exact) and np.all(cge >= exact)
+        assert np.all(np.abs(cle - rle) <= T) and np.all(np.abs(cge - rge) <= T)
+        assert np.all(np.abs(cle - vle) <= T) and np.all(np.abs(cge - vge) <= T)
+
+
 def test_tensor_wide_rrs_matches_ffma(b200):
     """Full RRS at d = 200 (wide tensor path) against the FFMA path: identical
     depths unless a count sits in the tie zone (Kendall tau over queries)."""
@@ -359,7 +403,10 @@ def test_tensor_wide_rrs_matches_ffma(b200):
         dt = b200.depth_batch_arrays(X[:24], data, cfg)[0]
     with contract_path(b200, "ffma"):
         df = b200.depth_batch_arrays(X[:24], data, cfg)[0]
+    with contract_path(b200, "convert"):
+        dc = b200.depth_batch_arrays(X[:24], data, cfg)[0]
     assert np.mean(dt == df) >= 0.9 and kendalltau(dt, df)[0] >= 0.95
+    assert np.mean(dt == dc) >= 0.9 and kendalltau(dt, dc)[0] >= 0.95
 
 
 @pytest.mark.parametrize("notion", ["projection", "asym_projection"])
@@ -444,8 +491,9 @@ def test_dataset_validation_on_device(b200):
                                    (20_000, 256, "gaussian"), (12_000, 64, "cauchy")])
 def test_tensor_store_projection_depths(b200, notion, shape, store):
     """The tensor-core projection stores of the centred frame: "tensor" = the
-    two-term FP16 split (contract_tc.cu STORE for d <= 64, contract_tcw.cu
-    STORE above; round 1's uncentred frame lost 1e-5 with it on Cauchy rows),
+    two-term FP16 split (contract_tc.cu STORE for d <= 64, the pre-split
+    contract_tcp.cu STORE above; round 1's uncentred frame lost 1e-5 with it on
+    Cauchy rows),
     "tensor3" = the three-term split (contract_tcs.cu, d <= 50): per-direction
     D_P / D_AP against the FP64 oracle to the north_star's 1e-5 relative, at the
     config-2 / config-3 shapes, odd n and d, far queries, shared-memory and
@@ -514,7 +562,7 @@ def test_store_direction_chunks_bitwise(b200, path):
 @pytest.mark.parametrize("d", [20, 90, 200])
 def test_tensor_paths_tiny_n(b200, n, d):
     """Tensor paths forced on tiny datasets (one partly padded tile, a single
-    point): halfspace counts (contract_tc / contract_tcw) exact against FP64
+    point): halfspace counts (contract_tc / contract_tcp) exact against FP64
     outside the tie zone, projection depths (contract_tcs for d <= 50, FFMA
     store above) against the oracle."""
     from oracle import oracle
@@ -569,7 +617,8 @@ def test_wide_dimensions(b200, d):
     assert np.array_equal(dg, dr), (dg, dr)
 
 
-@pytest.mark.parametrize("case", ["tensor_d50", "tensor_d80", "ffma_small_n", "wide_d300", "ffma_forced"])
+@pytest.mark.parametrize("case", ["tensor_d50", "tensor_d80", "tensor_d200", "convert_d120", "ffma_small_n",
+                                  "wide_d300", "ffma_forced"])
 def test_early_exit_bitwise(b200, case):
     """RrsConfig(early_exit=True): a query stops once its best count equals the
     rows coinciding with it (the strict-< update, optimizer.py:202, can never
@@ -579,6 +628,7 @@ def test_early_exit_bitwise(b200, case):
     from paper_2506_08262_b200.synthetic import toeplitz_gaussian
 
     n, d, path = {"tensor_d50": (20000, 50, "auto"), "tensor_d80": (8000, 80, "auto"),
+                  "tensor_d200": (6000, 200, "auto"), "convert_d120": (6000, 120, "convert"),
                   "ffma_small_n": (3000, 6, "auto"), "wide_d300": (3000, 300, "auto"),
                   "ffma_forced": (6000, 12, "ffma")}[case]
     X = toeplitz_gaussian(d, n, seed=9)
