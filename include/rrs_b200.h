@@ -150,12 +150,13 @@ int rrs_depth_of_projections_host(rrs_engine* e, int32_t notion, const double* p
 int rrs_philox4x32_host(rrs_engine* e, const uint32_t* ctr, int64_t N, uint32_t key0,
                         uint32_t key1, uint32_t* out);
 
-/* Halfspace contraction kernel: 0 = auto (tensor cores when d <= 256 and
- * n >= 4096), 1 = FP32 FFMA (contract.cu), 2 = tcgen05 FP16 hi/lo split with
- * FP32 accumulation (contract_tc.cu for d <= 64, contract_tcw.cu for
- * 64 < d <= 256), 4 = filter and refine
- * (contract_tcf.cu, d <= 64).  Any d > 256 (up to 1024) takes the FP64
- * contraction (contract64.cu) whatever the path. */
+/* Contraction kernel: 0 = auto (tensor cores when d <= 256 and n >= 4096),
+ * 1 = FP32 FFMA (contract.cu), 2 = tcgen05 FP16 hi/lo split with FP32
+ * accumulation (contract_tc.cu for d <= 64, the pre-split contract_tcp.cu for
+ * 64 < d <= 256), 4 = filter and refine (contract_tcf.cu, d <= 64), 5 = the
+ * three-term tensor projection store (contract_tcs.cu), 6 = as 0 but with the
+ * in-kernel converters above d = 64 (contract_tcw.cu).  Any d > 256 (up to
+ * 1024) takes the FP64 contraction (contract64.cu) whatever the path. */
 int rrs_engine_set_contract_path(rrs_engine* e, int32_t path);
 
 /* Page-locked host buffers (cudaHostAlloc, portable): the matrix loaders
