@@ -75,7 +75,7 @@ def store_split2(X) -> bool:
     center_sample_kernel: min(n, 1024) rows at strided positions)."""
     n = X.shape[0]
     S = min(n, 1024)
-    rows = ((2 * np.arange(S) + 1) * n) // (2 * S)
+    rows = ((4 * np.arange(S) + 1) * n) // (4 * S)
     s = np.sort(X[rows], axis=0)
     iqr = s[min((3 * S) // 4, S - 1)] - s[S // 4]
     iqr = iqr[iqr > 0]

@@ -25,13 +25,15 @@ namespace rrs {
 constexpr int CENTER_S = 1024;
 
 // m_c = lower median of column c over min(n, 1024) rows at strided positions
+// (4i + 1) n / 4S -- offset from the select kernels' sample positions
+// (2i + 1) n / 2S, so one crafted set of rows cannot bias both
 __global__ void __launch_bounds__(512) center_sample_kernel(const double* __restrict__ x, int64_t n, int d,
                                                             double* __restrict__ center, double* __restrict__ iqr) {
     __shared__ double s[CENTER_S];
     const int c = blockIdx.x;
     const int S = n >= CENTER_S ? CENTER_S : (int)n;
     for (int i = threadIdx.x; i < CENTER_S; i += blockDim.x)
-        s[i] = i < S ? x[(((int64_t)(2 * i + 1) * n) / (2 * S)) * d + c] : INFINITY;
+        s[i] = i < S ? x[(((int64_t)(4 * i + 1) * n) / (4 * S)) * d + c] : INFINITY;
     __syncthreads();
     for (int k = 2; k <= CENTER_S; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {

@@ -48,10 +48,10 @@ def _row(kind, n, rng):
         v[: n // 2 + 1] = 0.0
         return rng.permutation(v)
     if kind == "sample_trap":
-        # the strided sample positions of the kernel ((2s+1)n / 2S, S = 256 or
-        # 512) hold huge values: the sample bracket misses the median
+        # the strided sample positions of the kernel ((2s+1)n / 2S, S = 256,
+        # 512 or 1024) hold huge values: the sample bracket misses the median
         v = rng.standard_normal(n)
-        for S in (256, 512):
+        for S in (256, 512, 1024):
             v[((2 * np.arange(S) + 1) * n) // (2 * S)] = 1e6 + np.arange(S)
         return v
     if kind == "periodic":
