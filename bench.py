@@ -329,15 +329,9 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    eng.enable_timing(True)
     clocks = ClockSampler(local)
     clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    launches = 0
-    contract_ms = 0.0
-    contract_launches = 0
-    tensor_launches = 0
-    select_ms = 0.0
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -347,18 +341,36 @@ def main():
         ev[i][0].record(stream)
         recs.append(run_step(args.warmup + i))
         ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    # stage breakdown (kernel launches, contraction / select event times) from a
+    # second pass over the same steps with the engine's per-stage events on --
+    # outside the timed region: the event records and the per-step stats sync
+    # would otherwise slow launch-bound configurations (config 1)
+    eng.enable_timing(True)
+    launches = 0
+    contract_ms = 0.0
+    contract_launches = 0
+    tensor_launches = 0
+    select_ms = 0.0
+    stage_ms = 0.0
+    for i in range(args.steps):
+        flush.zero_()
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record(stream)
+        run_step(args.warmup + i)
+        b_ev.record(stream)
         st = eng.stats()  # syncs; per-kernel event times of this step
+        stage_ms += a_ev.elapsed_time(b_ev)
         launches += st["kernel_launches"]
         contract_ms += st["ms_contract_total"]
         contract_launches += st["contract_launches"]
         tensor_launches += st["tensor_contract_launches"]
         select_ms += st["ms_univariate"]
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    eng.enable_timing(False)
-    ms = sum(a.elapsed_time(b) for a, b in ev)
+    eng.enable_timing(False)  # kernel shares below: against this pass's own step time
     t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -377,15 +389,15 @@ def main():
         run_step(0)  # warm-up of the early-exit variant
         torch.cuda.synchronize()
         ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        same = True
+        recs2 = []
         for i in range(args.steps):
             flush.zero_()
             ev2[i][0].record(stream)
-            rec = run_step(args.warmup + i)
+            recs2.append(run_step(args.warmup + i))
             ev2[i][1].record(stream)
-            same = same and bool(torch.equal(rec, recs[i]))
         torch.cuda.synchronize()
         ms2 = sum(a.elapsed_time(b) for a, b in ev2)
+        same = all(bool(torch.equal(x, y)) for x, y in zip(recs2, recs))  # after the timed steps
         t2 = torch.tensor([ms2, 0.0 if same else 1.0], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
@@ -444,7 +456,7 @@ def main():
                     "peak_source": "nominal FP32 FFMA (148 SMs x 128 lanes x 2 x 1.965 GHz); MEASURED_PEAKS.json "
                                    "has no FP32 entry"}
     roofline.update({"flops_per_launch": flops_per_launch, "avg_launch_ms": avg_launch_ms,
-                     "kernel_share_of_step": contract_ms / ms if ms else None,
+                     "kernel_share_of_step": contract_ms / stage_ms if stage_ms else None,
                      "hbm_peak_measured_gbs": peaks.get("hbm_gbs")})
     if notion != "halfspace" and select_ms > contract_ms:
         # the univariate stage dominates: report its roofline, HBM-bound on reading every stored
@@ -462,7 +474,7 @@ def main():
                     else "select_v2_kernel<smem>" if n < 2048 else "select_kernel",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "nominal 8 TB/s",
                     "achieved_is": "algorithmic bytes (the stored projections, 4 n per direction) / select time",
-                    "kernel_share_of_step": select_ms / ms if ms else None,
+                    "kernel_share_of_step": select_ms / stage_ms if stage_ms else None,
                     "contraction": roofline}
 
     # e2e through the public API with host buffers (H2D of data + queries, D2H of results)
