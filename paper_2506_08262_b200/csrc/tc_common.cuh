@@ -16,243 +16,6 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
            ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
 }
 
-// One (point tile, direction block) product: NS MMAs of K = 16 along the packed
-// split-product K axis, then the commit to the accumulator-full barrier, all
-// under one elect with immediate operand offsets (ptxas keeps the sequence on
-// the uniform datapath).
-//   acc: accumulator columns; aT: the block's A columns (K step i at +8 i)
-//   bd : descriptor of the tile's K step 0 (K step i at +4096 i bytes = +256 i)
-template <int NS>
-__device__ __forceinline__ void mma_tile_block(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar);
-
-template <>
-__device__ __forceinline__ void mma_tile_block<1>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<2>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<3>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<4>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<5>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<6>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<7>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "add.s64 b6, %2, 1536;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<8>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "add.s64 b6, %2, 1536;\n"
-                 "add.s64 b7, %2, 1792;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<9>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7, b8;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "add.s64 b6, %2, 1536;\n"
-                 "add.s64 b7, %2, 1792;\n"
-                 "add.s64 b8, %2, 2048;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], b8, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<10>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7, b8, b9;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "add.s64 b6, %2, 1536;\n"
-                 "add.s64 b7, %2, 1792;\n"
-                 "add.s64 b8, %2, 2048;\n"
-                 "add.s64 b9, %2, 2304;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], b8, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], b9, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<11>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7, b8, b9, b10;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "add.s64 b6, %2, 1536;\n"
-                 "add.s64 b7, %2, 1792;\n"
-                 "add.s64 b8, %2, 2048;\n"
-                 "add.s64 b9, %2, 2304;\n"
-                 "add.s64 b10, %2, 2560;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], b8, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], b9, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+80], b10, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
-template <>
-__device__ __forceinline__ void mma_tile_block<12>(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
-    asm volatile("{\n.reg .pred e;\n.reg .b64 b1, b2, b3, b4, b5, b6, b7, b8, b9, b10, b11;\nelect.sync _|e, 0xffffffff;\n"
-                 "add.s64 b1, %2, 256;\n"
-                 "add.s64 b2, %2, 512;\n"
-                 "add.s64 b3, %2, 768;\n"
-                 "add.s64 b4, %2, 1024;\n"
-                 "add.s64 b5, %2, 1280;\n"
-                 "add.s64 b6, %2, 1536;\n"
-                 "add.s64 b7, %2, 1792;\n"
-                 "add.s64 b8, %2, 2048;\n"
-                 "add.s64 b9, %2, 2304;\n"
-                 "add.s64 b10, %2, 2560;\n"
-                 "add.s64 b11, %2, 2816;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+0], %2, %3, 0;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+8], b1, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+16], b2, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+24], b3, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+32], b4, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+40], b5, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+48], b6, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+56], b7, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+64], b8, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+72], b9, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+80], b10, %3, 1;\n"
-                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1+88], b11, %3, 1;\n"
-                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n}\n"
-                 ::"r"(acc), "r"(aT), "l"(bd), "r"(idesc), "r"(bar) : "memory");
-}
-
 // One MMA (K = 16): D (+)= A[aT] x B[bd]; `acc` nonzero accumulates into D.
 __device__ __forceinline__ void umma_f16(uint32_t d, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t acc) {
     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -312,6 +75,20 @@ template <int Q, int R>
 __device__ __forceinline__ void mma_split_block(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
     if (elect_one()) {
         mma_split_seq<Q, R>(acc, aT, bd, idesc, 0u);
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                     : "memory");
+    }
+    __syncwarp();
+}
+
+// One (point tile, direction block) product with NS consecutive K steps paired
+// one to one (contract_tcf.cu's single-product layout): MMA i reads A step i
+// and B step i, the first overwrites the accumulator; then the commit.
+template <int NS>
+__device__ __forceinline__ void mma_tile_block(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, uint32_t bar) {
+    if (elect_one()) {
+#pragma unroll
+        for (int i = 0; i < NS; ++i) umma_f16(acc, aT + 8u * i, bd + 256ull * i, idesc, i > 0 ? 1u : 0u);
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                      : "memory");
     }
