@@ -72,7 +72,8 @@ int rrs_engine_destroy(rrs_engine* e);
 /* Run on a caller stream (cudaStream_t as void*); NULL restores the engine's own. */
 int rrs_engine_set_stream(rrs_engine* e, void* stream);
 int rrs_engine_synchronize(rrs_engine* e);
-/* Cap on workspace bytes used for query batching (default 8 GiB). */
+/* Cap on workspace bytes used for query batching (default: a quarter of the
+ * device's free memory at engine creation, clamped to [1, 32] GiB). */
 int rrs_engine_set_workspace_limit(rrs_engine* e, int64_t bytes);
 
 /* Dataset(rows) -- projection.py:44-75.  x is n x d row-major FP64, finite;

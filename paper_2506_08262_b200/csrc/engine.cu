@@ -740,6 +740,18 @@ int rrs_engine_create(int32_t device, rrs_engine** out) {
         return fail(RRS_ERR_CUDA, std::string("stream create: ") + cudaGetErrorString(ce));
     }
     e->stream = e->own;
+    // query-batching workspace: a quarter of the free HBM, between 1 and 32 GiB
+    // (32 GiB on an idle B200: fewer, larger store / select launches for the
+    // projection notions; rrs_engine_set_workspace_limit overrides it)
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+        int64_t ws = (int64_t)(free_b / 4);
+        if (ws > (32ll << 30)) ws = 32ll << 30;
+        if (ws < (1ll << 30)) ws = 1ll << 30;
+        e->ws_limit = ws;
+    } else {
+        cudaGetLastError();
+    }
     *out = e;
     return RRS_OK;
 }
