@@ -18,11 +18,14 @@ cases = [
     # (n, d, notion, contract path, select path)
     (4100, 50, "halfspace", "tensor", "auto"),     # contract_tc + cap_generate_v2 + update
     (4100, 50, "halfspace", "filter", "auto"),     # contract_tcf
-    (4100, 80, "halfspace", "tensor", "auto"),     # contract_tcw
+    (4100, 80, "halfspace", "tensor", "auto"),     # contract_tcp (pre-split) + presplit + coincide_list32
+    (4100, 80, "halfspace", "convert", "auto"),    # contract_tcw (in-kernel converters)
+    (4100, 200, "halfspace", "tensor", "auto"),    # contract_tcp, four slices, one accumulator pair
     (1000, 5, "halfspace", "ffma", "auto"),        # contract_kernel<count>
     (1000, 300, "halfspace", "auto", "auto"),      # d > 256: contract64 count
     (5000, 300, "projection", "auto", "auto"),     # d > 256: contract64 store
-    (5000, 80, "asym_projection", "auto", "auto"),  # contract_tcw STORE (centred, 64 < d <= 256)
+    (5000, 80, "asym_projection", "auto", "auto"),  # contract_tcp STORE (centred pre-split, 64 < d <= 256)
+    (5000, 80, "projection", "convert", "auto"),    # contract_tcw STORE
     (5000, 40, "projection", "tensor", "auto"),    # contract_tcs + select v3<256>
     (20000, 20, "asym_projection", "ffma", "auto"),  # contract_kernel<store> + select v3<512>
     (20000, 20, "projection", "ffma", "wide"),     # select v3<1024>
