@@ -26,12 +26,14 @@ cases = [
     (5000, 300, "projection", "auto", "auto"),     # d > 256: contract64 store
     (5000, 80, "asym_projection", "auto", "auto"),  # contract_tcp STORE (centred pre-split, 64 < d <= 256)
     (5000, 80, "projection", "convert", "auto"),    # contract_tcw STORE
-    (5000, 40, "projection", "tensor", "auto"),    # contract_tcs + select v3<256>
+    (5000, 40, "projection", "tensor", "auto"),    # contract_tc STORE + select v3<256>
+    (5000, 40, "asym_projection", "tensor3", "auto"),  # contract_tcs (three-term store)
     (20000, 20, "asym_projection", "ffma", "auto"),  # contract_kernel<store> + select v3<512>
     (20000, 20, "projection", "ffma", "wide"),     # select v3<1024>
     (5000, 20, "projection", "ffma", "radix"),     # select v2<256, smem>
-    (60000, 7, "projection", "ffma", "auto"),      # select v2<1024, global>
-    (60001, 7, "asym_projection", "ffma", "auto"),  # select_kernel (legacy, unaligned rows)
+    (60000, 7, "projection", "ffma", "auto"),      # select v5 (rows past shared memory)
+    (60000, 7, "projection", "ffma", "radix"),     # select v2<1024, global>
+    (60001, 7, "asym_projection", "ffma", "radix"),  # select_kernel (legacy, unaligned rows)
     (500, 30, "projection", "auto", "auto"),       # store64 (FP64 centred store)
 ]
 for n, d, notion, path, sel in cases:
