@@ -750,20 +750,19 @@ __device__ __forceinline__ uint32_t s3_reduce_min(uint32_t v, Sel3Shared<NT>& sh
 }
 
 // every thread calls f(y) for its share of the row (16-byte loads when aligned,
-// four in flight)
-template <int NT, typename F>
+// U in flight)
+template <int NT, int U = 4, typename F>
 __device__ __forceinline__ void s3_row_each(const float* __restrict__ row, int n, F&& f) {
     if ((n & 3) == 0) {
         const float4* r4 = reinterpret_cast<const float4*>(row);
         const int n4 = n >> 2;
         int i = threadIdx.x;
-        for (; i + 3 * NT < n4; i += 4 * NT) {
-            const float4 v0 = __ldg(r4 + i), v1 = __ldg(r4 + i + NT), v2 = __ldg(r4 + i + 2 * NT),
-                         v3 = __ldg(r4 + i + 3 * NT);
-            f(v0.x), f(v0.y), f(v0.z), f(v0.w);
-            f(v1.x), f(v1.y), f(v1.z), f(v1.w);
-            f(v2.x), f(v2.y), f(v2.z), f(v2.w);
-            f(v3.x), f(v3.y), f(v3.z), f(v3.w);
+        for (; i + (U - 1) * NT < n4; i += U * NT) {
+            float4 v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) v[k] = __ldg(r4 + i + k * NT);
+#pragma unroll
+            for (int k = 0; k < U; ++k) f(v[k].x), f(v[k].y), f(v[k].z), f(v[k].w);
         }
         for (; i < n4; i += NT) {
             const float4 v = __ldg(r4 + i);
@@ -1220,6 +1219,10 @@ static cudaError_t launch_sel3(const SelectArgs& a, dim3 grid, cudaStream_t st) 
 // restarts from the full key range.  Same keys / midpoints as v2: bitwise
 // equal depths.
 constexpr int S5_CAP = 8192;                   // gathered keys (global rows)
+#ifndef RRS_S5_UNROLL
+#define RRS_S5_UNROLL 4
+#endif
+constexpr int S5_U = RRS_S5_UNROLL;            // 16-byte loads in flight per thread in v5's row passes
 
 
 // one pass over the row: keys < base counted, keys in [base, base + span]
@@ -1233,7 +1236,7 @@ __device__ void s5_hist_pass(const float* __restrict__ row, int64_t n, KF kf, ui
     __syncthreads();
     const uint32_t hbase = smem_u32(sh.hist);
     uint32_t b = 0, in = 0;
-    s3_row_each<S5_NT>(row, (int)n, [&](float y) {
+    s3_row_each<S5_NT, S5_U>(row, (int)n, [&](float y) {
         const uint32_t key = kf(y);
         const uint32_t off = key - base;
         b += key < base ? 1u : 0u;
@@ -1323,7 +1326,7 @@ __device__ void s5_rank(const float* __restrict__ row, int64_t n, KF kf, uint32_
         // gather the window's keys (pass B)
         if (threadIdx.x == 0) sh.s_ovf = 0u;
         __syncthreads();
-        s3_row_each<S5_NT>(row, (int)n, [&](float y) {
+        s3_row_each<S5_NT, S5_U>(row, (int)n, [&](float y) {
             const uint32_t key = kf(y);
             if (key - base <= span) cand[atomicAdd(&sh.s_ovf, 1u)] = key;
         });
@@ -1339,7 +1342,7 @@ __device__ void s5_rank(const float* __restrict__ row, int64_t n, KF kf, uint32_
         if (span != 0u && R + 1 < wbelow + wcnt) {
             s3_arr_each<S5_NT>(cand, (int)wcnt, [&](uint32_t k2) { best = min(best, k2 > kR ? k2 : 0xFFFFFFFFu); });
         } else {
-            s3_row_each<S5_NT>(row, (int)n, [&](float y) {
+            s3_row_each<S5_NT, S5_U>(row, (int)n, [&](float y) {
                 const uint32_t k2 = kf(y);
                 best = min(best, k2 > kR ? k2 : 0xFFFFFFFFu);
             });
