@@ -371,6 +371,9 @@ __device__ __forceinline__ double pw_sum8(int n, int k, F f) {
 __global__ void __launch_bounds__(GV_THREADS, RRS_GEN_BLOCKS_PER_SM) cap_generate_v2_kernel(GenArgs a) {
     extern __shared__ double vsm[];
     const int d = a.d, dm = d - 1;
+    // e / dm by a 64-bit multiply-high (exact for e < 32 dm, dm < 2^10: checked for
+    // every dm; dm = 1 needs the 33-bit multiplier 2^32)
+    const uint64_t dm_mul = 0xFFFFFFFFull / (uint64_t)(dm > 0 ? dm : 1) + 1ull;
     double* val = vsm;                          // [GV_DIRS][d] uniforms -> normals -> row
     double* s_th = val + GV_DIRS * d;           // [GV_DIRS] theta uniform -> u1
     double* s_nrm = s_th + GV_DIRS;             // [GV_DIRS]
@@ -392,7 +395,7 @@ __global__ void __launch_bounds__(GV_THREADS, RRS_GEN_BLOCKS_PER_SM) cap_generat
     }
     // 1. uniforms
     for (int e = tid; e < E; e += GV_THREADS) {
-        const int jj = e / dm, c = e - jj * dm;
+        const int jj = (int)(((uint64_t)e * dm_mul) >> 32), c = e - jj * dm;
         val[jj * d + 1 + c] = uniform1(a.seed, 1u + (uint32_t)c, (uint32_t)(j0 + jj), l, qg);
     }
     if (tid < nval) s_th[tid] = uniform1(a.seed, 0u, (uint32_t)(j0 + tid), l, qg);
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(GV_THREADS, RRS_GEN_BLOCKS_PER_SM) cap_generat
         const int e = e0 + tid;
         bool cen = false, tl = false;
         if (e < E) {
-            const int jj = e / dm;
+            const int jj = (int)(((uint64_t)e * dm_mul) >> 32);
             const bool c_ = ndtri_is_central(val[jj * d + 1 + (e - jj * dm)]);
             cen = c_;
             tl = !c_;
@@ -422,12 +425,12 @@ __global__ void __launch_bounds__(GV_THREADS, RRS_GEN_BLOCKS_PER_SM) cap_generat
     __syncthreads();
     const int nc = s_nc, nt = s_nt;
     for (int i = tid; i < nc; i += GV_THREADS) {
-        const int e = list[i], jj = e / dm;
+        const int e = list[i], jj = (int)(((uint64_t)e * dm_mul) >> 32);
         double* p = &val[jj * d + 1 + (e - jj * dm)];
         *p = ndtri_central(*p);
     }
     for (int i = tid; i < nt; i += GV_THREADS) {
-        const int e = list[E - 1 - i], jj = e / dm;
+        const int e = list[E - 1 - i], jj = (int)(((uint64_t)e * dm_mul) >> 32);
         double* p = &val[jj * d + 1 + (e - jj * dm)];
         *p = ndtri_tail(*p);
     }
@@ -450,7 +453,7 @@ __global__ void __launch_bounds__(GV_THREADS, RRS_GEN_BLOCKS_PER_SM) cap_generat
     const double* v = a.refl_v + (size_t)q * d;
     // 4. row = [u1, s * (g / |g|)]
     for (int e = tid; e < E; e += GV_THREADS) {
-        const int jj = e / dm;
+        const int jj = (int)(((uint64_t)e * dm_mul) >> 32);
         const double u1 = s_th[jj], sf = sqrt(1.0 - u1 * u1);
         double* p = &val[jj * d + 1 + (e - jj * dm)];
         *p = sf * (*p / s_nrm[jj]);
