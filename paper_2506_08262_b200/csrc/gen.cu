@@ -373,12 +373,13 @@ __global__ void __launch_bounds__(GV_THREADS, RRS_GEN_BLOCKS_PER_SM) cap_generat
     const int d = a.d, dm = d - 1;
     // e / dm by a 64-bit multiply-high (exact for e < 32 dm, dm < 2^10: checked for
     // every dm; dm = 1 needs the 33-bit multiplier 2^32)
-    const uint64_t dm_mul = 0xFFFFFFFFull / (uint64_t)(dm > 0 ? dm : 1) + 1ull;
+    const uint64_t dm_mul = (uint64_t)(0xFFFFFFFFu / (uint32_t)(dm > 0 ? dm : 1)) + 1ull;
     double* val = vsm;                          // [GV_DIRS][d] uniforms -> normals -> row
     double* s_th = val + GV_DIRS * d;           // [GV_DIRS] theta uniform -> u1
     double* s_nrm = s_th + GV_DIRS;             // [GV_DIRS]
     uint16_t* list = reinterpret_cast<uint16_t*>(s_nrm + GV_DIRS);  // [GV_DIRS * dm]
     __shared__ int s_nc, s_nt, s_zero;
+    __shared__ double s_sf[GV_DIRS];            // sqrt(1 - u1^2) per direction
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t gdir0 = (int64_t)blockIdx.x * GV_DIRS;
     const int q = (int)(gdir0 / a.mpad);
@@ -444,7 +445,9 @@ __global__ void __launch_bounds__(GV_THREADS, RRS_GEN_BLOCKS_PER_SM) cap_generat
         const double nrm = sqrt(pw_sum8(dm, k, [&](int i) { return live ? g[i] * g[i] : 0.0; }));
         if (k == 0 && jj < nval) {
             s_nrm[jj] = nrm;
-            s_th[jj] = cos(s_th[jj] * a.eps);  // u1 = cos(theta)
+            const double u1 = cos(s_th[jj] * a.eps);  // u1 = cos(theta)
+            s_th[jj] = u1;
+            s_sf[jj] = sqrt(1.0 - u1 * u1);
             if (nrm == 0.0) s_zero = 1;
         }
     }
@@ -454,9 +457,8 @@ __global__ void __launch_bounds__(GV_THREADS, RRS_GEN_BLOCKS_PER_SM) cap_generat
     // 4. row = [u1, s * (g / |g|)]
     for (int e = tid; e < E; e += GV_THREADS) {
         const int jj = (int)(((uint64_t)e * dm_mul) >> 32);
-        const double u1 = s_th[jj], sf = sqrt(1.0 - u1 * u1);
         double* p = &val[jj * d + 1 + (e - jj * dm)];
-        *p = sf * (*p / s_nrm[jj]);
+        *p = s_sf[jj] * (*p / s_nrm[jj]);
     }
     if (tid < nval) val[tid * d] = (mode == 1) ? -s_th[tid] : s_th[tid];
     __syncthreads();
