@@ -476,6 +476,13 @@ def main():
                     "achieved_is": "algorithmic bytes (the stored projections, 4 n per direction) / select time",
                     "kernel_share_of_step": select_ms / stage_ms if stage_ms else None,
                     "contraction": roofline}
+        # the store writes y once (4 n bytes per live direction): against the B200's
+        # write-only bandwidth (3.91 TB/s, torch zero_ of 8 GiB, scripts/hbm_write_bw.py)
+        y_bytes = 4.0 * n * m * r * B * args.steps
+        roofline["contraction"]["y_write"] = {
+            "achieved_gbs": y_bytes / (contract_ms / 1e3) / 1e9 if contract_ms else None,
+            "write_peak_gbs": 3911.7, "peak_source": "measured write-only bandwidth, scripts/hbm_write_bw.py",
+            "frac": (y_bytes / (contract_ms / 1e3) / 1e9) / 3911.7 if contract_ms else None}
 
     # e2e through the public API with host buffers (H2D of data + queries, D2H of results)
     e2e = None
