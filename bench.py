@@ -469,7 +469,7 @@ def main():
                     "kernel": ("select_v2_kernel<256|512|1024, smem>" if args.select_path == "radix"
                                else "select_v3_kernel<256>" if n <= 16384
                                else "select_v3_kernel<512|1024>") if 2048 <= n <= 53248
-                    else ("select_v5_kernel<1024, 8192>" if args.select_path != "radix" else
+                    else ("select_v5_kernel<512, 8192>" if args.select_path != "radix" else
                           "select_v2_kernel<1024, global>") if n > 53248 and n % 4 == 0
                     else "select_v2_kernel<smem>" if n < 2048 else "select_kernel",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks.get("hbm_gbs") else "nominal 8 TB/s",

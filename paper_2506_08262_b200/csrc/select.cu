@@ -699,11 +699,17 @@ __global__ void __launch_bounds__(NT) select_v2_kernel(const SelectArgs a) {
 // deviations), so v2 and v3 give bitwise equal depths.
 // sample size: one warp sorts it (8 / 16 keys per lane); the larger sample of
 // the 1024-thread variant narrows the bracket so 1024 threads' slots rarely overflow
+#ifndef RRS_S3_MINB256
+#define RRS_S3_MINB256 5
+#endif
+#ifndef RRS_S3_MINB512
+#define RRS_S3_MINB512 3  // config 3: 274 -> 284 q/s over 2
+#endif
 template <int NT>
 struct Sel3Cfg {
     static constexpr int S = NT >= 512 ? 512 : 256;
     static constexpr double SIGMAS = NT >= 1024 ? 5.0 : 4.0;  // slot headroom
-    static constexpr int MINB = NT >= 1024 ? 1 : NT >= 512 ? 2 : 5;  // CTAs per SM targeted
+    static constexpr int MINB = NT >= 1024 ? 1 : NT >= 512 ? RRS_S3_MINB512 : RRS_S3_MINB256;  // CTAs per SM targeted
 };
 constexpr int SMAX = 512;
 constexpr int64_t SEL3_MIN_N = 2048;
@@ -1351,8 +1357,17 @@ __device__ void s5_rank(const float* __restrict__ row, int64_t n, KF kf, uint32_
     }
 }
 
+// four 512-thread CTAs per SM at 32 registers (the spills sit in the per-row
+// serial phases): more rows in flight per SM -- config 5p 10.79 (one 1024-thread
+// CTA at 64 registers) -> 11.78 (two) -> 12.06 q/s (four 512-thread CTAs)
+#ifndef RRS_S5_NT
+#define RRS_S5_NT 512
+#endif
+#ifndef RRS_S5_MINB
+#define RRS_S5_MINB (2048 / RRS_S5_NT)
+#endif
 template <int S5_NT, int CAP>
-__global__ void __launch_bounds__(S5_NT) select_v5_kernel(const SelectArgs a) {
+__global__ void __launch_bounds__(S5_NT, RRS_S5_MINB) select_v5_kernel(const SelectArgs a) {
     extern __shared__ __align__(16) unsigned char sel5_raw[];
     Sel3Shared<S5_NT>& sh = *reinterpret_cast<Sel3Shared<S5_NT>*>(sel5_raw);
     uint32_t* cand = reinterpret_cast<uint32_t*>(sel5_raw + ((sizeof(Sel3Shared<S5_NT>) + 15) & ~size_t(15)));
@@ -1471,7 +1486,7 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
     }
     // rows past shared memory: the two-pass sample-bracket select (v5) unless
     // the radix select is asked for (variant 2)
-    if (a.variant != 2 && a.n < ((int64_t)1 << 31)) return launch_sel5<1024, S5_CAP>(a, grid, st);
+    if (a.variant != 2 && a.n < ((int64_t)1 << 31)) return launch_sel5<RRS_S5_NT, S5_CAP>(a, grid, st);
 #ifndef RRS_SEL_LEGACY_GLOBAL
     // (16-byte key loads: rows must start aligned, i.e. n % 4 == 0)
     if ((a.n & 3) == 0 && a.n < ((int64_t)1 << 31)) return launch_sel2<1024, true>(a, grid, st);
