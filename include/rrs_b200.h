@@ -99,6 +99,10 @@ int rrs_set_dataset_device(rrs_engine* e, const double* x_dev, int64_t n, int32_
 int rrs_depth_batch_host(rrs_engine* e, const double* queries, int64_t Q, int64_t q0,
                          const rrs_config* cfg, const double* eps, double* depth,
                          double* argmin, double* trace, int64_t* min_count);
+/* Device-resident variant: every pointer is device memory, the kernels run on
+ * the engine stream.  The queries are validated on the device (finite,
+ * |z| <= 1e38) and the flag is read back once the batch is enqueued, so the
+ * call returns after the batch completed; a bad query fails the call. */
 int rrs_depth_batch_device(rrs_engine* e, const double* queries_dev, int64_t Q, int64_t q0,
                            const rrs_config* cfg, const double* eps, double* depth_dev,
                            double* argmin_dev, double* trace_dev, int64_t* min_count_dev);

@@ -110,6 +110,7 @@ struct rrs_engine {
     int select_path = 0;  // 0 auto (select v3 where it applies), 2 radix select v2
     DevBuf fallbacks;     // device counter of select-v3 rows that left their bracket
     DevBuf tmp_in, tmp_out0, tmp_out1, tmp_out2, tmp_out3;
+    DevBuf qflag;  // device-query validation flag (rrs_depth_batch_device)
     // timing
     bool timing = false;
     rrs_stats stats{};
@@ -764,7 +765,7 @@ int rrs_engine_destroy(rrs_engine* e) {
                       &e->reflv, &e->reflmode, &e->dmin, &e->bestcnt, &e->tmp_in, &e->tmp_out0,
                       &e->tmp_out1, &e->tmp_out2, &e->tmp_out3, &e->center, &e->xcb, &e->xc64, &e->zq0,
                       &e->shift, &e->fallbacks, &e->x64, &e->done, &e->c0, &e->xcmax, &e->xps[0], &e->xps[1],
-                      &e->pinv[0], &e->pinv[1], &e->coin, &e->coin_n, &e->zero_d})
+                      &e->pinv[0], &e->pinv[1], &e->coin, &e->coin_n, &e->zero_d, &e->qflag})
         b->release();
     for (auto ev : e->ev_pool) cudaEventDestroy(ev);
     if (e->own) cudaStreamDestroy(e->own);
@@ -937,19 +938,21 @@ int rrs_depth_batch_device(rrs_engine* e, const double* queries_dev, int64_t Q, 
     if (Q == 0) return RRS_OK;
     if (!queries_dev || !depth_dev) return fail(RRS_ERR_INVALID, "null argument");
     if (int rc = set_device(e)) return rc;
-    {
-        CK(e->tmp_out0.ensure(16));
-        int* flag = e->tmp_out0.as<int>();
-        CK(cudaMemsetAsync(flag, 0, sizeof(int), e->stream));
-        CK(launch_validate_values(queries_dev, Q * (int64_t)e->d, flag, e->stream));
-        int h = 0;
-        CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
-        CK(cudaStreamSynchronize(e->stream));
-        if (h & 1) return fail(RRS_ERR_INVALID, "queries contain non-finite entries");
-        if (h & 2) return fail(RRS_ERR_INVALID, "queries exceed the FP32 contraction range (|z| > 1e38)");
-    }
+    // the queries are validated on the device; the flag is read back after the
+    // batch is enqueued (one synchronisation at the end of the call instead of a
+    // host round trip before the first kernel), and a bad query fails the call
+    CK(e->qflag.ensure(16));
+    int* flag = e->qflag.as<int>();
+    CK(cudaMemsetAsync(flag, 0, sizeof(int), e->stream));
+    CK(launch_validate_values(queries_dev, Q * (int64_t)e->d, flag, e->stream));
     reset_stats(e);
-    return run_batches(e, queries_dev, Q, q0, cfg, eps, depth_dev, argmin_dev, trace_dev, min_count_dev);
+    const int rc = run_batches(e, queries_dev, Q, q0, cfg, eps, depth_dev, argmin_dev, trace_dev, min_count_dev);
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    if (h & 1) return fail(RRS_ERR_INVALID, "queries contain non-finite entries");
+    if (h & 2) return fail(RRS_ERR_INVALID, "queries exceed the FP32 contraction range (|z| > 1e38)");
+    return rc;
 }
 
 int rrs_depth_batch_host(rrs_engine* e, const double* queries, int64_t Q, int64_t q0,
