@@ -426,7 +426,7 @@ def main():
             L_ns = 12 * full + 3 * (dl // 16) + (3 * (dl % 16) + 15) // 16  # MMAs per tile and block
             wide = "contract_tcw_kernel" if args.contract_path == "convert" else "contract_tcp_kernel"
             kname, nprod = ("contract_tc_kernel" if d <= 64 else wide), 3
-        elif d > 64 or store_split2(X):  # two-term split store (contract_tc / contract_tcp STORE)
+        elif args.contract_path != "tensor3" and (d > 64 or store_split2(X)):  # two-term split store
             full = (d - 1) // 64
             dl = d - 64 * full
             L_ns = 12 * full + 3 * (dl // 16) + (3 * (dl % 16) + 15) // 16

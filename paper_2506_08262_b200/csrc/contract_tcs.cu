@@ -83,15 +83,13 @@ __device__ __forceinline__ SUnit s_unit(const TcsArgs& a, int64_t u) {
     return r;
 }
 
+// ns MMAs of one (tile, block), K steps paired one to one; one elected thread
+// issues them all
 __device__ __forceinline__ void mma_block(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, int ns) {
-    for (int i = 0; i < ns; ++i) {
-        const uint32_t en = i == 0 ? 0u : 1u;
-        asm volatile(
-            "{\n.reg .pred e, p;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
-            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(acc),
-            "r"(aT + 8u * (uint32_t)i), "l"(bd + 256ull * (uint64_t)i), "r"(idesc), "r"(en)
-            : "memory");
+    if (elect_one()) {
+        for (int i = 0; i < ns; ++i) umma_f16(acc, aT + 8u * (uint32_t)i, bd + 256ull * (uint64_t)i, idesc, i ? 1u : 0u);
     }
+    __syncwarp();
 }
 
 // v = hi + mid + lo (FP16 each, exact residuals in FP32)
