@@ -26,7 +26,8 @@
 // Layout (M = 128 directions on TMEM lanes, N = 128 points, K = 16 per MMA):
 // one direction block per unit resident in TMEM (8 ns columns), two FP32
 // accumulators when 8 ns <= 256; per (tile, slice) one TMA of the slice's
-// pre-split bytes (32 KB for a full slice) into a 4-deep stage ring and
+// pre-split bytes (32 KB for a full slice, up to 36 KB for the last) into a
+// 4-deep stage ring and
 // 3 Q + R MMAs (kernels.h tc_mma_steps); the per-point inv_i (512 B per tile)
 // rides on the tile's first slice into an 8-deep ring read by the epilogue.
 // Warp roles: 0 direction-slice producer, 1 TMEM allocator + MMA issuer,
@@ -38,6 +39,10 @@
 #include "tc_common.cuh"
 
 #include <cuda_fp16.h>
+
+#ifndef RRS_FORCE_SINGLE_ACC
+#define RRS_FORCE_SINGLE_ACC 0
+#endif
 
 namespace rrs {
 
@@ -51,7 +56,7 @@ constexpr int P_MAXD = 256;
 constexpr int P_MD = 128;
 constexpr int P_NP = 128;
 constexpr int P_STAGES = 4;
-constexpr int P_STAGE = TC_SLICE_NS * 4096;  // one full slice of a tile: 32 KB
+constexpr int P_STAGE = TC_SLICE_NS_MAX * 4096;  // any slice of a tile (36 KB: a last slice may hold 9 steps)
 constexpr int P_DSTEPS = 4;                  // K steps of A per staging load
 constexpr int P_IRING = 8;                   // per-point inv ring (tiles)
 constexpr uint32_t P_TMEM_COLS = 512;
@@ -112,7 +117,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) contract_tcp_kernel(const TcArgs
     const int d = a.d;
     const TcLayout L = tc_layout(d);
     const int S = L.full + 1;
-    const bool dbl = 8 * L.ns <= 256;  // two accumulator buffers fit beside A
+    const bool dbl = 8 * L.ns <= 256 && !RRS_FORCE_SINGLE_ACC;  // two accumulator buffers fit beside A
     const uint32_t a_base = dbl ? 2 * P_ACC : P_ACC;
     const PSmem lay(STORE);
     unsigned char* sP = sm + lay.P;

@@ -34,6 +34,10 @@
 
 #include <cuda_fp16.h>
 
+#ifndef RRS_FORCE_SINGLE_ACC
+#define RRS_FORCE_SINGLE_ACC 0
+#endif
+
 namespace rrs {
 
 namespace {
@@ -56,7 +60,7 @@ constexpr int W_MD = 128;
 constexpr int W_NP = 128;
 constexpr int W_P_STAGES = 2;
 constexpr int W_R_MAX = 4;
-constexpr int W_STAGE = TC_SLICE_NS * 4096;  // one slice of a tile: 32 KB
+constexpr int W_STAGE = TC_SLICE_NS_MAX * 4096;  // any slice of a tile (36 KB: a last slice may hold 9 steps)
 #ifndef RRS_TCW_DSTEPS
 #define RRS_TCW_DSTEPS 4
 #endif
@@ -122,14 +126,16 @@ __device__ __forceinline__ int slice_ns(const TcLayout& L, int s) {
     return s < L.full ? TC_SLICE_NS : L.ns - TC_SLICE_NS * L.full;
 }
 
-// The nm MMAs (K = 16 each) of one slice with q aligned groups into the
-// accumulator, A / B K steps paired by kernels.h tc_mma_steps; the first one
-// overwrites it when `first` (the tile's first slice), the rest accumulate.
-__device__ __forceinline__ void mma_slice(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, int q, int nm,
+// The 3 q + r MMAs (K = 16 each) of one slice (q aligned groups, r remainder
+// steps) into the accumulator, A / B K steps paired by kernels.h
+// tc_mma_steps; the first one overwrites it when `first` (the tile's first
+// slice), the rest accumulate.  (q, r) = (4, 0) for a full slice; a last
+// slice of (3, 3) has as many MMAs as a full one but a different pairing.
+__device__ __forceinline__ void mma_slice(uint32_t acc, uint32_t aT, uint64_t bd, uint32_t idesc, int q, int r,
                                           bool first) {
     if (elect_one()) {
-        if (nm == TC_SLICE_MMA) mma_split_seq<4, 0>(acc, aT, bd, idesc, first ? 0u : 1u);
-        else mma_split_seq_rt(q, nm - 3 * q, acc, aT, bd, idesc, first ? 0u : 1u);
+        if (q == 4) mma_split_seq<4, 0>(acc, aT, bd, idesc, first ? 0u : 1u);
+        else mma_split_seq_rt(q, r, acc, aT, bd, idesc, first ? 0u : 1u);
     }
     __syncwarp();
 }
@@ -229,7 +235,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
     const int d = a.d;
     const TcLayout L = tc_layout(d);
     const int S = L.full + 1;                 // slices
-    const bool dbl = 8 * L.ns <= 256;         // two accumulator buffers fit beside A
+    const bool dbl = 8 * L.ns <= 256 && !RRS_FORCE_SINGLE_ACC;  // two accumulator buffers fit beside A
     const uint32_t a_base = dbl ? 2 * W_ACC : W_ACC;
     const WSmem lay(STORE);
     unsigned char* sP = sm + lay.P;
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) contract_tcw_kernel(const TcArgs
                     tc_fence_after();
                     mma_slice(tmem + buf * W_ACC, tmem + a_base + 8u * TC_SLICE_NS * s,
                               umma_desc(smem_u32(sP) + st * W_STAGE, 2048, 128), idesc, s < L.full ? 4 : L.q16,
-                              s < L.full ? TC_SLICE_MMA : 3 * L.q16 + L.rsteps, s == 0);
+                              s < L.full ? 0 : L.rsteps, s == 0);
                     mma_commit_elect(&pempty[st]);
                 }
                 mma_commit_elect(&tfull[buf]);

@@ -109,6 +109,7 @@ struct TcLayout {
 };
 constexpr int TC_SLICE = 64;
 constexpr int TC_SLICE_NS = 8;    // stored K steps of a full slice
+constexpr int TC_SLICE_NS_MAX = 9;  // of any slice: a last slice of 59..63 coordinates takes 2 * 3 + 3
 constexpr int TC_SLICE_MMA = 12;  // its MMAs
 __host__ __device__ inline TcLayout tc_layout(int d) {
     TcLayout L;

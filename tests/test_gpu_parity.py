@@ -302,7 +302,7 @@ def test_tier1_config4_scale_counts(b200, orc, dist):
           f"{slack} / 4000")
 
 
-@pytest.mark.parametrize("d", [1, 3, 16, 22, 27, 44, 50, 64])
+@pytest.mark.parametrize("d", [1, 3, 16, 22, 27, 44, 50, 59, 61, 64])
 def test_tensor_layout_dims(b200, d):
     """The packed split-product K layout (kernels.h tc_layout) for every shape of
     remainder: d % 16 = 0 (no tail step), 3 (one), 6 (two), 11/12 (three tail
@@ -323,10 +323,12 @@ def test_tensor_layout_dims(b200, d):
         assert np.all(np.abs(cle - rle) <= T) and np.all(np.abs(cge - rge) <= T), d
 
 
-@pytest.mark.parametrize("d", [65, 72, 100, 128, 129, 150, 200, 256])
+@pytest.mark.parametrize("d", [65, 72, 100, 123, 128, 129, 150, 187, 200, 253, 256])
 def test_tensor_wide_dims(b200, d):
     """The wide tensor path (64 < d <= 256: the pre-split contract_tcp.cu by
-    default, 64-coordinate slices, one or two accumulator buffers) against FP64
+    default, 64-coordinate slices, one or two accumulator buffers; d = 123 /
+    187 / 253: a last slice of 59..63 coordinates, 9 stored K steps and as many
+    MMAs as a full slice; d = 253: one accumulator) against FP64
     within the tie zone and against the FFMA kernel, with a near-duplicate
     query, an in-sample query (self tie) and heterogeneous coordinate scales;
     n not a multiple of the tile, m not of the block."""
@@ -348,7 +350,7 @@ def test_tensor_wide_dims(b200, d):
         assert np.all(np.abs(cle - fle) <= T) and np.all(np.abs(cge - fge) <= T), d
 
 
-@pytest.mark.parametrize("d", [80, 200])
+@pytest.mark.parametrize("d", [80, 200, 253])
 def test_presplit_vs_converter(b200, d):
     """The pre-split wide kernel (contract_tcp.cu: query applied in the epilogue
     as y = acc inv_i + <u, -z>, coinciding rows excluded by index) against FP64
@@ -488,7 +490,8 @@ def test_dataset_validation_on_device(b200):
 @pytest.mark.parametrize("notion", ["projection", "asym_projection"])
 @pytest.mark.parametrize("shape", [(10_000, 20, "gaussian"), (50_000, 50, "cauchy"), (53_248, 7, "cauchy"),
                                    (4_097, 33, "gaussian"), (60_001, 48, "cauchy"), (30_000, 90, "cauchy"),
-                                   (20_000, 256, "gaussian"), (12_000, 64, "cauchy")])
+                                   (20_000, 256, "gaussian"), (12_000, 64, "cauchy"), (9_000, 253, "gaussian"),
+                                   (6_000, 123, "gaussian")])
 def test_tensor_store_projection_depths(b200, notion, shape, store):
     """The tensor-core projection stores of the centred frame: "tensor" = the
     two-term FP16 split (contract_tc.cu STORE for d <= 64, the pre-split
