@@ -350,6 +350,34 @@ def test_tensor_wide_dims(b200, d):
         assert np.all(np.abs(cle - fle) <= T) and np.all(np.abs(cge - fge) <= T), d
 
 
+def test_tensor_dims_sweep(b200):
+    """Every tensor-path K layout shape in one sweep: d = 1 .. 256 (every
+    remainder of the last 64-coordinate slice, 1 to 4 slices, one and two
+    accumulators), halfspace counts of the tensor path (contract_tc /
+    contract_tcp) and the converter path (contract_tcw) against FP64 within
+    the tie zone, an in-sample and an off-sample query."""
+    rng = np.random.default_rng(77)
+    Xall = rng.standard_normal((4096 + 45, 256))
+    Uall = rng.standard_normal((72, 256))
+    bad = []
+    dims = sorted(set(list(range(1, 257, 5)) + [59, 61, 63, 64, 65, 123, 127, 128, 187, 191, 192, 251, 255, 256]))
+    for d in dims:
+        X = np.ascontiguousarray(Xall[:, :d])
+        U = Uall[:, :d] / np.linalg.norm(Uall[:, :d], axis=1)[:, None]
+        data = b200.Dataset(X)
+        xn = np.linalg.norm(X, axis=1)
+        for z in (X[11], 0.5 * X[2] + 0.3):
+            y = X @ U.T - (U @ z)[None, :]
+            T = (np.abs(y) < TIE_REL * np.maximum(xn, np.linalg.norm(z))[:, None]).sum(axis=0)
+            rle, rge = (y <= 0).sum(axis=0), (y >= 0).sum(axis=0)
+            for path in (("tensor", "convert") if d > 64 else ("tensor",)):
+                with contract_path(b200, path):
+                    _, cle, cge = b200.evaluate_directions_counts(z, data, U)
+                if not (np.all(np.abs(cle - rle) <= T) and np.all(np.abs(cge - rge) <= T)):
+                    bad.append((d, path))
+    assert not bad, bad
+
+
 @pytest.mark.parametrize("d", [80, 200, 253])
 def test_presplit_vs_converter(b200, d):
     """The pre-split wide kernel (contract_tcp.cu: query applied in the epilogue
@@ -491,7 +519,7 @@ def test_dataset_validation_on_device(b200):
 @pytest.mark.parametrize("shape", [(10_000, 20, "gaussian"), (50_000, 50, "cauchy"), (53_248, 7, "cauchy"),
                                    (4_097, 33, "gaussian"), (60_001, 48, "cauchy"), (30_000, 90, "cauchy"),
                                    (20_000, 256, "gaussian"), (12_000, 64, "cauchy"), (9_000, 253, "gaussian"),
-                                   (6_000, 123, "gaussian")])
+                                   (6_000, 123, "gaussian"), (8_000, 61, "gaussian")])
 def test_tensor_store_projection_depths(b200, notion, shape, store):
     """The tensor-core projection stores of the centred frame: "tensor" = the
     two-term FP16 split (contract_tc.cu STORE for d <= 64, the pre-split
