@@ -378,6 +378,32 @@ def test_tensor_dims_sweep(b200):
     assert not bad, bad
 
 
+def test_tensor_store_dims_sweep(b200):
+    """The tensor projection stores over every K layout shape (contract_tc
+    STORE for d <= 64, contract_tcp STORE above; d = 1 .. 256 in steps of 9
+    plus the 9-step last slices): D_P / D_AP per direction against the FP64
+    oracle to 1e-5 relative."""
+    from oracle import oracle
+
+    rng = np.random.default_rng(78)
+    Xall = rng.standard_normal((4096 + 61, 256))
+    Uall = rng.standard_normal((24, 256))
+    bad = []
+    dims = sorted(set(list(range(2, 257, 9)) + [59, 61, 63, 123, 187, 251, 255]))
+    for d in dims:
+        X = np.ascontiguousarray(Xall[:, :d])
+        U = Uall[:, :d] / np.linalg.norm(Uall[:, :d], axis=1)[:, None]
+        data = b200.Dataset(X)
+        z = 0.4 * X[5] + 0.1
+        for notion in ("projection", "asym_projection"):
+            with contract_path(b200, "tensor"):
+                got = b200.evaluate_directions(z, data, U, notion, b200.ParallelConfig(workers=1))
+            ref = oracle.evaluate_directions(z, X, U, notion)
+            if not np.allclose(got, ref, rtol=DEPTH_RTOL, atol=0):
+                bad.append((d, notion, float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300)))))
+    assert not bad, bad
+
+
 @pytest.mark.parametrize("d", [80, 200, 253])
 def test_presplit_vs_converter(b200, d):
     """The pre-split wide kernel (contract_tcp.cu: query applied in the epilogue
