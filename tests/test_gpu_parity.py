@@ -378,6 +378,33 @@ def test_tensor_dims_sweep(b200):
     assert not bad, bad
 
 
+def test_ffma_dims_sweep(b200):
+    """The FP32 FFMA kernels over d = 1 .. 256 (contract.cu: the halfspace
+    count below n = 4096 and the forced FFMA projection store): counts within
+    the tie zone of FP64 and D_P depths against the oracle to 1e-5."""
+    from oracle import oracle
+
+    rng = np.random.default_rng(79)
+    Xall = rng.standard_normal((3000, 256))
+    Uall = rng.standard_normal((40, 256))
+    bad = []
+    for d in sorted(set(list(range(1, 257, 7)) + [63, 64, 65, 128, 129, 255, 256])):
+        X = np.ascontiguousarray(Xall[:, :d])
+        U = Uall[:, :d] / np.linalg.norm(Uall[:, :d], axis=1)[:, None]
+        data = b200.Dataset(X)
+        z = 0.5 * X[9] + 0.05
+        y = X @ U.T - (U @ z)[None, :]
+        T = (np.abs(y) < TIE_REL * np.maximum(np.linalg.norm(X, axis=1), np.linalg.norm(z))[:, None]).sum(axis=0)
+        with contract_path(b200, "ffma"):
+            _, cle, cge = b200.evaluate_directions_counts(z, data, U)
+            got = b200.evaluate_directions(z, data, U, "projection", b200.ParallelConfig(workers=1))
+        if not (np.all(np.abs(cle - (y <= 0).sum(axis=0)) <= T) and np.all(np.abs(cge - (y >= 0).sum(axis=0)) <= T)):
+            bad.append((d, "counts"))
+        if not np.allclose(got, oracle.evaluate_directions(z, X, U, "projection"), rtol=DEPTH_RTOL, atol=0):
+            bad.append((d, "projection"))
+    assert not bad, bad
+
+
 def test_tensor_store_dims_sweep(b200):
     """The tensor projection stores over every K layout shape (contract_tc
     STORE for d <= 64, contract_tcp STORE above; d = 1 .. 256 in steps of 9
