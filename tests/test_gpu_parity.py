@@ -407,9 +407,10 @@ def test_ffma_dims_sweep(b200):
 
 def test_tensor_store_dims_sweep(b200):
     """The tensor projection stores over every K layout shape (contract_tc
-    STORE for d <= 64, contract_tcp STORE above; d = 1 .. 256 in steps of 9
-    plus the 9-step last slices): D_P / D_AP per direction against the FP64
-    oracle to 1e-5 relative."""
+    STORE for d <= 64, contract_tcp STORE above, and the three-term
+    contract_tcs for d <= 50; d = 2 .. 256 in steps of 9 plus the 9-step last
+    slices): D_P / D_AP per direction against the FP64 oracle to 1e-5
+    relative."""
     from oracle import oracle
 
     rng = np.random.default_rng(78)
@@ -423,11 +424,12 @@ def test_tensor_store_dims_sweep(b200):
         data = b200.Dataset(X)
         z = 0.4 * X[5] + 0.1
         for notion in ("projection", "asym_projection"):
-            with contract_path(b200, "tensor"):
-                got = b200.evaluate_directions(z, data, U, notion, b200.ParallelConfig(workers=1))
             ref = oracle.evaluate_directions(z, X, U, notion)
-            if not np.allclose(got, ref, rtol=DEPTH_RTOL, atol=0):
-                bad.append((d, notion, float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300)))))
+            for path in (("tensor", "tensor3") if d <= 50 else ("tensor",)):
+                with contract_path(b200, path):
+                    got = b200.evaluate_directions(z, data, U, notion, b200.ParallelConfig(workers=1))
+                if not np.allclose(got, ref, rtol=DEPTH_RTOL, atol=0):
+                    bad.append((d, notion, path, float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300)))))
     assert not bad, bad
 
 
