@@ -433,6 +433,32 @@ def test_tensor_store_dims_sweep(b200):
     assert not bad, bad
 
 
+@pytest.mark.parametrize("d", [50, 120])
+def test_halfspace_query_batches_bitwise(b200, d):
+    """A workspace that holds only a few queries splits a depth_batch into
+    several engine batches (per batch: the coinciding-row lists, the state,
+    the refinements): depths, argmins and counts bitwise equal to one batch,
+    with and without the early exit (tensor paths: contract_tc / the pre-split
+    contract_tcp)."""
+    from paper_2506_08262_b200.synthetic import toeplitz_gaussian
+
+    X = toeplitz_gaussian(d, 6000, seed=4)
+    Z = np.vstack([X[:20], 0.5 * X[20:37]])
+    data = b200.Dataset(X)
+    eng = b200.engine()
+    for early in (False, True):
+        cfg = b200.RrsConfig(total_directions=1200, refinements=4, shrink=0.8, notion="halfspace", seed=2,
+                             early_exit=early)
+        one = b200.depth_batch_arrays(Z, data, cfg)
+        eng.set_workspace_limit(4 << 20)
+        try:
+            many = b200.depth_batch_arrays(Z, data, cfg)
+        finally:
+            eng.set_workspace_limit(8 << 30)
+        for a_, b_ in zip(one, many):
+            assert np.array_equal(a_, b_)
+
+
 @pytest.mark.parametrize("d", [80, 200, 253])
 def test_presplit_vs_converter(b200, d):
     """The pre-split wide kernel (contract_tcp.cu: query applied in the epilogue
