@@ -378,6 +378,34 @@ def test_tensor_dims_sweep(b200):
     assert not bad, bad
 
 
+def test_tensor_tile_padding_sweep(b200):
+    """Point counts around the 128-point tile and the 4096-point auto switch
+    (padding rows excluded from every count, the last tile partly filled):
+    tensor-path halfspace counts within the tie zone of FP64 at d = 50
+    (contract_tc) and d = 120 (contract_tcp, contract_tcw), in- and
+    off-sample queries."""
+    rng = np.random.default_rng(80)
+    Xall = rng.standard_normal((4400, 120))
+    Uall = rng.standard_normal((40, 120))
+    bad = []
+    for n in (4096, 4097, 4223, 4224, 4225, 4351, 4352):
+        for d in (50, 120):
+            X = np.ascontiguousarray(Xall[:n, :d])
+            U = Uall[:, :d] / np.linalg.norm(Uall[:, :d], axis=1)[:, None]
+            data = b200.Dataset(X)
+            xn = np.linalg.norm(X, axis=1)
+            for z in (X[n - 1], 0.3 * X[0] - 0.2):
+                y = X @ U.T - (U @ z)[None, :]
+                T = (np.abs(y) < TIE_REL * np.maximum(xn, np.linalg.norm(z))[:, None]).sum(axis=0)
+                for path in ("tensor", "convert") if d > 64 else ("tensor",):
+                    with contract_path(b200, path):
+                        _, cle, cge = b200.evaluate_directions_counts(z, data, U)
+                    if not (np.all(np.abs(cle - (y <= 0).sum(axis=0)) <= T)
+                            and np.all(np.abs(cge - (y >= 0).sum(axis=0)) <= T)):
+                        bad.append((n, d, path))
+    assert not bad, bad
+
+
 def test_ffma_dims_sweep(b200):
     """The FP32 FFMA kernels over d = 1 .. 256 (contract.cu: the halfspace
     count below n = 4096 and the forced FFMA projection store): counts within
