@@ -406,6 +406,30 @@ def test_tensor_tile_padding_sweep(b200):
     assert not bad, bad
 
 
+def test_projection_rowlength_sweep(b200):
+    """D_P / D_AP across the row lengths where the kernels switch (the FP64
+    store below n = 4096, the tensor store above; select v2 below 2048, v3 with
+    256 / 512 threads, v5 past 53248), auto paths, against the FP64 oracle to
+    1e-5 relative."""
+    from oracle import oracle
+
+    rng = np.random.default_rng(81)
+    Xall = rng.standard_normal((60_001, 20))
+    U = rng.standard_normal((12, 20))
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    bad = []
+    for n in (2047, 2048, 4095, 4096, 16384, 16385, 53248, 53249, 60_001):
+        X = np.ascontiguousarray(Xall[:n])
+        data = b200.Dataset(X)
+        z = 0.2 * X[1] + 0.05
+        for notion in ("projection", "asym_projection"):
+            got = b200.evaluate_directions(z, data, U, notion, b200.ParallelConfig(workers=1))
+            ref = oracle.evaluate_directions(z, X, U, notion)
+            if not np.allclose(got, ref, rtol=DEPTH_RTOL, atol=0):
+                bad.append((n, notion))
+    assert not bad, bad
+
+
 def test_ffma_dims_sweep(b200):
     """The FP32 FFMA kernels over d = 1 .. 256 (contract.cu: the halfspace
     count below n = 4096 and the forced FFMA projection store): counts within
